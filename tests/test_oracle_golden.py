@@ -1,0 +1,81 @@
+"""Pin the CPU oracle against fixtures recorded from the reference itself."""
+
+import numpy as np
+import pytest
+
+from oracle import skel_oracle as O
+from paper_2001_11619_b200 import configs
+
+
+def _boxes(g, prefix):
+    keys = [tuple(k) for k in g[prefix + "keys"]]
+    so, S = g[prefix + "S_off"], g[prefix + "S"]
+    ao, act = g[prefix + "act_off"], g[prefix + "act"]
+    fo, far = g[prefix + "far_off"], g[prefix + "far"]
+    out = {}
+    for i, k in enumerate(keys):
+        out[k] = dict(S=S[so[i]:so[i + 1]], act=act[ao[i]:ao[i + 1]], far=far[fo[i]:fo[i + 1]],
+                      k=int(g[prefix + "k"][i]))
+    return out
+
+
+def test_kat_id(golden):
+    qr = O.QRID(np.array([[1.0, 2.0], [2.0, 4.0]]))
+    S, R, T = qr.split(qr.rank(1e-10))
+    assert list(S) == list(golden["kat_rank1_S"]) == [1]
+    assert np.array_equal(T, golden["kat_rank1_T"])
+    qr = O.QRID(golden["kat_cluster_A"])
+    S, R, T = qr.split(qr.rank(1e-10))
+    assert len(S) == 8
+    assert np.array_equal(S, golden["kat_cluster_S"])
+    assert np.array_equal(T, golden["kat_cluster_T"])
+
+
+@pytest.mark.parametrize("name,builder", [("cfg1_", configs.cfg1), ("mini_", configs.mini_holes)])
+def test_oracle_matches_reference(golden, name, builder):
+    wl = builder()
+    rec = {}
+    f = O.factor_full(wl.boundary, wl.leaf_cap, wl.tol, wl.proxy_count, wl.proxy_factor, record=rec)
+    ref = _boxes(golden, name)
+    assert set(ref) == set(f.boxes)
+    for k, r in ref.items():
+        bo = f.boxes[k]
+        assert np.array_equal(bo.dofs, r["act"]), k
+        assert np.array_equal(rec[k]["far"], r["far"]), k
+        assert len(bo.S) == r["k"], k
+        assert np.array_equal(bo.S, r["S"]), k
+    i = 0
+    while name + f"stack{i}_key" in golden.files:
+        k = tuple(golden[name + f"stack{i}_key"])
+        assert np.array_equal(rec[k]["stack"], golden[name + f"stack{i}"]), k
+        i += 1
+    i = 0
+    while name + f"T{i}_key" in golden.files:
+        k = tuple(golden[name + f"T{i}_key"])
+        np.testing.assert_allclose(rec[k]["T"], golden[name + f"T{i}"], rtol=0, atol=1e-12)
+        i += 1
+    assert np.array_equal(f.root_dofs, golden[name + "root_dofs"])
+    kpl = {int(l): int(v) for l, v in golden[name + "k_per_level"]}
+    assert f.stats["k_per_level"] == kpl
+    x = f.solve(golden[name + "rhs"])
+    xr = golden[name + "x"]
+    assert np.linalg.norm(x - xr) / np.linalg.norm(xr) < 1e-13
+    y = f.apply(golden[name + "apply_in"])
+    yr = golden[name + "apply_out"]
+    assert np.linalg.norm(y - yr) / np.linalg.norm(yr) < 1e-13
+
+
+def test_oracle_update_dirty_set(golden):
+    from paper_2001_11619_b200.geometry import MoveHole, apply_perturbation
+    wl = configs.mini_holes()
+    f = O.factor_full(wl.boundary, wl.leaf_cap, wl.tol, wl.proxy_count, wl.proxy_factor)
+    nb, rep = apply_perturbation(wl.boundary, [MoveHole(2, translation=(0.1, -0.05))])
+    fu = O.update(f, nb, rep)
+    ref_dirty = {tuple(k) for k in golden["mini_upd_dirty"]}
+    assert fu.stats["dirty"] == ref_dirty
+    x = fu.solve(golden["mini_rhs"])
+    xr = golden["mini_upd_x"]
+    assert np.linalg.norm(x - xr) / np.linalg.norm(xr) < 1e-13
+    # update == refactor on the new geometry (reference claim skel.py:459-465)
+    fr = O.factor_full(nb, wl.leaf_cap, wl.tol, wl.proxy_count, wl.proxy_factor)
+    assert np.array_equal(fr.solve(golden["mini_rhs"]), x)
