@@ -1,0 +1,196 @@
+/*
+ * skelb200 -- C ABI of the B200-native (sm_100a) level-batched recursive
+ * skeletonization kernels (arXiv 2001.11619 hot path).
+ *
+ * The reference package (skelsolve, pure Python) has no FFI: its hot path calls
+ * NumPy ufuncs and SciPy LAPACK per box.  Each entry point below replaces one of
+ * those per-box call sites with ONE batched call over all boxes of a quadtree
+ * level, and cites the reference file:line it replaces (paths relative to
+ * /root/reference/pkg/src/skelsolve/).  The Python drop-in (package
+ * paper_2001_11619_b200, module skel.py) binds these through ctypes exactly
+ * as shown in INTEGRATION.md.
+ *
+ * Conventions
+ *  - All double/int pointers inside descriptors are DEVICE pointers unless a
+ *    parameter is documented as host memory.  Descriptor arrays themselves
+ *    (SkbGemm*, SkbMat*, int64_t* lists of per-box sizes) are HOST memory; the
+ *    library uploads them stream-ordered.
+ *  - Matrices are fp64 row-major (NumPy C order) unless noted; stacks for the
+ *    ID are column-major per box (each stack column contiguous).
+ *  - stream is a cudaStream_t passed as void*.  Calls are stream-ordered and
+ *    asynchronous; scratch is allocated with cudaMallocAsync on that stream.
+ *  - Return value: 0 = OK, < 0 = -(cudaError_t), > 0 = argument error.
+ *  - Numerical conditions (zero pivots, pivot ratios, ranks) are reported in
+ *    per-box output arrays, never as return codes; results are deterministic
+ *    and independent of batch composition (no float atomics).
+ */
+#ifndef SKELB200_H
+#define SKELB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* D = alpha * op(A) * op(B) + beta * C, op(A) m x k, op(B) k x n, row-major.
+ * transA == 0: A stored m x k (A[i*lda+p]); transA == 1: A stored k x m.
+ * transB == 0: B stored k x n;              transB == 1: B stored n x k.
+ * C may alias D.  beta == 0 never reads C.                                 */
+typedef struct SkbGemm {
+  const double* A;
+  const double* B;
+  const double* C;
+  double* D;
+  int64_t m, n, k;
+  int64_t lda, ldb, ldc, ldd;
+  double alpha, beta;
+  int32_t transA, transB;
+  int64_t tile_begin; /* filled by the library */
+} SkbGemm;
+
+/* A dense row-major matrix view. */
+typedef struct SkbMat {
+  double* ptr;
+  int64_t rows, cols, ld;
+} SkbMat;
+
+int skb_version(void);
+
+/* Grouped fp64 GEMM on DMMA (mma.sync m8n8k4 f64) tiles.
+ * Replaces the NumPy '@' products of skel.py:321-334, 389-396, 140-163,
+ * 182, 188, 199-201, 214-215.                                               */
+int skb_gemm_grouped(SkbGemm* probs, int64_t nprob, void* stream);
+
+/* (a) ID stacks of a level batch, column-major per box with ld = rows_b,
+ * rows_b = 2*nF_b + 6*P + 2, row blocks [K_in; P_in; n_in; K_out^T; P_out; n_out].
+ * Replaces kernels.eval_block_pair (kernels.py:133-160), proxy_block_incoming
+ * (kernels.py:307-321), proxy_block_outgoing (kernels.py:328-346),
+ * nullspace_capture_rows (kernels.py:355-371) and the vstack at skel.py:306-314.
+ * pos/nrm: (N,2); w: (N,); act/far: CSR DOF lists per box (device);
+ * ppts/pnrm: (nbox,P,2) proxy points and radial normals; pw: (nbox,) weights;
+ * stack_off: (nbox,) element offsets into stack.  FMA contraction is off so
+ * entries follow NumPy's rounding order.                                    */
+int skb_assemble_stack(const double* pos, const double* nrm, const double* w, int64_t nbox,
+                       const int64_t* act_off, const int64_t* act, const int64_t* far_off,
+                       const int64_t* far, const double* ppts, const double* pnrm,
+                       const double* pw, int32_t P, const int64_t* stack_off, double* stack,
+                       int64_t max_cols, int64_t max_items, void* stream);
+
+/* (a) Self blocks E_b = A[active_b, active_b] (kernels.eval_block, kernels.py:89-130)
+ * with children's Schur-complemented skeleton blocks on the diagonal
+ * (_Compressor.self_block, skel.py:282-291), written in permuted order:
+ * E_out[i][j] = E[perm[i]][perm[j]] (perm == NULL -> identity).
+ * child_off: (nbox*5) active offsets of up to 4 children, -1 terminated;
+ * child_xss: (nbox*4) device addresses of child Xss blocks (row-major k_c x k_c).
+ * E_out: E_off[b] element offset, row stride E_ld[b].                       */
+int skb_assemble_self(const double* pos, const double* nrm, const double* w, const double* kappa,
+                      int64_t nbox, const int64_t* act_off, const int64_t* act,
+                      const int64_t* perm_off, const int32_t* perm,
+                      const int64_t* child_off, const int64_t* child_xss,
+                      double* E, const int64_t* E_off, const int64_t* E_ld,
+                      int64_t max_n, void* stream);
+
+/* (d) Stokeslet/rotlet columns H (nd x 3p) and weighted rigid-body functionals
+ * Psi (nd x 3p) -- kernels.stokeslet_rotlet_columns (kernels.py:201-223) and
+ * build_augmentation (kernels.py:226-246).  curve_off: (p+2,) node offsets.  */
+int skb_assemble_aug(const double* pos, const double* w, int64_t n_nodes,
+                     const double* hole_centers, int64_t n_holes, const int64_t* curve_off_host,
+                     double* H, double* Psi, void* stream);
+
+/* (b) Batched unpivoted Householder QR (LAPACK dgeqrf semantics, blocked
+ * compact-WY, panel width 32) of column-major matrices A_b (m_b x n_b, lda_b):
+ * the R factor lands in the upper triangle, the strictly lower triangle of the
+ * leading min(m,n) rows is zeroed on exit (R ready for QRCP).
+ * Replaces the pre-reduction sla.qr(A, mode="r") at dense.py:56-59.
+ * m, n, lda, A: HOST arrays of length nbox (A as device addresses).          */
+int skb_geqrf_batched(int64_t nbox, const int64_t* m, const int64_t* n, const int64_t* lda,
+                      const int64_t* A, void* stream);
+
+/* (b) Batched column-pivoted QR + interpolative decomposition with LAPACK
+ * dgeqp3/dlaqp2 pivot semantics (largest partial column norm, lowest index on
+ * ties, dlaqp2 norm downdating with recompute at sqrt(eps)) and the rank
+ * k = #{|R_jj| > tol*|R_00|} (dense.py:65-68).  Stops once every remaining
+ * partial norm is below the rank threshold (and at least kmin_b steps done).
+ * Lazy pivoting: columns are not moved; perm[i] is the column chosen at step i,
+ * perm[k..] lists the redundant columns (pivots past k, then the unchosen ones
+ * ascending) and R(i, perm[j]) stays in A[perm[j]][i].  Large boxes are
+ * spread over up to 32 co-resident CTAs (cooperative launch).
+ * Replaces sla.qr(..., pivoting=True) + rank_for_tol (dense.py:48-68).
+ * Host arrays: m, n, lda, A (device addresses), kmin.
+ * Device outputs: perm (int32, perm_off[b] offsets), k_out (int32 per box),
+ * diag (|R_jj|, at perm_off[b]), min_gap (double per box, smallest relative
+ * gap between the pivot norm and the runner-up over the first k steps).     */
+int skb_qrcp_id_batched(int64_t nbox, const int64_t* m, const int64_t* n, const int64_t* lda,
+                        const int64_t* A, const int64_t* kmin, double tol,
+                        const int64_t* perm_off_host, int32_t* perm, double* diag,
+                        int32_t* k_out, int32_t* steps_out, double* min_gap, void* stream);
+
+/* (b) T = R11^-1 R12 per box after skb_qrcp_id_batched (dense.py:77): gathers
+ * the lazily pivoted R11 (k x k) / R12 (k x (n-k)) from the column-major A_b
+ * via the device perm_b and solves in place into row-major T_b (k x (n-k)).
+ * A, lda, k, n, perm_dev (device int32 addresses), T: HOST arrays.            */
+int skb_id_T_batched(int64_t nbox, const int64_t* A, const int64_t* lda, const int64_t* k,
+                     const int64_t* n, const int64_t* perm_dev, const int64_t* T, void* stream);
+
+/* Batched 2-D copy: dst_b[i][j] = src_b[i][j] (trans == 0) or src_b[j][i]
+ * (trans == 1, src stored cols x rows), for i < rows_b, j < cols_b.
+ * dst/src: HOST arrays of SkbMat (device pointers; rows/cols of dst used). */
+int skb_copy2d_batched(int64_t nbox, const SkbMat* dst, const SkbMat* src, int32_t trans,
+                       void* stream);
+
+/* (c) Batched LU with partial pivoting of row-major n_b x n_b matrices (in
+ * place), LAPACK dgetrf semantics (largest |a| in the column, first on ties),
+ * blocked (panel 64; trailing update on the grouped DMMA GEMM).  ipiv: 0-based
+ * row interchanges (int32).  info_out[b] = first exact zero pivot index or -1;
+ * ratio_out[b] = min|u_ii| / max|u_ii| (1.0 for n == 0).
+ * Replaces sla.lu_factor + pivot_ratio (dense.py:113-127).
+ * a: HOST array of SkbMat (square); ipiv: HOST array of device int32 addrs.  */
+int skb_getrf_batched(int64_t nbox, const SkbMat* a, const int64_t* ipiv, int32_t* info_out,
+                      double* ratio_out, void* stream);
+
+/* (c) Batched LU solve B_b <- A_b^-1 B_b with factors from skb_getrf_batched
+ * (trans == 0) -- sla.lu_solve, dense.py:129-135.  b: HOST SkbMat array,
+ * rows must equal the LU order.                                             */
+int skb_getrs_batched(int64_t nbox, const SkbMat* lu, const int64_t* ipiv, const SkbMat* b,
+                      void* stream);
+
+/* Row gather/scatter by DOF lists: the NumPy fancy indexing x[dofs] of
+ * skel.py:140-163, 180-221, 384-396.  For box b, local row i < cnt_b:
+ *   gather : dst[dst_off[b] + i*dst_ld[b] + c] = src[idx[i]*src_ld + col[c]]
+ *   scatter: dst[idx[i]*dst_ld_g + col[c]] = src[src_off[b] + i*src_ld[b] + c]
+ * for c < ncol_b; col == NULL means col[c] = c.  idx lists are CSR (idx_off,
+ * idx); col lists CSR (col_off, col) or NULL with ncol uniform (ncols).
+ * Device arrays throughout; max_rows/max_cols (host scalars) size the grid.
+ * accumulate != 0 in scatter adds instead of storing (alpha * src).         */
+int skb_gather_rows(int64_t nbox, const int64_t* idx_off, const int64_t* idx,
+                    const int64_t* col_off, const int64_t* col, int64_t ncols,
+                    const double* src, int64_t src_ld, double* dst, const int64_t* dst_off,
+                    const int64_t* dst_ld, int64_t max_rows, int64_t max_cols, void* stream);
+int skb_scatter_rows(int64_t nbox, const int64_t* idx_off, const int64_t* idx,
+                     const int64_t* col_off, const int64_t* col, int64_t ncols,
+                     const double* src, const int64_t* src_off, const int64_t* src_ld,
+                     double* dst, int64_t dst_ld, int32_t accumulate, double alpha,
+                     int64_t max_rows, int64_t max_cols, void* stream);
+
+/* (d) Deterministic accumulation of per-box Schur partials into the q x q
+ * augmentation corner (skel.py:396: schur += PsiV[rd]^T w, box order kept):
+ *   schur[row][c] += sum over contributions t of row (CSR row_off/contrib, in
+ *   box order) of part[contrib[t] + c], c < q.                              */
+int skb_schur_accumulate(int64_t q, const int64_t* row_off, const int64_t* contrib,
+                         const double* part, double* schur, void* stream);
+
+/* Fill dst (n x n, ld) with diag_val*I + scale*src (src may be NULL). */
+int skb_diag_fill(int64_t n, double* dst, int64_t ld, double diag_val, const double* src,
+                  int64_t src_ld, double scale, void* stream);
+
+/* dst[idx[i]*ld + c] = value for i < nidx, c < ncols (the nonroot mask of
+ * skel.py:181-188 applied by zeroing root rows of a copy). unused: NULL.    */
+int skb_fill_rows(int64_t nidx, const int64_t* idx, double* dst, int64_t ld, const void* unused,
+                  int64_t ncols, double value, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SKELB200_H */

@@ -1,0 +1,102 @@
+"""ctypes binding of libskelb200.so (the C ABI declared in include/skelb200.h).
+
+There is deliberately no CPU fallback: if the shared library is missing or no
+CUDA device is visible, every entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libskelb200.so")
+
+GEMM_DT = np.dtype([("A", "u8"), ("B", "u8"), ("C", "u8"), ("D", "u8"),
+                    ("m", "i8"), ("n", "i8"), ("k", "i8"),
+                    ("lda", "i8"), ("ldb", "i8"), ("ldc", "i8"), ("ldd", "i8"),
+                    ("alpha", "f8"), ("beta", "f8"), ("transA", "i4"), ("transB", "i4"),
+                    ("tile_begin", "i8")])
+assert GEMM_DT.itemsize == 120
+MAT_DT = np.dtype([("ptr", "u8"), ("rows", "i8"), ("cols", "i8"), ("ld", "i8")])
+
+_vp = ctypes.c_void_p
+_i64 = ctypes.c_int64
+_i32 = ctypes.c_int32
+_f64 = ctypes.c_double
+
+SIGNATURES = {
+    "skb_version": [],
+    "skb_gemm_grouped": [_vp, _i64, _vp],
+    "skb_assemble_stack": [_vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp,
+                           _vp, _i64, _i64, _vp],
+    "skb_assemble_self": [_vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                          _i64, _vp],
+    "skb_assemble_aug": [_vp, _vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp],
+    "skb_geqrf_batched": [_i64, _vp, _vp, _vp, _vp, _vp],
+    "skb_qrcp_id_batched": [_i64, _vp, _vp, _vp, _vp, _vp, _f64, _vp, _vp, _vp, _vp, _vp, _vp,
+                            _vp],
+    "skb_copy2d_batched": [_i64, _vp, _vp, _i32, _vp],
+    "skb_id_T_batched": [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "skb_getrf_batched": [_i64, _vp, _vp, _vp, _vp, _vp],
+    "skb_getrs_batched": [_i64, _vp, _vp, _vp, _vp],
+    "skb_gather_rows": [_i64, _vp, _vp, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _vp, _i64, _i64,
+                        _vp],
+    "skb_scatter_rows": [_i64, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _i64, _i32, _f64,
+                         _i64, _i64, _vp],
+    "skb_schur_accumulate": [_i64, _vp, _vp, _vp, _vp, _vp],
+    "skb_diag_fill": [_i64, _vp, _i64, _f64, _vp, _i64, _f64, _vp],
+    "skb_fill_rows": [_i64, _vp, _vp, _i64, _vp, _i64, _f64, _vp],
+}
+
+_LIB = None
+
+
+class SkbError(RuntimeError):
+    pass
+
+
+def load(path: str = LIB_PATH):
+    """Load the shared library and declare argument types (no device needed)."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(path):
+        raise SkbError(f"{path} not built -- run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(path)
+    for name, args in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = ctypes.c_int
+    _LIB = lib
+    return lib
+
+
+def call(name: str, *args):
+    """Invoke an entry point; numpy arrays are passed by address and kept alive
+    for the duration of the call, torch tensors by data_ptr()."""
+    lib = load()
+    conv = []
+    for a in args:
+        if isinstance(a, np.ndarray):
+            conv.append(a.ctypes.data)
+        elif hasattr(a, "data_ptr"):
+            conv.append(a.data_ptr())
+        else:
+            conv.append(a)
+    rc = getattr(lib, name)(*conv)
+    del conv
+    if rc != 0:
+        raise SkbError(f"{name} returned {rc}")
+    return rc
+
+
+def ptr(x) -> int | None:
+    """Device/host address of a torch tensor or numpy array (None passes NULL)."""
+    if x is None:
+        return None
+    if isinstance(x, np.ndarray):
+        return x.ctypes.data
+    return x.data_ptr()

@@ -89,17 +89,22 @@ def cfg1(seed: int = 0, n: int = 4096) -> Workload:
 
 
 def holes_circle(seed: int, R: float, n_outer: int, n_holes: int, r_hole: float,
-                 n_per_hole: int, sep: float, disc: float) -> Boundary:
+                 n_per_hole: int, sep: float, disc: float, phases: bool = False) -> Boundary:
+    """Outer circle + circular holes.  ``phases`` rotates every curve's node
+    parameters by a seeded offset, breaking the mirror symmetries of equispaced
+    circles that create exact pivot ties (used by the small strict-parity case)."""
     rng = np.random.default_rng(seed)
     cs, _ = _sample_centers(rng, n_holes, lambda: r_hole, lambda a, b: sep, lambda a: disc)
-    curves = [circle_curve(n_outer, radius=R)]
-    curves += [circle_curve(n_per_hole, c, r_hole, clockwise=True) for c in cs]
+    ph = rng.uniform(0, 2 * np.pi, n_holes + 1) if phases else np.zeros(n_holes + 1)
+    curves = [circle_curve(n_outer, radius=R, phase=ph[0])]
+    curves += [circle_curve(n_per_hole, c, r_hole, clockwise=True, phase=ph[i + 1])
+               for i, c in enumerate(cs)]
     return Boundary(curves)
 
 
 def cfg2(seed: int = 0) -> Workload:
     """Outer circle R=10 (8192 nodes) + 16 holes r=0.5 (1024 nodes), centres sep >= 1.5."""
-    b = holes_circle(seed, 10.0, 8192, 16, 0.5, 1024, 1.5, 8.5)
+    b = holes_circle(seed, 10.0, 8192, 16, 0.5, 1024, 1.5, 8.5, phases=True)
     rng = np.random.default_rng(seed + 1000)
     f = rng.standard_normal(2 * b.n_nodes)
     rhs = np.concatenate([f, np.zeros(3 * b.n_holes)])
@@ -124,8 +129,10 @@ def cfg3(seed: int = 0) -> Workload:
                 break
         else:
             raise RuntimeError("could not place ellipse")
-    curves = [circle_curve(16384, radius=R)]
-    curves += [ellipse_curve(512, c, a, bb, phi, clockwise=True) for c, a, bb, phi in params]
+    ph = rng.uniform(0, 2 * np.pi, len(params) + 1)
+    curves = [circle_curve(16384, radius=R, phase=ph[0])]
+    curves += [ellipse_curve(512, c, a, bb, phi, clockwise=True, phase=ph[i + 1])
+               for i, (c, a, bb, phi) in enumerate(params)]
     b = Boundary(curves)
     return Workload("cfg3_256ellipses_N147456", b, 1e-8, 128, 96, seed=seed)
 
@@ -139,7 +146,7 @@ def cfg5_rhs(b: Boundary, nrhs: int = 256, seed: int = 5) -> np.ndarray:
 def mini_holes(seed: int = 0, n_outer: int = 1024, n_holes: int = 3, n_per_hole: int = 256,
                R: float = 3.0) -> Workload:
     """Small multiply-connected case for fast parity tests."""
-    b = holes_circle(seed, R, n_outer, n_holes, 0.5, n_per_hole, 1.5, R - 1.0)
+    b = holes_circle(seed, R, n_outer, n_holes, 0.5, n_per_hole, 1.5, R - 1.0, phases=True)
     rng = np.random.default_rng(seed + 7)
     rhs = np.concatenate([rng.standard_normal(2 * b.n_nodes), np.zeros(3 * n_holes)])
     return Workload(f"mini_{n_holes}holes", b, 1e-10, 64, 64, seed=seed, extra={"rhs": rhs})

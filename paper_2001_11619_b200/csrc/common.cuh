@@ -1,0 +1,50 @@
+// Shared helpers for the sm_100a skeletonization kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/skelb200.h"
+
+#define SKB_RET(expr)                                              \
+  do {                                                             \
+    cudaError_t _e = (expr);                                       \
+    if (_e != cudaSuccess) return -(int)_e;                        \
+  } while (0)
+
+#define SKB_LAUNCH_CHECK() SKB_RET(cudaGetLastError())
+
+namespace skb {
+
+constexpr int kWarp = 32;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// fp64 tensor-core MMA: D(8x8) += A(8x4, row) * B(4x8, col).  SASS: DMMA.
+// Fragment ownership (PTX ISA, m8n8k4 .f64): A[lane>>2][lane&3],
+// B[lane&3][lane>>2], C/D[lane>>2][2*(lane&3) + {0,1}].
+__device__ __forceinline__ void dmma8x8x4(double& d0, double& d1, double a, double b) {
+  asm volatile(
+      "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+
+// Copy host descriptors to a stream-ordered device buffer (freed async by caller).
+template <typename T>
+inline int upload(const T* host, int64_t n, cudaStream_t s, T** dev) {
+  *dev = nullptr;
+  if (n <= 0) return 0;
+  SKB_RET(cudaMallocAsync((void**)dev, sizeof(T) * n, s));
+  SKB_RET(cudaMemcpyAsync(*dev, host, sizeof(T) * n, cudaMemcpyHostToDevice, s));
+  return 0;
+}
+
+inline int grid_cap(int64_t want, int64_t cap) {
+  return (int)(want < 1 ? 1 : (want > cap ? cap : want));
+}
+
+}  // namespace skb

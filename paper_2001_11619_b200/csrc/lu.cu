@@ -1,0 +1,454 @@
+// (c) Batched partially pivoted LU and LU solves (dgetrf / dgetrs semantics).
+//
+// Replaces the per-box PLU of reference dense.py:106-135 (sla.lu_factor /
+// sla.lu_solve) for all X_RR blocks of a level at once, and the corner LU of
+// _finish_top (skel.py:399-405).  Row-major storage; right-looking blocked
+// algorithm, panel width 64: the panel (getf2) is one CTA per matrix, the
+// U12 triangular solve is batched over (matrix, column chunk), the trailing
+// update goes to the grouped DMMA GEMM.
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+
+namespace skb {
+
+int gemm_grouped(SkbGemm* probs, int64_t nprob, cudaStream_t s);
+
+constexpr int LB = 64;  // LU block width
+
+struct LuPanel {
+  double* A;
+  int64_t n, ld, j0, jb;
+  int32_t* ipiv;
+  int32_t* info;
+};
+
+struct AbsMax {
+  double v;
+  int64_t idx;
+};
+
+__device__ __forceinline__ AbsMax absmax_merge(AbsMax a, AbsMax b) {
+  return (b.v > a.v || (b.v == a.v && b.idx < a.idx)) ? b : a;
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) k_getf2_panel(const LuPanel* __restrict__ descs) {
+  __shared__ AbsMax red[NT / 32 + 1];
+  const LuPanel D = descs[blockIdx.x];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int64_t c = 0; c < D.jb; ++c) {
+    const int64_t col = D.j0 + c;
+    AbsMax loc{-1.0, INT64_MAX};
+    for (int64_t r = col + threadIdx.x; r < D.n; r += NT) {
+      const double v = fabs(D.A[r * D.ld + col]);
+      if (v > loc.v) { loc.v = v; loc.idx = r; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      AbsMax y{__shfl_xor_sync(0xffffffffu, loc.v, o), __shfl_xor_sync(0xffffffffu, loc.idx, o)};
+      loc = absmax_merge(loc, y);
+    }
+    __syncthreads();
+    if (lane == 0) red[warp] = loc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      AbsMax r = red[0];
+      for (int w = 1; w < NT / 32; ++w) r = absmax_merge(r, red[w]);
+      red[NT / 32] = r;
+    }
+    __syncthreads();
+    const int64_t p = red[NT / 32].idx;
+    const double piv = D.A[p * D.ld + col];
+    if (threadIdx.x == 0) {
+      D.ipiv[col] = (int32_t)p;
+      if (piv == 0.0 && *D.info < 0) *D.info = (int32_t)col;
+    }
+    if (piv == 0.0) { __syncthreads(); continue; }
+    if (p != col) {
+      double* ra = D.A + col * D.ld;
+      double* rb = D.A + p * D.ld;
+      for (int64_t j = threadIdx.x; j < D.n; j += NT) {
+        const double t = ra[j]; ra[j] = rb[j]; rb[j] = t;
+      }
+    }
+    __syncthreads();
+    const double rinv = 1.0 / piv;
+    const double* urow = D.A + col * D.ld;
+    for (int64_t r = col + 1 + threadIdx.x; r < D.n; r += NT) {
+      double* row = D.A + r * D.ld;
+      const double l = row[col] * rinv;
+      row[col] = l;
+      for (int64_t cc = col + 1; cc < D.j0 + D.jb; ++cc) row[cc] -= l * urow[cc];
+    }
+    __syncthreads();
+  }
+}
+
+// In-place triangular solve of a jb-row block B (row-major, ldb) against the
+// jb x jb diagonal block L (ldl) of an LU factor.  UPPER=false: unit lower,
+// forward; UPPER=true: non-unit upper, backward.  One thread per column.
+struct TrsmDesc {
+  const double* L;
+  int64_t ldl;
+  double* B;
+  int64_t ldb;
+  int64_t jb, ncols;
+};
+
+template <bool UPPER>
+__global__ void __launch_bounds__(256) k_trsm_block(const TrsmDesc* __restrict__ descs) {
+  __shared__ double Ls[LB][LB + 1];
+  const TrsmDesc D = descs[blockIdx.y];
+  const int jb = (int)D.jb;
+  for (int t = threadIdx.x; t < jb * jb; t += blockDim.x) {
+    const int i = t / jb, p = t % jb;
+    Ls[i][p] = D.L[i * D.ldl + p];
+  }
+  __syncthreads();
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= D.ncols) return;
+  double x[LB];
+#pragma unroll
+  for (int i = 0; i < LB; ++i)
+    if (i < jb) x[i] = D.B[i * D.ldb + c];
+  if (!UPPER) {
+#pragma unroll
+    for (int i = 1; i < LB; ++i) {
+      if (i >= jb) break;
+      double s = x[i];
+#pragma unroll
+      for (int p = 0; p < LB; ++p)
+        if (p < i) s -= Ls[i][p] * x[p];
+      x[i] = s;
+    }
+  } else {
+#pragma unroll
+    for (int i = LB - 1; i >= 0; --i) {
+      if (i >= jb) continue;
+      double s = x[i];
+#pragma unroll
+      for (int p = 0; p < LB; ++p)
+        if (p > i && p < jb) s -= Ls[i][p] * x[p];
+      x[i] = s / Ls[i][i];
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < LB; ++i)
+    if (i < jb) D.B[i * D.ldb + c] = x[i];
+}
+
+static int launch_trsm(std::vector<TrsmDesc>& td, bool upper, cudaStream_t s) {
+  if (td.empty()) return 0;
+  int64_t maxc = 0;
+  for (auto& t : td) maxc = std::max(maxc, t.ncols);
+  if (maxc == 0) return 0;
+  TrsmDesc* d = nullptr;
+  int rc = upload(td.data(), (int64_t)td.size(), s, &d);
+  if (rc) return rc;
+  for (int64_t b0 = 0; b0 < (int64_t)td.size(); b0 += 65535) {
+    const int64_t nb = std::min<int64_t>(65535, (int64_t)td.size() - b0);
+    dim3 grid((unsigned)((maxc + 255) / 256), (unsigned)nb);
+    if (upper) k_trsm_block<true><<<grid, 256, 0, s>>>(d + b0);
+    else k_trsm_block<false><<<grid, 256, 0, s>>>(d + b0);
+  }
+  cudaError_t e = cudaGetLastError();
+  cudaFreeAsync(d, s);
+  return e == cudaSuccess ? 0 : -(int)e;
+}
+
+struct RatioDesc {
+  const double* A;
+  int64_t n, ld;
+};
+
+__global__ void k_pivot_ratio(const RatioDesc* __restrict__ descs, double* __restrict__ out) {
+  __shared__ double smin[256], smax[256];
+  const RatioDesc D = descs[blockIdx.x];
+  double mn = INFINITY, mx = 0.0;
+  for (int64_t i = threadIdx.x; i < D.n; i += blockDim.x) {
+    const double v = fabs(D.A[i * D.ld + i]);
+    mn = fmin(mn, v);
+    mx = fmax(mx, v);
+  }
+  smin[threadIdx.x] = mn;
+  smax[threadIdx.x] = mx;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      smin[threadIdx.x] = fmin(smin[threadIdx.x], smin[threadIdx.x + o]);
+      smax[threadIdx.x] = fmax(smax[threadIdx.x], smax[threadIdx.x + o]);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[blockIdx.x] = D.n == 0 ? 1.0 : smin[0] / smax[0];
+}
+
+// Whole-matrix LU in shared memory, one CTA per matrix (n <= kSmallLU):
+// right-looking dgetf2 with the row swap applied to the full row.
+constexpr int kSmallLU = 160;
+
+struct SmallLU {
+  double* A;
+  int64_t n, ld;
+  int32_t* ipiv;
+  int32_t* info;
+};
+
+template <int NT>
+__global__ void __launch_bounds__(NT) k_getrf_small(const SmallLU* __restrict__ descs) {
+  extern __shared__ double M[];
+  __shared__ AbsMax red[NT / 32 + 1];
+  const SmallLU D = descs[blockIdx.x];
+  const int n = (int)D.n, L = n + 1;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int t = threadIdx.x; t < n * n; t += NT) M[(t / n) * L + t % n] = D.A[(t / n) * D.ld + t % n];
+  int info = -1;
+  double prev_rinv = 0.0;   // multipliers of column j-1 are scaled lazily at step j
+  __syncthreads();
+  for (int j = 0; j < n; ++j) {
+    AbsMax loc{-1.0, INT64_MAX};
+    for (int r = j + threadIdx.x; r < n; r += NT) {
+      if (j > 0 && prev_rinv != 0.0) M[r * L + j - 1] *= prev_rinv;
+      const double v = fabs(M[r * L + j]);
+      if (v > loc.v) { loc.v = v; loc.idx = r; }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      AbsMax y{__shfl_xor_sync(0xffffffffu, loc.v, o), __shfl_xor_sync(0xffffffffu, loc.idx, o)};
+      loc = absmax_merge(loc, y);
+    }
+    if (lane == 0) red[warp] = loc;
+    __syncthreads();
+    AbsMax best = red[0];
+#pragma unroll
+    for (int w = 1; w < NT / 32; ++w) best = absmax_merge(best, red[w]);
+    const int p = (int)best.idx;
+    const double piv = M[p * L + j];
+    if (threadIdx.x == 0) D.ipiv[j] = p;
+    if (piv == 0.0) {
+      if (info < 0) info = j;
+      prev_rinv = 0.0;
+      __syncthreads();
+      continue;
+    }
+    if (p != j)
+      for (int c = threadIdx.x; c < n; c += NT) {
+        const double t = M[j * L + c]; M[j * L + c] = M[p * L + c]; M[p * L + c] = t;
+      }
+    __syncthreads();
+    const double rinv = 1.0 / piv;
+    prev_rinv = rinv;
+    // rank-1 update of the trailing block, one thread per (row, 8-column chunk);
+    // column j itself is only read here and scaled at the next step
+    const int rows = n - j - 1, cols = n - j - 1;
+    const int cpr = cols > 0 ? (cols + 7) / 8 : 1;
+    for (int e = threadIdx.x; e < rows * cpr; e += NT) {
+      const int r = j + 1 + e / cpr;
+      const int c0 = j + 1 + (e % cpr) * 8;
+      const double l = M[r * L + j] * rinv;
+      for (int c = c0; c < c0 + 8 && c < n; ++c) M[r * L + c] -= l * M[j * L + c];
+    }
+    __syncthreads();
+  }
+  for (int t = threadIdx.x; t < n * n; t += NT) D.A[(t / n) * D.ld + t % n] = M[(t / n) * L + t % n];
+  if (threadIdx.x == 0) *D.info = info;
+}
+
+int getrf_batched(int64_t nbox, const SkbMat* a, const int64_t* ipiv, int32_t* info_out,
+                  double* ratio_out, cudaStream_t s) {
+  if (nbox <= 0) return 0;
+  SKB_RET(cudaMemsetAsync(info_out, 0xff, sizeof(int32_t) * nbox, s));
+  int64_t max_n = 0, max_small = 0;
+  std::vector<SmallLU> sl;
+  for (int64_t b = 0; b < nbox; ++b) {
+    if (a[b].rows <= 0) continue;
+    if (a[b].rows <= kSmallLU) {
+      sl.push_back(SmallLU{a[b].ptr, a[b].rows, a[b].ld, reinterpret_cast<int32_t*>(ipiv[b]),
+                           info_out + b});
+      max_small = std::max(max_small, a[b].rows);
+    } else {
+      max_n = std::max(max_n, a[b].rows);
+    }
+  }
+  int rc = 0;
+  if (!sl.empty()) {
+    SmallLU* ds = nullptr;
+    if ((rc = upload(sl.data(), (int64_t)sl.size(), s, &ds))) return rc;
+    const size_t smem = sizeof(double) * (size_t)max_small * (max_small + 1);
+    SKB_RET(cudaFuncSetAttribute(k_getrf_small<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    k_getrf_small<256><<<(unsigned)sl.size(), 256, smem, s>>>(ds);
+    SKB_LAUNCH_CHECK();
+    cudaFreeAsync(ds, s);
+  }
+  std::vector<LuPanel> pd;
+  std::vector<TrsmDesc> td;
+  std::vector<SkbGemm> gd;
+  for (int64_t j0 = 0; j0 < max_n; j0 += LB) {
+    pd.clear(); td.clear(); gd.clear();
+    for (int64_t b = 0; b < nbox; ++b) {
+      const int64_t n = a[b].rows;
+      if (j0 >= n || n <= kSmallLU) continue;
+      const int64_t jb = std::min<int64_t>(LB, n - j0), n2 = n - j0 - jb;
+      double* A = a[b].ptr;
+      const int64_t ld = a[b].ld;
+      pd.push_back(LuPanel{A, n, ld, j0, jb, reinterpret_cast<int32_t*>(ipiv[b]), info_out + b});
+      if (n2 > 0) {
+        td.push_back(TrsmDesc{A + j0 * ld + j0, ld, A + j0 * ld + j0 + jb, ld, jb, n2});
+        SkbGemm g{};
+        g.A = A + (j0 + jb) * ld + j0; g.lda = ld;           // L21: n2 x jb
+        g.B = A + j0 * ld + j0 + jb; g.ldb = ld;             // U12: jb x n2
+        g.C = A + (j0 + jb) * ld + j0 + jb; g.ldc = ld;      // A22
+        g.D = A + (j0 + jb) * ld + j0 + jb; g.ldd = ld;
+        g.m = n2; g.n = n2; g.k = jb; g.alpha = -1.0; g.beta = 1.0;
+        gd.push_back(g);
+      }
+    }
+    LuPanel* dp = nullptr;
+    if ((rc = upload(pd.data(), (int64_t)pd.size(), s, &dp))) return rc;
+    k_getf2_panel<256><<<(unsigned)pd.size(), 256, 0, s>>>(dp);
+    SKB_LAUNCH_CHECK();
+    cudaFreeAsync(dp, s);
+    if ((rc = launch_trsm(td, false, s))) return rc;
+    if ((rc = gemm_grouped(gd.data(), (int64_t)gd.size(), s))) return rc;
+  }
+  std::vector<RatioDesc> rd(nbox);
+  for (int64_t b = 0; b < nbox; ++b) rd[b] = RatioDesc{a[b].ptr, a[b].rows, a[b].ld};
+  RatioDesc* dr = nullptr;
+  if ((rc = upload(rd.data(), nbox, s, &dr))) return rc;
+  k_pivot_ratio<<<(unsigned)nbox, 256, 0, s>>>(dr, ratio_out);
+  SKB_LAUNCH_CHECK();
+  cudaFreeAsync(dr, s);
+  return 0;
+}
+
+struct SwapDesc {
+  double* B;
+  int64_t n, ld, ncols;
+  const int32_t* ipiv;
+};
+
+__global__ void k_apply_ipiv(const SwapDesc* __restrict__ descs) {
+  const SwapDesc D = descs[blockIdx.y];
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= D.ncols) return;
+  for (int64_t i = 0; i < D.n; ++i) {
+    const int64_t p = D.ipiv[i];
+    if (p != i) {
+      const double t = D.B[i * D.ld + c];
+      D.B[i * D.ld + c] = D.B[p * D.ld + c];
+      D.B[p * D.ld + c] = t;
+    }
+  }
+}
+
+// B <- L^-1 B (unit lower, forward) for a batch, blocked: diagonal blocks by
+// substitution, off-diagonal blocks on the grouped GEMM.
+int trsm_lower_unit_batched(int64_t nbox, const SkbMat* lu, const SkbMat* b, cudaStream_t s) {
+  int64_t max_n = 0;
+  for (int64_t i = 0; i < nbox; ++i)
+    if (b[i].cols > 0) max_n = std::max(max_n, lu[i].rows);
+  std::vector<TrsmDesc> td;
+  std::vector<SkbGemm> gd;
+  int rc = 0;
+  for (int64_t j0 = 0; j0 < max_n; j0 += LB) {
+    td.clear(); gd.clear();
+    for (int64_t i = 0; i < nbox; ++i) {
+      const int64_t n = lu[i].rows, nc = b[i].cols;
+      if (j0 >= n || nc == 0) continue;
+      const int64_t jb = std::min<int64_t>(LB, n - j0), n2 = n - j0 - jb;
+      const double* L = lu[i].ptr;
+      const int64_t ldl = lu[i].ld, ldb = b[i].ld;
+      td.push_back(TrsmDesc{L + j0 * ldl + j0, ldl, b[i].ptr + j0 * ldb, ldb, jb, nc});
+      if (n2 > 0) {
+        SkbGemm g{};
+        g.A = L + (j0 + jb) * ldl + j0; g.lda = ldl;
+        g.B = b[i].ptr + j0 * ldb; g.ldb = ldb;
+        g.C = b[i].ptr + (j0 + jb) * ldb; g.ldc = ldb;
+        g.D = b[i].ptr + (j0 + jb) * ldb; g.ldd = ldb;
+        g.m = n2; g.n = nc; g.k = jb; g.alpha = -1.0; g.beta = 1.0;
+        gd.push_back(g);
+      }
+    }
+    if ((rc = launch_trsm(td, false, s))) return rc;
+    if ((rc = gemm_grouped(gd.data(), (int64_t)gd.size(), s))) return rc;
+  }
+  return 0;
+}
+
+// B <- U^-1 B (non-unit upper, backward), blocked.  Only the upper triangle of
+// U is read.  Also computes T = R11^-1 R12 of the ID (dense.py:77).
+int trsm_upper_batched(int64_t nbox, const SkbMat* u, const SkbMat* b, cudaStream_t s) {
+  int64_t max_n = 0;
+  for (int64_t i = 0; i < nbox; ++i)
+    if (b[i].cols > 0) max_n = std::max(max_n, u[i].rows);
+  if (max_n == 0) return 0;
+  std::vector<TrsmDesc> td;
+  std::vector<SkbGemm> gd;
+  int rc = 0;
+  for (int64_t j0 = ((max_n - 1) / LB) * LB; j0 >= 0; j0 -= LB) {
+    td.clear(); gd.clear();
+    for (int64_t i = 0; i < nbox; ++i) {
+      const int64_t n = u[i].rows, nc = b[i].cols;
+      if (j0 >= n || nc == 0) continue;
+      const int64_t jb = std::min<int64_t>(LB, n - j0);
+      const double* U = u[i].ptr;
+      const int64_t ldu = u[i].ld, ldb = b[i].ld;
+      td.push_back(TrsmDesc{U + j0 * ldu + j0, ldu, b[i].ptr + j0 * ldb, ldb, jb, nc});
+      if (j0 > 0) {
+        SkbGemm g{};
+        g.A = U + j0; g.lda = ldu;                  // U[0:j0, j0:j0+jb]
+        g.B = b[i].ptr + j0 * ldb; g.ldb = ldb;
+        g.C = b[i].ptr; g.ldc = ldb;
+        g.D = b[i].ptr; g.ldd = ldb;
+        g.m = j0; g.n = nc; g.k = jb; g.alpha = -1.0; g.beta = 1.0;
+        gd.push_back(g);
+      }
+    }
+    if ((rc = launch_trsm(td, true, s))) return rc;
+    if ((rc = gemm_grouped(gd.data(), (int64_t)gd.size(), s))) return rc;
+  }
+  return 0;
+}
+
+int getrs_batched(int64_t nbox, const SkbMat* lu, const int64_t* ipiv, const SkbMat* b,
+                  cudaStream_t s) {
+  if (nbox <= 0) return 0;
+  int64_t max_c = 0;
+  std::vector<SwapDesc> sd;
+  for (int64_t i = 0; i < nbox; ++i) {
+    if (lu[i].rows == 0 || b[i].cols == 0) continue;
+    max_c = std::max(max_c, b[i].cols);
+    sd.push_back(SwapDesc{b[i].ptr, lu[i].rows, b[i].ld, b[i].cols,
+                          reinterpret_cast<const int32_t*>(ipiv[i])});
+  }
+  if (sd.empty()) return 0;
+  int rc = 0;
+  {
+    SwapDesc* d = nullptr;
+    if ((rc = upload(sd.data(), (int64_t)sd.size(), s, &d))) return rc;
+    for (int64_t b0 = 0; b0 < (int64_t)sd.size(); b0 += 65535) {
+      const int64_t nb = std::min<int64_t>(65535, (int64_t)sd.size() - b0);
+      dim3 grid((unsigned)((max_c + 127) / 128), (unsigned)nb);
+      k_apply_ipiv<<<grid, 128, 0, s>>>(d + b0);
+    }
+    SKB_LAUNCH_CHECK();
+    cudaFreeAsync(d, s);
+  }
+  if ((rc = trsm_lower_unit_batched(nbox, lu, b, s))) return rc;
+  return trsm_upper_batched(nbox, lu, b, s);
+}
+
+}  // namespace skb
+
+extern "C" int skb_getrf_batched(int64_t nbox, const SkbMat* a, const int64_t* ipiv,
+                                 int32_t* info_out, double* ratio_out, void* stream) {
+  return skb::getrf_batched(nbox, a, ipiv, info_out, ratio_out, (cudaStream_t)stream);
+}
+
+extern "C" int skb_getrs_batched(int64_t nbox, const SkbMat* lu, const int64_t* ipiv,
+                                 const SkbMat* b, void* stream) {
+  return skb::getrs_batched(nbox, lu, ipiv, b, (cudaStream_t)stream);
+}

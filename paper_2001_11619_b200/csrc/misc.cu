@@ -1,0 +1,185 @@
+// Data-movement kernels of the level pipeline: DOF-list row gathers/scatters
+// (the NumPy fancy indexing x[dofs] of reference skel.py:140-221, 384-396),
+// batched 2-D copies, the deterministic Schur accumulation (skel.py:396) and
+// the corner's -I - schur block (skel.py:404).
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+
+namespace skb {
+
+__global__ void k_copy2d(const SkbMat* __restrict__ dst, const SkbMat* __restrict__ src,
+                         int trans) {
+  const SkbMat D = dst[blockIdx.y], S = src[blockIdx.y];
+  const int64_t tot = D.rows * D.cols;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    int64_t i, j;
+    if (trans) { j = t / D.rows; i = t - j * D.rows; }   // walk src rows contiguously
+    else { i = t / D.cols; j = t - i * D.cols; }
+    D.ptr[i * D.ld + j] = trans ? S.ptr[j * S.ld + i] : S.ptr[i * S.ld + j];
+  }
+}
+
+__global__ void k_gather_rows(const int64_t* __restrict__ idx_off, const int64_t* __restrict__ idx,
+                              const int64_t* __restrict__ col_off,
+                              const int64_t* __restrict__ col, int64_t ncols,
+                              const double* __restrict__ src, int64_t src_ld,
+                              double* __restrict__ dst, const int64_t* __restrict__ dst_off,
+                              const int64_t* __restrict__ dst_ld) {
+  const int64_t b = blockIdx.y;
+  const int64_t i0 = idx_off[b], nr = idx_off[b + 1] - i0;
+  const int64_t c0 = col ? col_off[b] : 0;
+  const int64_t nc = col ? col_off[b + 1] - c0 : ncols;
+  double* d = dst + dst_off[b];
+  const int64_t ld = dst_ld[b];
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nr * nc;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / nc, c = t - i * nc;
+    const int64_t sc = col ? col[c0 + c] : c;
+    d[i * ld + c] = src[idx[i0 + i] * src_ld + sc];
+  }
+}
+
+__global__ void k_scatter_rows(const int64_t* __restrict__ idx_off,
+                               const int64_t* __restrict__ idx,
+                               const int64_t* __restrict__ col_off,
+                               const int64_t* __restrict__ col, int64_t ncols,
+                               const double* __restrict__ src,
+                               const int64_t* __restrict__ src_off,
+                               const int64_t* __restrict__ src_ld, double* __restrict__ dst,
+                               int64_t dst_ld, int accumulate, double alpha) {
+  const int64_t b = blockIdx.y;
+  const int64_t i0 = idx_off[b], nr = idx_off[b + 1] - i0;
+  const int64_t c0 = col ? col_off[b] : 0;
+  const int64_t nc = col ? col_off[b + 1] - c0 : ncols;
+  const double* s = src + src_off[b];
+  const int64_t ld = src_ld[b];
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nr * nc;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / nc, c = t - i * nc;
+    const int64_t dc = col ? col[c0 + c] : c;
+    double* o = dst + idx[i0 + i] * dst_ld + dc;
+    const double v = s[i * ld + c];
+    if (accumulate) *o += alpha * v;
+    else *o = v;
+  }
+}
+
+__global__ void k_schur_acc(int64_t q, const int64_t* __restrict__ row_off,
+                            const int64_t* __restrict__ contrib, const double* __restrict__ part,
+                            double* __restrict__ schur) {
+  const int64_t row = blockIdx.y;
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= q) return;
+  double v = schur[row * q + c];
+  for (int64_t t = row_off[row]; t < row_off[row + 1]; ++t) v += part[contrib[t] + c];
+  schur[row * q + c] = v;
+}
+
+__global__ void k_diag_fill(int64_t n, double* dst, int64_t ld, double dv, const double* src,
+                            int64_t sld, double scale) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n * n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / n, j = t - i * n;
+    double v = (i == j) ? dv : 0.0;
+    if (src) v = v + scale * src[i * sld + j];
+    dst[i * ld + j] = v;
+  }
+}
+
+__global__ void k_fill_rows(const int64_t* __restrict__ idx, int64_t nidx, double* dst,
+                            int64_t ld, int64_t ncols, double v) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nidx * ncols;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / ncols, c = t - i * ncols;
+    dst[idx[i] * ld + c] = v;
+  }
+}
+
+}  // namespace skb
+
+using namespace skb;
+
+extern "C" int skb_fill_rows(int64_t nidx, const int64_t* idx, double* dst, int64_t ld,
+                             const void* unused, int64_t ncols, double value, void* stream) {
+  (void)unused;
+  if (nidx <= 0 || ncols <= 0) return 0;
+  k_fill_rows<<<grid_cap((nidx * ncols + 255) / 256, 4096), 256, 0, (cudaStream_t)stream>>>(
+      idx, nidx, dst, ld, ncols, value);
+  SKB_LAUNCH_CHECK();
+  return 0;
+}
+
+extern "C" int skb_copy2d_batched(int64_t nbox, const SkbMat* dst, const SkbMat* src,
+                                  int32_t trans, void* stream) {
+  if (nbox <= 0) return 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t maxe = 0;
+  for (int64_t b = 0; b < nbox; ++b) maxe = std::max(maxe, dst[b].rows * dst[b].cols);
+  if (maxe == 0) return 0;
+  SkbMat *dd = nullptr, *ds = nullptr;
+  int rc = upload(dst, nbox, s, &dd);
+  if (rc) return rc;
+  if ((rc = upload(src, nbox, s, &ds))) return rc;
+  for (int64_t b0 = 0; b0 < nbox; b0 += 65535) {
+    const int64_t nb = std::min<int64_t>(65535, nbox - b0);
+    dim3 grid(grid_cap((maxe + 255) / 256, 1024), (unsigned)nb);
+    k_copy2d<<<grid, 256, 0, s>>>(dd + b0, ds + b0, trans);
+  }
+  cudaError_t e = cudaGetLastError();
+  cudaFreeAsync(dd, s);
+  cudaFreeAsync(ds, s);
+  return e == cudaSuccess ? 0 : -(int)e;
+}
+
+extern "C" int skb_gather_rows(int64_t nbox, const int64_t* idx_off, const int64_t* idx,
+                               const int64_t* col_off, const int64_t* col, int64_t ncols,
+                               const double* src, int64_t src_ld, double* dst,
+                               const int64_t* dst_off, const int64_t* dst_ld, int64_t max_rows,
+                               int64_t max_cols, void* stream) {
+  if (nbox <= 0 || max_rows <= 0 || max_cols <= 0) return 0;
+  if (nbox > 65535) return 2;
+  dim3 grid(grid_cap((max_rows * max_cols + 255) / 256, 2048), (unsigned)nbox);
+  k_gather_rows<<<grid, 256, 0, (cudaStream_t)stream>>>(idx_off, idx, col_off, col, ncols, src,
+                                                        src_ld, dst, dst_off, dst_ld);
+  SKB_LAUNCH_CHECK();
+  return 0;
+}
+
+extern "C" int skb_scatter_rows(int64_t nbox, const int64_t* idx_off, const int64_t* idx,
+                                const int64_t* col_off, const int64_t* col, int64_t ncols,
+                                const double* src, const int64_t* src_off,
+                                const int64_t* src_ld, double* dst, int64_t dst_ld,
+                                int32_t accumulate, double alpha, int64_t max_rows,
+                                int64_t max_cols, void* stream) {
+  if (nbox <= 0 || max_rows <= 0 || max_cols <= 0) return 0;
+  if (nbox > 65535) return 2;
+  dim3 grid(grid_cap((max_rows * max_cols + 255) / 256, 2048), (unsigned)nbox);
+  k_scatter_rows<<<grid, 256, 0, (cudaStream_t)stream>>>(idx_off, idx, col_off, col, ncols, src,
+                                                         src_off, src_ld, dst, dst_ld, accumulate,
+                                                         alpha);
+  SKB_LAUNCH_CHECK();
+  return 0;
+}
+
+extern "C" int skb_schur_accumulate(int64_t q, const int64_t* row_off, const int64_t* contrib,
+                                    const double* part, double* schur, void* stream) {
+  if (q <= 0) return 0;
+  dim3 grid((unsigned)((q + 127) / 128), (unsigned)q);
+  k_schur_acc<<<grid, 128, 0, (cudaStream_t)stream>>>(q, row_off, contrib, part, schur);
+  SKB_LAUNCH_CHECK();
+  return 0;
+}
+
+extern "C" int skb_diag_fill(int64_t n, double* dst, int64_t ld, double diag_val,
+                             const double* src, int64_t src_ld, double scale, void* stream) {
+  if (n <= 0) return 0;
+  k_diag_fill<<<grid_cap((n * n + 255) / 256, 4096), 256, 0, (cudaStream_t)stream>>>(
+      n, dst, ld, diag_val, src, src_ld, scale);
+  SKB_LAUNCH_CHECK();
+  return 0;
+}
+
+extern "C" int skb_version(void) { return 1; }

@@ -114,9 +114,12 @@ def star_curve(n: int, arms: int = 5, amp: float = 0.3, scale: float = 1.0) -> C
 
 
 def ellipse_curve(n: int, center=(0.0, 0.0), a: float = 1.0, b: float = 1.0,
-                  phi: float = 0.0, clockwise: bool = False) -> Curve:
-    """Ellipse with semi-axes (a, b) rotated by phi; clockwise for holes."""
+                  phi: float = 0.0, clockwise: bool = False, phase: float = 0.0) -> Curve:
+    """Ellipse with semi-axes (a, b) rotated by phi; clockwise for holes.
+    ``phase`` shifts the node parameters (t_j = 2 pi j / n + phase)."""
     t = 2 * np.pi * np.arange(n) / n
+    if phase:
+        t = t + phase
     sg = -1.0 if clockwise else 1.0
     c, s = np.cos(t), np.sin(t)
     lx, ly = a * c, sg * b * s
@@ -133,8 +136,8 @@ def ellipse_curve(n: int, center=(0.0, 0.0), a: float = 1.0, b: float = 1.0,
 
 
 def circle_curve(n: int, center=(0.0, 0.0), radius: float = 1.0,
-                 clockwise: bool = False) -> Curve:
-    return ellipse_curve(n, center, radius, radius, 0.0, clockwise)
+                 clockwise: bool = False, phase: float = 0.0) -> Curve:
+    return ellipse_curve(n, center, radius, radius, 0.0, clockwise, phase)
 
 
 # ---------------------------------------------------------------------------

@@ -1,0 +1,1105 @@
+"""Level-batched recursive skeletonization on one B200 -- the drop-in for the
+reference's ``factor`` / ``update`` / ``Factorization.solve`` / ``apply``
+(``/root/reference/pkg/src/skelsolve/skel.py``).
+
+Host Python keeps only the bookkeeping the reference does in Python (tree,
+active/far DOF lists, proxy rings, dirty sets); every floating-point operation
+of the factorization runs in libskelb200.so kernels on the device, one batched
+call per quadtree level:
+
+  per level (bottom-up, skel.py:445-449):
+    (a) ID stacks of all boxes          skb_assemble_stack     (skel.py:297-314)
+    (b) Householder pre-reduction       skb_geqrf_batched      (dense.py:56-59)
+        pivoted QR, rank, T             skb_qrcp_id_batched    (dense.py:48-79, skel.py:314-319)
+    (a) permuted self blocks            skb_assemble_self      (skel.py:282-291,316)
+    (c) Schur blocks                    skb_gemm_grouped       (skel.py:320-334)
+        X_RR LU / X_RR^-1 X_RS          skb_getrf/getrs        (skel.py:324,333)
+  _finish_top (skel.py:364-425):
+    (d) H, Psi + per-level U/V^T sweeps + deterministic q x q Schur + corner LU.
+
+Factor data stay resident in HBM; ``Factorization.factors[key]`` materialises
+a reference-style ``BoxFactors`` view (host copies) on demand.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import GEMM_DT, MAT_DT, call, ptr
+from .tree import Tree, build_tree, dirty_set, proxy_radius, refit_tree
+
+PIVOT_RATIO_FLOOR = 1e-12          # skel.py:46
+DEFAULT_PROXY_COUNT = 64           # skel.py:47
+DEFAULT_PROXY_FACTOR = 1.5         # skel.py:48
+STOKES = "stokes_dirichlet"        # kernels.py:36
+
+
+class SingularPivotError(RuntimeError):
+    """Exact zero pivot (reference dense.py:18-23)."""
+
+    def __init__(self, index: int):
+        super().__init__(f"zero pivot at elimination step {index}")
+        self.index = index
+
+
+class RootBoxExceededError(RuntimeError):
+    """A perturbed node escaped the fixed root box (reference skel.py:51-52)."""
+
+
+@dataclass(frozen=True)
+class SystemSpec:
+    """PDE selection (reference kernels.py:41-63); Stokes only on this path."""
+
+    pde: str = STOKES
+
+    def __post_init__(self):
+        if self.pde != STOKES:
+            raise ValueError("only the Stokes double-layer system is on the B200 path")
+
+    @property
+    def dof_per_node(self) -> int:
+        return 2
+
+    def augmented(self, b) -> bool:
+        return b.n_holes >= 1
+
+    def n_dofs(self, b) -> int:
+        return 2 * b.n_nodes
+
+
+# ---------------------------------------------------------------------------
+# small helpers
+# ---------------------------------------------------------------------------
+def _stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+class _Prof:
+    """Optional per-stage wall-clock breakdown (SKB_PROFILE=1 synchronises
+    after every stage; off by default so the pipeline stays asynchronous)."""
+
+    enabled = bool(int(__import__("os").environ.get("SKB_PROFILE", "0")))
+    acc: dict = {}
+    _t = 0.0
+
+    @classmethod
+    def start(cls):
+        if cls.enabled:
+            torch.cuda.synchronize()
+            cls._t = time.perf_counter()
+
+    @classmethod
+    def tick(cls, name):
+        if cls.enabled:
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            cls.acc[name] = cls.acc.get(name, 0.0) + t - cls._t
+            cls._t = t
+
+    @classmethod
+    def reset(cls):
+        cls.acc = {}
+
+
+def _dev():
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2001_11619_b200 needs a CUDA device (no CPU fallback)")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _csr(arrays):
+    lens = np.fromiter((len(a) for a in arrays), dtype=np.int64, count=len(arrays))
+    off = np.zeros(len(arrays) + 1, np.int64)
+    np.cumsum(lens, out=off[1:])
+    flat = np.concatenate(arrays).astype(np.int64) if len(arrays) else np.zeros(0, np.int64)
+    return off, flat
+
+
+def _upload(**arrays):
+    """One pinned H2D copy for several host arrays; returns device views."""
+    dev = _dev()
+    items, total = [], 0
+    for k, a in arrays.items():
+        a = np.ascontiguousarray(a)
+        total = (total + 15) // 16 * 16
+        items.append((k, a, total))
+        total += a.nbytes
+    host = torch.empty(max(total, 16), dtype=torch.uint8, pin_memory=True)
+    hn = host.numpy()
+    for k, a, o in items:
+        hn[o:o + a.nbytes] = a.view(np.uint8).reshape(-1)
+    d = host.to(dev, non_blocking=True)
+    out = {}
+    for k, a, o in items:
+        tdt = {np.dtype(np.int64): torch.int64, np.dtype(np.float64): torch.float64,
+               np.dtype(np.int32): torch.int32, np.dtype(np.uint64): torch.int64}[a.dtype]
+        out[k] = d[o:o + a.nbytes].view(tdt)
+    out["_keep"] = (host, d)
+    return out
+
+
+def _gemm(rows):
+    """Launch one grouped GEMM from a list of per-problem column dicts."""
+    if not rows:
+        return
+    n = sum(len(r["m"]) for r in rows)
+    if n == 0:
+        return
+    g = np.zeros(n, GEMM_DT)
+    o = 0
+    for r in rows:
+        c = len(r["m"])
+        for f in ("A", "B", "C", "D", "m", "n", "k", "lda", "ldb", "ldc", "ldd", "alpha", "beta",
+                  "transA", "transB"):
+            g[f][o:o + c] = r.get(f, 0)
+        o += c
+    call("skb_gemm_grouped", g, n, _stream())
+
+
+def _mats(ptrs, rows, cols, ld):
+    m = np.zeros(len(ptrs), MAT_DT)
+    m["ptr"], m["rows"], m["cols"], m["ld"] = ptrs, rows, cols, ld
+    return m
+
+
+def _addr(t: torch.Tensor) -> int:
+    return t.data_ptr()
+
+
+# ---------------------------------------------------------------------------
+# device geometry
+# ---------------------------------------------------------------------------
+class DeviceBoundary:
+    def __init__(self, b):
+        up = _upload(pos=np.ascontiguousarray(b.positions, np.float64),
+                     nrm=np.ascontiguousarray(b.normals, np.float64),
+                     w=np.ascontiguousarray(b.weights, np.float64),
+                     kap=np.ascontiguousarray(b.curvatures, np.float64))
+        self.pos, self.nrm, self.w, self.kap = up["pos"], up["nrm"], up["w"], up["kap"]
+        self._keep = up["_keep"]
+        self.n = b.n_nodes
+
+
+# ---------------------------------------------------------------------------
+# per-level factor storage
+# ---------------------------------------------------------------------------
+class BoxBatch:
+    """Factors of a batch of boxes of one level, resident on the device."""
+
+    FIELDS = ("T", "Xrr", "LU", "Xsr", "Xrsdiv", "Xss")
+
+    def __init__(self, idx, act_off, act):
+        self.idx = np.asarray(idx, np.int64)
+        self.act_off, self.act = act_off, act
+        self.nB = np.diff(act_off)
+        n = len(self.idx)
+        self.k = np.zeros(n, np.int64)
+        self.perm = np.zeros(len(act), np.int32)
+        self.gap = np.ones(n)
+        self.steps = np.zeros(n, np.int64)
+        self.ratio = np.ones(n)
+        self.info = np.full(n, -1, np.int64)
+        self.ptr = {f: np.zeros(n, np.uint64) for f in self.FIELDS}
+        self.ipiv = np.zeros(n, np.uint64)
+        self.slabs = []
+
+    @property
+    def r(self):
+        return self.nB - self.k
+
+    def skel_lists(self):
+        return [self.act[self.act_off[b] + self.perm[self.act_off[b]:self.act_off[b] + self.k[b]]]
+                for b in range(len(self.idx))]
+
+    def red_lists(self):
+        return [self.act[self.act_off[b] + self.perm[self.act_off[b] + self.k[b]:self.act_off[b + 1]]]
+                for b in range(len(self.idx))]
+
+    def take(self, sel, other, osel):
+        """Overwrite boxes ``sel`` with ``other``'s boxes ``osel`` (same DOF layout)."""
+        for s, o in zip(sel, osel):
+            a0, a1 = self.act_off[s], self.act_off[s + 1]
+            b0 = other.act_off[o]
+            self.perm[a0:a1] = other.perm[b0:b0 + (a1 - a0)]
+            self.k[s], self.gap[s], self.steps[s] = other.k[o], other.gap[o], other.steps[o]
+            self.ratio[s], self.info[s] = other.ratio[o], other.info[o]
+            for f in self.FIELDS:
+                self.ptr[f][s] = other.ptr[f][o]
+            self.ipiv[s] = other.ipiv[o]
+        have = {id(x) for x in self.slabs}
+        self.slabs.extend(x for x in other.slabs if id(x) not in have)
+
+
+class LevelFactors:
+    """All boxes of one tree level (sorted keys) with device CSR lists of
+    skeleton/redundant DOFs for the gathers of the sweeps."""
+
+    def __init__(self, lev, tree, batch: BoxBatch, cols_off, cols):
+        self.lev = lev
+        self.batch = batch
+        self.idx = batch.idx
+        self.keys = [tree.key(i) for i in self.idx]
+        self.k = batch.k.copy()
+        self.r = batch.r.copy()
+        sk = batch.skel_lists()
+        rd = batch.red_lists()
+        self.sd_off, self.sd = _csr(sk)
+        self.rd_off, self.rd = _csr(rd)
+        self.cols_off, self.cols = cols_off, cols
+        self.ncols = np.diff(cols_off)
+        up = _upload(sd_off=self.sd_off, sd=self.sd if len(self.sd) else np.zeros(1, np.int64),
+                     rd_off=self.rd_off, rd=self.rd if len(self.rd) else np.zeros(1, np.int64),
+                     c_off=cols_off, c=cols if len(cols) else np.zeros(1, np.int64))
+        self.d = up
+        self.P = {f: batch.ptr[f] for f in BoxBatch.FIELDS}
+        self.ipiv = batch.ipiv
+
+
+# ---------------------------------------------------------------------------
+# the compression pipeline for one batch of boxes
+# ---------------------------------------------------------------------------
+class _Ctx:
+    def __init__(self, spec, b, t: Tree, tol, proxy_count, proxy_factor):
+        self.spec, self.b, self.t = spec, b, t
+        self.tol, self.P, self.factor = float(tol), int(proxy_count), float(proxy_factor)
+        if self.P < 8:
+            raise ValueError("need at least 8 proxy nodes")
+        self._g = None
+        self.dof_xy = np.repeat(b.positions, 2, axis=0)
+        th = 2 * np.pi * np.arange(self.P) / self.P
+        self.cs = np.stack([np.cos(th), np.sin(th)], axis=1)
+        self.xss = {}        # tree box index -> (device address, k)
+        self.stats = {"kernel_s": {}}
+
+    @property
+    def g(self) -> DeviceBoundary:
+        if self._g is None:
+            self._g = DeviceBoundary(self.b)
+        return self._g
+
+    # -- host bookkeeping ---------------------------------------------------
+    def far_lists(self, idx, act_of):
+        """F_int per box (reference _Compressor.far_dofs, skel.py:258-280)."""
+        t = self.t
+        rp = proxy_radius(t.hw[idx], self.factor)
+        nbr = t.neighbors[idx]
+        bl_n, s_n = np.nonzero(nbr >= 0)
+        src_n = nbr[bl_n, s_n]
+        mask, cand = t.coarse_leaves_mask(idx, rp)
+        bl_c, c_c = np.nonzero(mask)
+        src_c = cand[c_c]
+        pb = np.concatenate([bl_n, bl_c]).astype(np.int64)
+        ps = np.concatenate([src_n, src_c]).astype(np.int64)
+        order = np.argsort(pb, kind="stable")
+        pb, ps = pb[order], ps[order]
+        B = len(idx)
+        if len(ps) == 0:
+            return np.zeros(B + 1, np.int64), np.zeros(0, np.int64)
+        parts = [act_of[s] for s in ps]
+        lens = np.fromiter((len(p) for p in parts), np.int64, len(parts))
+        flat = np.concatenate(parts)
+        owner = np.repeat(pb, lens)
+        d = self.dof_xy[flat] - t.center[idx][owner]
+        d2 = (d ** 2).sum(axis=1)
+        keep = d2 < (rp * rp)[owner]
+        F = flat[keep]
+        cnt = np.bincount(owner[keep], minlength=B)
+        off = np.zeros(B + 1, np.int64)
+        np.cumsum(cnt, out=off[1:])
+        return off, F
+
+    def proxies(self, idx):
+        """Proxy rings + radial normals + weights (kernels.py:263-273, 340-342)."""
+        rp = proxy_radius(self.t.hw[idx], self.factor)
+        pts = self.t.center[idx][:, None, :] + rp[:, None, None] * self.cs[None]
+        acc = pts[:, 0, :].copy()
+        for p in range(1, self.P):
+            acc = acc + pts[:, p, :]
+        ctr = acc / self.P
+        pn = pts - ctr[:, None, :]
+        pn = pn / np.sqrt((pn * pn).sum(axis=2))[:, :, None]
+        pw = 2 * np.pi * rp / self.P
+        return pts, pn, pw
+
+    def child_desc(self, idx, act_of):
+        co = np.full((len(idx), 5), -1, np.int64)
+        cx = np.zeros((len(idx), 4), np.uint64)
+        t = self.t
+        for bi, i in enumerate(idx):
+            ch = t.children_of(i)
+            if not ch:
+                continue
+            off = 0
+            co[bi, 0] = 0
+            for c, j in enumerate(ch):
+                p, kc = self.xss[j]
+                off += kc
+                co[bi, c + 1] = off
+                cx[bi, c] = p
+        return co, cx
+
+    # -- device pipeline ----------------------------------------------------
+    def compress(self, idx, act_of, kmin=None) -> BoxBatch:
+        """Compress a batch of same-level boxes (reference compress_box, skel.py:293-338)."""
+        t, P = self.t, self.P
+        _Prof.start()
+        idx = np.asarray(idx, np.int64)
+        B = len(idx)
+        act_off, act = _csr([act_of[i] for i in idx])
+        nB = np.diff(act_off)
+        far_off, far = self.far_lists(idx, act_of)
+        nF = np.diff(far_off)
+        pts, pn, pw = self.proxies(idx)
+        rows = 2 * nF + 6 * P + 2
+        sizes = rows * nB
+        stack_off = np.zeros(B + 1, np.int64)
+        np.cumsum(sizes, out=stack_off[1:])
+        dev = _dev()
+        _Prof.tick("host_far_proxy")
+        stack = torch.empty(max(int(stack_off[-1]), 1), dtype=torch.float64, device=dev)
+        up = _upload(act_off=act_off, act=act if len(act) else np.zeros(1, np.int64),
+                     far_off=far_off, far=far if len(far) else np.zeros(1, np.int64),
+                     pts=pts.reshape(-1), pn=pn.reshape(-1), pw=pw, stack_off=stack_off[:-1])
+        s = _stream()
+        call("skb_assemble_stack", ptr(self.g.pos), ptr(self.g.nrm), ptr(self.g.w), B,
+             ptr(up["act_off"]), ptr(up["act"]), ptr(up["far_off"]), ptr(up["far"]),
+             ptr(up["pts"]), ptr(up["pn"]), ptr(up["pw"]), P, ptr(up["stack_off"]), ptr(stack),
+             int(nB.max(initial=0)), int((nF + P + 1).max(initial=0)), s)
+        _Prof.tick("a_stack")
+        base = _addr(stack)
+        A = (base + 8 * stack_off[:-1]).astype(np.int64)
+        pre = rows > nB
+        if pre.any():
+            call("skb_geqrf_batched", int(pre.sum()), np.ascontiguousarray(rows[pre]),
+                 np.ascontiguousarray(nB[pre]),
+                 np.ascontiguousarray(rows[pre]),
+                 np.ascontiguousarray(A[pre]), s)
+        _Prof.tick("b_geqrf")
+        m_q = np.where(pre, nB, rows).astype(np.int64)
+        kmin_a = np.zeros(B, np.int64) if kmin is None else np.asarray(kmin, np.int64)
+        perm_d = torch.empty(max(len(act), 1), dtype=torch.int32, device=dev)
+        diag_d = torch.empty(max(len(act), 1), dtype=torch.float64, device=dev)
+        out_i = torch.empty(2 * B, dtype=torch.int32, device=dev)
+        gap_d = torch.empty(B, dtype=torch.float64, device=dev)
+        lda = rows.astype(np.int64)
+        call("skb_qrcp_id_batched", B, m_q, nB, lda,
+             A, kmin_a, self.tol, act_off, ptr(perm_d),
+             ptr(diag_d), ptr(out_i), ptr(out_i) + 4 * B, ptr(gap_d), s)
+        _Prof.tick("b_qrcp")
+        bt = BoxBatch(idx, act_off, act)
+        bt.perm[:] = perm_d[:len(act)].cpu().numpy()      # sync point 1 (sizes for (c))
+        oi = out_i.cpu().numpy()
+        bt.k[:] = oi[:B]
+        bt.steps[:] = oi[B:]
+        bt.gap[:] = gap_d.cpu().numpy()
+        k = bt.k
+        r = nB - k
+        # ---- factor storage (one slab) and scratch
+        sz = np.stack([k * r, r * r, r * r, k * r, r * k, k * k], axis=1)
+        tot = sz.sum(axis=1)
+        boff = np.zeros(B + 1, np.int64)
+        np.cumsum(tot, out=boff[1:])
+        slab = torch.empty(max(int(boff[-1]), 1), dtype=torch.float64, device=dev)
+        ipiv = torch.empty(max(int(r.sum()), 1), dtype=torch.int32, device=dev)
+        bt.slabs.append(slab)
+        bt.slabs.append(ipiv)
+        sb = _addr(slab)
+        fo = boff[:-1].copy()
+        for fi, f in enumerate(BoxBatch.FIELDS):
+            bt.ptr[f][:] = (sb + 8 * fo).astype(np.uint64)
+            fo = fo + sz[:, fi]
+        ioff = np.zeros(B + 1, np.int64)
+        np.cumsum(r, out=ioff[1:])
+        bt.ipiv[:] = (_addr(ipiv) + 4 * ioff[:-1]).astype(np.uint64)
+        E_off = np.zeros(B + 1, np.int64)
+        np.cumsum(nB * nB, out=E_off[1:])
+        Ebuf = torch.empty(max(int(E_off[-1]), 1), dtype=torch.float64, device=dev)
+        Xrs = torch.empty(max(int((r * k).sum()), 1), dtype=torch.float64, device=dev)
+        # ---- T: column-major in place over R12 -> row-major k x r
+        perm_ptrs = (_addr(perm_d) + 4 * act_off[:-1]).astype(np.int64)
+        call("skb_id_T_batched", B, A, lda, k.astype(np.int64), nB.astype(np.int64), perm_ptrs,
+             bt.ptr["T"].astype(np.int64), s)
+        # ---- permuted self blocks with children's Xss
+        co, cx = self.child_desc(idx, act_of)
+        up2 = _upload(co=co.reshape(-1), cx=cx.reshape(-1), E_off=E_off[:-1], E_ld=nB.astype(np.int64))
+        call("skb_assemble_self", ptr(self.g.pos), ptr(self.g.nrm), ptr(self.g.w), ptr(self.g.kap),
+             B, ptr(up["act_off"]), ptr(up["act"]), ptr(up["act_off"]), ptr(perm_d),
+             ptr(up2["co"]), ptr(up2["cx"]), ptr(Ebuf), ptr(up2["E_off"]), ptr(up2["E_ld"]),
+             int(nB.max(initial=0)), s)
+        _Prof.tick("a_self_T")
+        E = (_addr(Ebuf) + 8 * E_off[:-1]).astype(np.uint64)
+        xoff = np.zeros(B + 1, np.int64)
+        np.cumsum(r * k, out=xoff[1:])
+        Xrs_p = (_addr(Xrs) + 8 * xoff[:-1]).astype(np.uint64)
+        Ess, Esr = E, E + (8 * k).astype(np.uint64)
+        Ers = E + (8 * k * nB).astype(np.uint64)
+        Err = Ers + (8 * k).astype(np.uint64)
+        T, Xsr, Xrr = bt.ptr["T"], bt.ptr["Xsr"], bt.ptr["Xrr"]
+        one, mone = np.ones(B), -np.ones(B)
+        # X_sr = E_SR - E_SS T ; X_rs = E_RS - T^T E_SS ; X_rr = E_RR - E_RS T   (skel.py:321-332)
+        _gemm([
+            dict(A=Ess, B=T, C=Esr, D=Xsr, m=k, n=r, k=k, lda=nB, ldb=r, ldc=nB, ldd=r,
+                 alpha=mone, beta=one),
+            dict(A=T, B=Ess, C=Ers, D=Xrs_p, m=r, n=k, k=k, lda=r, ldb=nB, ldc=nB, ldd=k,
+                 alpha=mone, beta=one, transA=1),
+            dict(A=Ers, B=T, C=Err, D=Xrr, m=r, n=r, k=k, lda=nB, ldb=r, ldc=nB, ldd=r,
+                 alpha=mone, beta=one),
+        ])
+        # X_rr -= T^T X_sr
+        _gemm([dict(A=T, B=Xsr, C=Xrr, D=Xrr, m=r, n=r, k=k, lda=r, ldb=r, ldc=r, ldd=r,
+                    alpha=mone, beta=one, transA=1)])
+        _Prof.tick("c_schur_gemm")
+        LU = bt.ptr["LU"]
+        call("skb_copy2d_batched", B, _mats(LU, r, r, r),
+             _mats(Xrr, r, r, r), 0, s)
+        info_d = torch.empty(B, dtype=torch.int32, device=dev)
+        ratio_d = torch.empty(B, dtype=torch.float64, device=dev)
+        call("skb_getrf_batched", B, _mats(LU, r, r, r), bt.ipiv,
+             ptr(info_d), ptr(ratio_d), s)
+        _Prof.tick("c_getrf")
+        # X_rs_div = X_rr^-1 X_rs (skel.py:333)
+        Xrsdiv = bt.ptr["Xrsdiv"]
+        call("skb_copy2d_batched", B, _mats(Xrsdiv, r, k, k),
+             _mats(Xrs_p, r, k, k), 0, s)
+        call("skb_getrs_batched", B, _mats(LU, r, r, r), bt.ipiv,
+             _mats(Xrsdiv, r, k, k), s)
+        # Xss_mod = E_SS - X_sr X_rs_div (skel.py:334)
+        _gemm([dict(A=Xsr, B=Xrsdiv, C=Ess, D=bt.ptr["Xss"], m=k, n=k, k=r, lda=r, ldb=k,
+                    ldc=nB, ldd=k, alpha=mone, beta=one)])
+        _Prof.tick("c_getrs_xss")
+        bt.info[:] = info_d.cpu().numpy()                 # sync point 2 (migration check)
+        bt.ratio[:] = ratio_d.cpu().numpy()
+        bt._scratch = None
+        del stack, Ebuf, Xrs
+        return bt
+
+    def compress_level(self, idx, act_of) -> BoxBatch:
+        bt = self.compress(idx, act_of)
+        # R -> S migration while the X_RR pivot ratio is below the floor (skel.py:317-330)
+        while True:
+            kk = bt.k
+            bad = ((bt.info >= 0) | (bt.ratio < PIVOT_RATIO_FLOOR)) & (kk < bt.nB)
+            if not bad.any():
+                break
+            sel = np.flatnonzero(bad)
+            knew = np.minimum(bt.nB[sel], kk[sel] + np.maximum(1, (bt.nB[sel] - kk[sel]) // 8))
+            sub = self.compress(bt.idx[sel], act_of, kmin=knew)
+            bt.take(sel, sub, np.arange(len(sel)))
+        return bt
+
+
+# ---------------------------------------------------------------------------
+# Factorization
+# ---------------------------------------------------------------------------
+class BoxFactors:
+    """Reference-style per-box view (skel.py:55-85), host copies on demand."""
+
+    def __init__(self, key, b_dofs, S_loc, R_loc, mats):
+        self.key, self.b_dofs, self.S_loc, self.R_loc = key, b_dofs, S_loc, R_loc
+        self._mats = mats
+
+    @property
+    def skel_dofs(self):
+        return self.b_dofs[self.S_loc]
+
+    @property
+    def red_dofs(self):
+        return self.b_dofs[self.R_loc]
+
+    def __getattr__(self, name):
+        m = self.__dict__.get("_mats")
+        if m is not None and name in m:
+            return m[name]()
+        raise AttributeError(name)
+
+
+def _fetch(addr, rows, cols):
+    """Host copy of a device row-major (rows x cols) block at a raw address."""
+    rows, cols = int(rows), int(cols)
+    if rows * cols == 0:
+        return np.zeros((rows, cols))
+    t = torch.empty((rows, cols), dtype=torch.float64, device=_dev())
+    call("skb_copy2d_batched", 1, _mats([_addr(t)], [rows], [cols], [cols]),
+         _mats(np.array([addr], np.uint64), [rows], [cols], [cols]), 0, _stream())
+    return t.cpu().numpy()
+
+
+class _FactorsView:
+    """Lazy mapping key -> BoxFactors (reference Factorization.factors)."""
+
+    def __init__(self, fct):
+        self._f = fct
+        self._where = {}
+        for li, L in enumerate(fct.levels):
+            for bi, key in enumerate(L.keys):
+                self._where[key] = (li, bi)
+
+    def __len__(self):
+        return len(self._where)
+
+    def __iter__(self):
+        return iter(self._where)
+
+    def __contains__(self, key):
+        return tuple(key) in self._where
+
+    def keys(self):
+        return self._where.keys()
+
+    def __getitem__(self, key):
+        li, bi = self._where[tuple(key)]
+        L = self._f.levels[li]
+        bt = L.batch
+        a0, a1 = bt.act_off[bi], bt.act_off[bi + 1]
+        dofs = bt.act[a0:a1]
+        perm = bt.perm[a0:a1].astype(np.int64)
+        k, r = int(L.k[bi]), int(L.r[bi])
+        P = L.P
+        mats = {
+            "T": lambda: _fetch(P["T"][bi], k, r),
+            "X_rr": lambda: _fetch(P["Xrr"][bi], r, r),
+            "X_sr": lambda: _fetch(P["Xsr"][bi], k, r),
+            "X_rs_div": lambda: _fetch(P["Xrsdiv"][bi], r, k),
+            "Xss_mod": lambda: _fetch(P["Xss"][bi], k, k),
+        }
+        return BoxFactors(tuple(key), dofs, perm[:k], perm[k:], mats)
+
+
+class Factorization:
+    """Device-resident factorization (reference skel.py:88-221)."""
+
+    def __init__(self, spec, boundary, tree, tol, proxy_count, proxy_factor, levels, root_dofs,
+                 E_root, top, top_ipiv, UH, PsiV, UH_div, q, ctx, stats):
+        self.spec, self.boundary, self.tree = spec, boundary, tree
+        self.tol, self.proxy_count, self.proxy_factor = tol, proxy_count, proxy_factor
+        self.levels = levels                # bottom-up (reference sweep_levels order)
+        self.root_dofs = root_dofs
+        self.E_root, self.top, self.top_ipiv = E_root, top, top_ipiv
+        self.UH, self.PsiV, self.UH_div = UH, PsiV, UH_div
+        self.q = q
+        self._ctx = ctx
+        self.stats = stats
+        rd = root_dofs if len(root_dofs) else np.zeros(1, np.int64)
+        self._root_d = _upload(r=rd)
+        self.factors = _FactorsView(self)
+
+    @property
+    def n_dofs(self) -> int:
+        return 2 * self.boundary.n_nodes
+
+    @property
+    def n_aug(self) -> int:
+        return self.q
+
+    @property
+    def dim(self) -> int:
+        return self.n_dofs + self.q
+
+    @property
+    def sweep_levels(self):
+        return [(L.lev, L.keys) for L in self.levels]
+
+    # ---- device sweeps -----------------------------------------------------
+    def _gather(self, L, which, x, nr, buf):
+        off, dd = (L.d["sd_off"], L.d["sd"]) if which == "s" else (L.d["rd_off"], L.d["rd"])
+        cnt = L.k if which == "s" else L.r
+        o = np.zeros(len(cnt) + 1, np.int64)
+        np.cumsum(cnt * nr, out=o[1:])
+        up = _upload(o=o[:-1], ld=np.full(len(cnt), nr, np.int64))
+        call("skb_gather_rows", len(cnt), ptr(off), ptr(dd), None, None, nr, ptr(x), nr,
+             ptr(buf), ptr(up["o"]), ptr(up["ld"]), int(cnt.max(initial=0)), nr, _stream())
+        return (_addr(buf) + 8 * o[:-1]).astype(np.uint64), up
+
+    def _scatter(self, L, which, x, nr, bptr, keep):
+        off, dd = (L.d["sd_off"], L.d["sd"]) if which == "s" else (L.d["rd_off"], L.d["rd"])
+        cnt = L.k if which == "s" else L.r
+        base = int(bptr[0]) if len(bptr) else 0
+        up = _upload(o=((bptr.astype(np.int64) - base) // 8), ld=np.full(len(cnt), nr, np.int64))
+        keep.append(up)
+        call("skb_scatter_rows", len(cnt), ptr(off), ptr(dd), None, None, nr, base,
+             ptr(up["o"]), ptr(up["ld"]), ptr(x), nr, 0, 1.0, int(cnt.max(initial=0)), nr,
+             _stream())
+
+    def _solve_dev(self, x: torch.Tensor) -> torch.Tensor:
+        """In-place solve on a (dim, nrhs) row-major device tensor (skel.py:166-221)."""
+        nr = x.shape[1]
+        nd, q = self.n_dofs, self.q
+        s = _stream()
+        dev = x.device
+        keep = []
+        for L in self.levels:                       # _level_up, skel.py:195-208
+            B = len(L.k)
+            xs = torch.empty(max(int(L.k.sum()) * nr, 1), dtype=torch.float64, device=dev)
+            xr = torch.empty(max(int(L.r.sum()) * nr, 1), dtype=torch.float64, device=dev)
+            ps, u1 = self._gather(L, "s", x, nr, xs)
+            pr, u2 = self._gather(L, "r", x, nr, xr)
+            keep += [u1, u2, xs, xr]
+            one, mone = np.ones(B), -np.ones(B)
+            _gemm([dict(A=L.P["T"], B=ps, C=pr, D=pr, m=L.r, n=nr, k=L.k, lda=L.r, ldb=nr,
+                        ldc=nr, ldd=nr, alpha=mone, beta=one, transA=1)])
+            call("skb_getrs_batched", B, _mats(L.P["LU"], L.r, L.r, L.r),
+                 L.ipiv, _mats(pr, L.r, nr, nr), s)
+            _gemm([dict(A=L.P["Xsr"], B=pr, C=ps, D=ps, m=L.k, n=nr, k=L.r, lda=L.r, ldb=nr,
+                        ldc=nr, ldd=nr, alpha=mone, beta=one)])
+            self._scatter(L, "s", x, nr, ps, keep)
+            self._scatter(L, "r", x, nr, pr, keep)
+        ns = len(self.root_dofs)
+        rd = self._root_d
+        if q:                                        # skel.py:180-188
+            z = torch.empty((nd, nr), dtype=torch.float64, device=dev)
+            z.copy_(x[:nd])
+            call("skb_fill_rows", ns, ptr(rd["r"]), ptr(z), nr, None, nr, 0.0, s)
+            top_rhs = torch.empty((ns + q, nr), dtype=torch.float64, device=dev)
+            up = _upload(o=np.zeros(1, np.int64), ld=np.array([nr], np.int64),
+                         ro=np.array([0, ns], np.int64))
+            keep.append(up)
+            call("skb_gather_rows", 1, ptr(up["ro"]), ptr(rd["r"]), None, None, nr, ptr(x), nr,
+                 ptr(top_rhs), ptr(up["o"]), ptr(up["ld"]), ns, nr, s)
+            _gemm([dict(A=np.array([_addr(self.PsiV)], np.uint64),
+                        B=np.array([_addr(z)], np.uint64),
+                        C=np.array([_addr(x) + 8 * nd * nr], np.uint64),
+                        D=np.array([_addr(top_rhs) + 8 * ns * nr], np.uint64),
+                        m=[q], n=[nr], k=[nd], lda=[q], ldb=[nr], ldc=[nr], ldd=[nr],
+                        alpha=[-1.0], beta=[1.0], transA=[1])])
+            call("skb_getrs_batched", 1, _mats([_addr(self.top)], [ns + q], [ns + q],
+                                              [ns + q]),
+                 np.array([_addr(self.top_ipiv)], np.uint64),
+                 _mats([_addr(top_rhs)], [ns + q], [nr], [nr]), s)
+            call("skb_scatter_rows", 1, ptr(up["ro"]), ptr(rd["r"]), None, None, nr,
+                 _addr(top_rhs), ptr(up["o"]), ptr(up["ld"]), ptr(x), nr, 0, 1.0, ns, nr, s)
+            x[nd:].copy_(top_rhs[ns:])
+            # x[:nd] -= UH_div lam (UH_div rows of root DOFs are exactly zero)
+            _gemm([dict(A=np.array([_addr(self.UH_div)], np.uint64),
+                        B=np.array([_addr(top_rhs) + 8 * ns * nr], np.uint64),
+                        C=np.array([_addr(x)], np.uint64), D=np.array([_addr(x)], np.uint64),
+                        m=[nd], n=[nr], k=[q], lda=[q], ldb=[nr], ldc=[nr], ldd=[nr],
+                        alpha=[-1.0], beta=[1.0])])
+            keep += [z, top_rhs]
+        else:
+            top_rhs = torch.empty((ns, nr), dtype=torch.float64, device=dev)
+            up = _upload(o=np.zeros(1, np.int64), ld=np.array([nr], np.int64),
+                         ro=np.array([0, ns], np.int64))
+            keep += [up, top_rhs]
+            call("skb_gather_rows", 1, ptr(up["ro"]), ptr(rd["r"]), None, None, nr, ptr(x), nr,
+                 ptr(top_rhs), ptr(up["o"]), ptr(up["ld"]), ns, nr, s)
+            call("skb_getrs_batched", 1, _mats([_addr(self.top)], [ns], [ns], [ns]),
+                 np.array([_addr(self.top_ipiv)], np.uint64),
+                 _mats([_addr(top_rhs)], [ns], [nr], [nr]), s)
+            call("skb_scatter_rows", 1, ptr(up["ro"]), ptr(rd["r"]), None, None, nr,
+                 _addr(top_rhs), ptr(up["o"]), ptr(up["ld"]), ptr(x), nr, 0, 1.0, ns, nr, s)
+        for L in reversed(self.levels):             # _level_down, skel.py:210-221
+            B = len(L.k)
+            xs = torch.empty(max(int(L.k.sum()) * nr, 1), dtype=torch.float64, device=dev)
+            xr = torch.empty(max(int(L.r.sum()) * nr, 1), dtype=torch.float64, device=dev)
+            ps, u1 = self._gather(L, "s", x, nr, xs)
+            pr, u2 = self._gather(L, "r", x, nr, xr)
+            keep += [u1, u2, xs, xr]
+            one, mone = np.ones(B), -np.ones(B)
+            _gemm([dict(A=L.P["Xrsdiv"], B=ps, C=pr, D=pr, m=L.r, n=nr, k=L.k, lda=L.k, ldb=nr,
+                        ldc=nr, ldd=nr, alpha=mone, beta=one)])
+            _gemm([dict(A=L.P["T"], B=pr, C=ps, D=ps, m=L.k, n=nr, k=L.r, lda=L.r, ldb=nr,
+                        ldc=nr, ldd=nr, alpha=mone, beta=one)])
+            self._scatter(L, "s", x, nr, ps, keep)
+            self._scatter(L, "r", x, nr, pr, keep)
+        self._keep = keep
+        return x
+
+    def solve(self, rhs, workers: int = 1):
+        """Solve A x = rhs for (dim,) or (dim, nrhs) input (reference skel.py:166-193)."""
+        is_t = isinstance(rhs, torch.Tensor)
+        r = rhs if is_t else np.asarray(rhs, float)
+        if r.shape[0] != self.dim:
+            raise ValueError(f"dimension mismatch: got {r.shape[0]}, need {self.dim}")
+        vec = r.ndim == 1
+        if is_t:
+            x = r.to(device=_dev(), dtype=torch.float64).reshape(self.dim, -1).clone()
+        else:
+            x = torch.from_numpy(np.ascontiguousarray(r.reshape(self.dim, -1))).to(_dev())
+        x = x.contiguous()
+        self._solve_dev(x)
+        if is_t:
+            return x.reshape(-1) if vec else x
+        out = x.cpu().numpy()
+        return out.reshape(-1) if vec else out
+
+    def apply(self, x, workers: int = 1):
+        """Compressed product ~ A x (reference skel.py:126-164); vectors or matrices."""
+        is_t = isinstance(x, torch.Tensor)
+        xa = x if is_t else np.asarray(x, float)
+        if xa.shape[0] != self.dim:
+            raise ValueError(f"dimension mismatch: got {xa.shape[0]}, need {self.dim}")
+        vec = xa.ndim == 1
+        dev = _dev()
+        X = (xa.to(device=dev, dtype=torch.float64) if is_t
+             else torch.from_numpy(np.ascontiguousarray(xa)).to(dev)).reshape(self.dim, -1)
+        nr = X.shape[1]
+        nd, q = self.n_dofs, self.q
+        s = _stream()
+        y = X[:nd].clone().contiguous()
+        lam = X[nd:].clone().contiguous()
+        keep = []
+        # V^-1 upward: y_S += T y_R ; y_R += X_rs_div y_S
+        for L in self.levels:
+            B = len(L.k)
+            xs = torch.empty(max(int(L.k.sum()) * nr, 1), dtype=torch.float64, device=dev)
+            xr = torch.empty(max(int(L.r.sum()) * nr, 1), dtype=torch.float64, device=dev)
+            ps, u1 = self._gather(L, "s", y, nr, xs)
+            pr, u2 = self._gather(L, "r", y, nr, xr)
+            keep += [u1, u2, xs, xr]
+            one = np.ones(B)
+            _gemm([dict(A=L.P["T"], B=pr, C=ps, D=ps, m=L.k, n=nr, k=L.r, lda=L.r, ldb=nr,
+                        ldc=nr, ldd=nr, alpha=one, beta=one)])
+            _gemm([dict(A=L.P["Xrsdiv"], B=ps, C=pr, D=pr, m=L.r, n=nr, k=L.k, lda=L.k, ldb=nr,
+                        ldc=nr, ldd=nr, alpha=one, beta=one)])
+            self._scatter(L, "s", y, nr, ps, keep)
+            self._scatter(L, "r", y, nr, pr, keep)
+        bottom = None
+        if q:
+            bottom = torch.empty((q, nr), dtype=torch.float64, device=dev)
+            _gemm([dict(A=np.array([_addr(self.PsiV)], np.uint64), B=np.array([_addr(y)], np.uint64),
+                        C=np.array([_addr(lam)], np.uint64), D=np.array([_addr(bottom)], np.uint64),
+                        m=[q], n=[nr], k=[nd], lda=[q], ldb=[nr], ldc=[nr], ldd=[nr],
+                        alpha=[1.0], beta=[-1.0], transA=[1])])
+        # X_D: y_R <- X_rr y_R (stash y_R), y_root <- E_root y_root, y += UH lam
+        stash = []
+        for L in self.levels:
+            B = len(L.k)
+            xr = torch.empty(max(int(L.r.sum()) * nr, 1), dtype=torch.float64, device=dev)
+            yr = torch.empty(max(int(L.r.sum()) * nr, 1), dtype=torch.float64, device=dev)
+            pr, u2 = self._gather(L, "r", y, nr, xr)
+            o = np.zeros(B + 1, np.int64)
+            np.cumsum(L.r * nr, out=o[1:])
+            py = (_addr(yr) + 8 * o[:-1]).astype(np.uint64)
+            _gemm([dict(A=L.P["Xrr"], B=pr, D=py, m=L.r, n=nr, k=L.r, lda=L.r, ldb=nr, ldd=nr,
+                        alpha=np.ones(B), beta=np.zeros(B))])
+            self._scatter(L, "r", y, nr, py, keep)
+            stash.append((pr, xr))
+            keep += [u2, yr]
+        ns = len(self.root_dofs)
+        rd = self._root_d
+        up = _upload(o=np.zeros(1, np.int64), ld=np.array([nr], np.int64),
+                     ro=np.array([0, ns], np.int64))
+        yroot = torch.empty((ns, nr), dtype=torch.float64, device=dev)
+        yroot2 = torch.empty((ns, nr), dtype=torch.float64, device=dev)
+        call("skb_gather_rows", 1, ptr(up["ro"]), ptr(rd["r"]), None, None, nr, ptr(y), nr,
+             ptr(yroot), ptr(up["o"]), ptr(up["ld"]), ns, nr, s)
+        _gemm([dict(A=np.array([_addr(self.E_root)], np.uint64), B=np.array([_addr(yroot)], np.uint64),
+                    D=np.array([_addr(yroot2)], np.uint64), m=[ns], n=[nr], k=[ns], lda=[ns],
+                    ldb=[nr], ldd=[nr], alpha=[1.0], beta=[0.0])])
+        call("skb_scatter_rows", 1, ptr(up["ro"]), ptr(rd["r"]), None, None, nr, _addr(yroot2),
+             ptr(up["o"]), ptr(up["ld"]), ptr(y), nr, 0, 1.0, ns, nr, s)
+        keep += [up, yroot, yroot2]
+        if q:
+            _gemm([dict(A=np.array([_addr(self.UH)], np.uint64), B=np.array([_addr(lam)], np.uint64),
+                        C=np.array([_addr(y)], np.uint64), D=np.array([_addr(y)], np.uint64),
+                        m=[nd], n=[nr], k=[q], lda=[q], ldb=[nr], ldc=[nr], ldd=[nr],
+                        alpha=[1.0], beta=[1.0])])
+        # U^-1 downward: t = stash + UH_div[rd] lam ; y_S += X_sr t ; y_R += T^T y_S
+        for L, (pr, xr) in zip(reversed(self.levels), reversed(stash)):
+            B = len(L.k)
+            one = np.ones(B)
+            if q:
+                ud = torch.empty(max(int(L.r.sum()) * q, 1), dtype=torch.float64, device=dev)
+                pu, u3 = self._gather(L, "r", self.UH_div, q, ud)
+                _gemm([dict(A=pu, B=np.full(B, _addr(lam), np.uint64), C=pr, D=pr, m=L.r, n=nr,
+                            k=np.full(B, q), lda=np.full(B, q), ldb=nr, ldc=nr, ldd=nr,
+                            alpha=one, beta=one)])
+                keep += [ud, u3]
+            xs = torch.empty(max(int(L.k.sum()) * nr, 1), dtype=torch.float64, device=dev)
+            ps, u1 = self._gather(L, "s", y, nr, xs)
+            _gemm([dict(A=L.P["Xsr"], B=pr, C=ps, D=ps, m=L.k, n=nr, k=L.r, lda=L.r, ldb=nr,
+                        ldc=nr, ldd=nr, alpha=one, beta=one)])
+            yr = torch.empty(max(int(L.r.sum()) * nr, 1), dtype=torch.float64, device=dev)
+            py2, u4 = self._gather(L, "r", y, nr, yr)
+            _gemm([dict(A=L.P["T"], B=ps, C=py2, D=py2, m=L.r, n=nr, k=L.k, lda=L.r, ldb=nr,
+                        ldc=nr, ldd=nr, alpha=one, beta=one, transA=1)])
+            self._scatter(L, "s", y, nr, ps, keep)
+            self._scatter(L, "r", y, nr, py2, keep)
+            keep += [xs, u1, yr, u4]
+        out = torch.cat([y, bottom], dim=0) if q else y
+        torch.cuda.current_stream().synchronize()
+        if is_t:
+            return out.reshape(-1) if vec else out
+        o = out.cpu().numpy()
+        return o.reshape(-1) if vec else o
+
+
+# ---------------------------------------------------------------------------
+# _finish_top and the drivers
+# ---------------------------------------------------------------------------
+def _hole_columns(t: Tree, b, idx):
+    """Augmentation columns touched by each box: 3 per hole with nodes in the box."""
+    if b.n_holes == 0:
+        return np.zeros(len(idx) + 1, np.int64), np.zeros(0, np.int64)
+    cof = b.curve_of_node()
+    lists = []
+    for i in idx:
+        cur = np.unique(cof[t.nodes_of(i)])
+        h = cur[cur >= 1] - 1
+        lists.append((3 * h[:, None] + np.arange(3)[None, :]).ravel())
+    return _csr(lists)
+
+
+def _finish_top(ctx: _Ctx, levels, act_of):
+    """Root block, augmentation sweep and corner LU (reference skel.py:364-425)."""
+    t, b = ctx.t, ctx.b
+    dev = _dev()
+    s = _stream()
+    root = 0
+    if t.is_leaf[root]:
+        rd = (2 * t.nodes_of(root)[:, None] + np.arange(2)[None, :]).ravel()
+    else:
+        rd = np.concatenate([ctx.skel_of[c] for c in t.children_of(root)])
+    act_of[root] = rd
+    ns = len(rd)
+    nd = 2 * b.n_nodes
+    q = 3 * b.n_holes if ctx.spec.augmented(b) else 0
+    co, cx = ctx.child_desc(np.array([root]), act_of)
+    E_root = torch.empty((max(ns, 1), max(ns, 1)), dtype=torch.float64, device=dev)
+    up = _upload(ao=np.array([0, ns], np.int64), a=rd if ns else np.zeros(1, np.int64),
+                 co=co.reshape(-1), cx=cx.reshape(-1), eo=np.zeros(1, np.int64),
+                 eld=np.array([ns], np.int64))
+    call("skb_assemble_self", ptr(ctx.g.pos), ptr(ctx.g.nrm), ptr(ctx.g.w), ptr(ctx.g.kap), 1,
+         ptr(up["ao"]), ptr(up["a"]), None, None, ptr(up["co"]), ptr(up["cx"]), ptr(E_root),
+         ptr(up["eo"]), ptr(up["eld"]), ns, s)
+    UH = PsiV = UH_div = None
+    if q:
+        UH = torch.empty((nd, q), dtype=torch.float64, device=dev)
+        PsiV = torch.empty((nd, q), dtype=torch.float64, device=dev)
+        UH_div = torch.zeros((nd, q), dtype=torch.float64, device=dev)
+        hc = torch.from_numpy(np.ascontiguousarray(b.hole_centers, np.float64)).to(dev)
+        call("skb_assemble_aug", ptr(ctx.g.pos), ptr(ctx.g.w), b.n_nodes, ptr(hc), b.n_holes,
+             np.ascontiguousarray(b.offsets, np.int64), ptr(UH), ptr(PsiV), s)
+        schur = torch.zeros((q, q), dtype=torch.float64, device=dev)
+        _Prof.start()
+        for L in levels:
+            _aug_level(L, UH, PsiV, UH_div, schur, q)
+        _Prof.tick("d_aug_sweep")
+        n = ns + q
+        top = torch.empty((n, n), dtype=torch.float64, device=dev)
+        call("skb_copy2d_batched", 1, _mats([_addr(top)], [ns], [ns], [n]),
+             _mats([_addr(E_root)], [ns], [ns], [ns]), 0, s)
+        # corner[:ns, ns:] = UH[root]; corner[ns:, :ns] = PsiV[root]^T; corner[ns:, ns:] = -I - schur
+        up2 = _upload(o=np.array([ns], np.int64), ld=np.array([n], np.int64),
+                      o0=np.zeros(1, np.int64), ldq=np.array([q], np.int64))
+        call("skb_gather_rows", 1, ptr(up["ao"]), ptr(up["a"]), None, None, q, ptr(UH), q,
+             ptr(top), ptr(up2["o"]), ptr(up2["ld"]), ns, q, s)
+        tmp = torch.empty((max(ns, 1), q), dtype=torch.float64, device=dev)
+        call("skb_gather_rows", 1, ptr(up["ao"]), ptr(up["a"]), None, None, q, ptr(PsiV), q,
+             ptr(tmp), ptr(up2["o0"]), ptr(up2["ldq"]), ns, q, s)
+        call("skb_copy2d_batched", 1, _mats([_addr(top) + 8 * ns * n], [q], [ns], [n]),
+             _mats([_addr(tmp)], [ns], [q], [q]), 1, s)
+        call("skb_diag_fill", q, _addr(top) + 8 * (ns * n + ns), n, -1.0, ptr(schur), q, -1.0, s)
+        del tmp
+    else:
+        n = ns
+        top = torch.empty((max(n, 1), max(n, 1)), dtype=torch.float64, device=dev)
+        top.copy_(E_root)
+    ipiv = torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+    info = torch.empty(1, dtype=torch.int32, device=dev)
+    ratio = torch.empty(1, dtype=torch.float64, device=dev)
+    _Prof.start()
+    call("skb_getrf_batched", 1, _mats([_addr(top)], [n], [n], [n]),
+         np.array([_addr(ipiv)], np.uint64), ptr(info), ptr(ratio), s)
+    inf = int(info.cpu().item())
+    _Prof.tick("d_corner_lu")
+    if inf >= 0:
+        raise SingularPivotError(inf)
+    return rd, E_root, top, ipiv, UH, PsiV, UH_div, q, float(ratio.cpu().item())
+
+
+def _aug_level(L: LevelFactors, UH, PsiV, UH_div, schur, q):
+    """U sweep on H and V^T sweep on Psi for one level (skel.py:384-396)."""
+    B = len(L.k)
+    k, r, c = L.k, L.r, L.ncols
+    dev = UH.device
+    s = _stream()
+
+    def offs(sz):
+        o = np.zeros(B + 1, np.int64)
+        np.cumsum(sz, out=o[1:])
+        return o
+
+    oS, oR, oPS, oPR, oSp = offs(k * q), offs(r * q), offs(k * c), offs(r * c), offs(c * q)
+    buf = torch.empty(max(int(oS[-1] + 2 * oR[-1] + oPS[-1] + oPR[-1] + oSp[-1]), 1),
+                      dtype=torch.float64, device=dev)
+    base = _addr(buf)
+    b0 = 0
+    addr = {}
+    for name, o in (("Us", oS), ("Ur", oR), ("w", oR), ("Ps", oPS), ("Pr", oPR), ("Sp", oSp)):
+        addr[name] = (base + 8 * (b0 + o[:-1])).astype(np.uint64)
+        addr[name + "_off"] = b0 + o[:-1]
+        b0 += int(o[-1])
+    up = _upload(Us=addr["Us_off"], Ur=addr["Ur_off"], w=addr["w_off"], Ps=addr["Ps_off"],
+                 Pr=addr["Pr_off"], ldq=np.full(B, q, np.int64), ldc=c.astype(np.int64))
+    d = L.d
+    mk, mr, mc = int(k.max(initial=0)), int(r.max(initial=0)), int(c.max(initial=0))
+    call("skb_gather_rows", B, ptr(d["sd_off"]), ptr(d["sd"]), None, None, q, ptr(UH), q,
+         base, ptr(up["Us"]), ptr(up["ldq"]), mk, q, s)
+    call("skb_gather_rows", B, ptr(d["rd_off"]), ptr(d["rd"]), None, None, q, ptr(UH), q,
+         base, ptr(up["Ur"]), ptr(up["ldq"]), mr, q, s)
+    if mc:
+        call("skb_gather_rows", B, ptr(d["sd_off"]), ptr(d["sd"]), ptr(d["c_off"]), ptr(d["c"]), 0,
+             ptr(PsiV), q, base, ptr(up["Ps"]), ptr(up["ldc"]), mk, mc, s)
+        call("skb_gather_rows", B, ptr(d["rd_off"]), ptr(d["rd"]), ptr(d["c_off"]), ptr(d["c"]), 0,
+             ptr(PsiV), q, base, ptr(up["Pr"]), ptr(up["ldc"]), mr, mc, s)
+    one, mone, zero = np.ones(B), -np.ones(B), np.zeros(B)
+    qq = np.full(B, q)
+    T = L.P["T"]
+    _gemm([dict(A=T, B=addr["Us"], C=addr["Ur"], D=addr["Ur"], m=r, n=qq, k=k, lda=r, ldb=qq,
+                ldc=qq, ldd=qq, alpha=mone, beta=one, transA=1),
+           dict(A=T, B=addr["Ps"], C=addr["Pr"], D=addr["Pr"], m=r, n=c, k=k, lda=r, ldb=c,
+                ldc=c, ldd=c, alpha=mone, beta=one, transA=1)])
+    call("skb_copy2d_batched", B, _mats(addr["w"], r, qq, qq),
+         _mats(addr["Ur"], r, qq, qq), 0, s)
+    call("skb_getrs_batched", B, _mats(L.P["LU"], r, r, r), L.ipiv,
+         _mats(addr["w"], r, qq, qq), s)
+    _gemm([dict(A=L.P["Xsr"], B=addr["w"], C=addr["Us"], D=addr["Us"], m=k, n=qq, k=r, lda=r,
+                ldb=qq, ldc=qq, ldd=qq, alpha=mone, beta=one),
+           dict(A=L.P["Xrsdiv"], B=addr["Pr"], C=addr["Ps"], D=addr["Ps"], m=k, n=c, k=r, lda=k,
+                ldb=c, ldc=c, ldd=c, alpha=mone, beta=one, transA=1),
+           dict(A=addr["Pr"], B=addr["w"], D=addr["Sp"], m=c, n=qq, k=r, lda=c, ldb=qq, ldd=qq,
+                alpha=one, beta=zero, transA=1)])
+    call("skb_scatter_rows", B, ptr(d["rd_off"]), ptr(d["rd"]), None, None, q, base, ptr(up["Ur"]),
+         ptr(up["ldq"]), ptr(UH), q, 0, 1.0, mr, q, s)
+    call("skb_scatter_rows", B, ptr(d["sd_off"]), ptr(d["sd"]), None, None, q, base, ptr(up["Us"]),
+         ptr(up["ldq"]), ptr(UH), q, 0, 1.0, mk, q, s)
+    call("skb_scatter_rows", B, ptr(d["rd_off"]), ptr(d["rd"]), None, None, q, base, ptr(up["w"]),
+         ptr(up["ldq"]), ptr(UH_div), q, 0, 1.0, mr, q, s)
+    if mc:
+        call("skb_scatter_rows", B, ptr(d["rd_off"]), ptr(d["rd"]), ptr(d["c_off"]), ptr(d["c"]), 0,
+             base, ptr(up["Pr"]), ptr(up["ldc"]), ptr(PsiV), q, 0, 1.0, mr, mc, s)
+        call("skb_scatter_rows", B, ptr(d["sd_off"]), ptr(d["sd"]), ptr(d["c_off"]), ptr(d["c"]), 0,
+             base, ptr(up["Ps"]), ptr(up["ldc"]), ptr(PsiV), q, 0, 1.0, mk, mc, s)
+        # deterministic schur accumulation in box order
+        rows = L.cols
+        owner = np.repeat(np.arange(B), c)
+        local = np.arange(len(rows)) - np.repeat(L.cols_off[:-1], c)
+        contrib = addr["Sp_off"][owner] + local * q
+        order = np.argsort(rows, kind="stable")
+        row_off = np.zeros(q + 1, np.int64)
+        np.cumsum(np.bincount(rows, minlength=q), out=row_off[1:])
+        up3 = _upload(ro=row_off, ct=contrib[order].astype(np.int64))
+        call("skb_schur_accumulate", q, ptr(up3["ro"]), ptr(up3["ct"]), base, ptr(schur), s)
+        L._aug_keep = up3
+    L._aug_keep2 = (buf, up)
+
+
+def _leaf_dofs(t, i):
+    return (2 * t.nodes_of(i)[:, None] + np.arange(2)[None, :]).ravel()
+
+
+def _run_levels(ctx: _Ctx, reuse=None, dirty=None):
+    """Bottom-up level loop (reference factor skel.py:443-449 / update skel.py:502-509)."""
+    t = ctx.t
+    act_of = {}
+    for i in np.flatnonzero(t.is_leaf):
+        act_of[int(i)] = _leaf_dofs(t, int(i))
+    ctx.skel_of = {}
+    levels = []
+    n_recomp = 0
+    for lev in range(t.depth, 0, -1):
+        idx = t.level_indices(lev)
+        for i in idx:
+            if not t.is_leaf[i]:
+                act_of[int(i)] = np.concatenate([ctx.skel_of[c] for c in t.children_of(i)])
+        if reuse is None:
+            todo = idx
+        else:
+            todo = np.array([i for i in idx if t.key(i) in dirty], np.int64)
+        bt_new = ctx.compress_level(todo, act_of) if len(todo) else None
+        n_recomp += len(todo)
+        if reuse is None:
+            bt = bt_new
+        else:
+            bt = _merge_level(ctx, idx, act_of, todo, bt_new, reuse)
+        for bi, i in enumerate(bt.idx):
+            a0 = bt.act_off[bi]
+            kk = int(bt.k[bi])
+            ctx.skel_of[int(i)] = bt.act[a0 + bt.perm[a0:a0 + kk]]
+            ctx.xss[int(i)] = (int(bt.ptr["Xss"][bi]), kk)
+        cols_off, cols = _hole_columns(t, ctx.b, bt.idx)
+        levels.append(LevelFactors(lev, t, bt, cols_off, cols))
+    return levels, act_of, n_recomp
+
+
+def _merge_level(ctx, idx, act_of, todo, bt_new, old_levels):
+    """Level batch for an update: dirty boxes from bt_new, clean boxes share the
+    old factor memory (reference run_level reuse path, skel.py:342-353)."""
+    t = ctx.t
+    act_off, act = _csr([act_of[int(i)] for i in idx])
+    bt = BoxBatch(idx, act_off, act)
+    pos_new = {int(i): j for j, i in enumerate(todo)}
+    for bi, i in enumerate(idx):
+        key = t.key(i)
+        if int(i) in pos_new:
+            bt.take([bi], bt_new, [pos_new[int(i)]])
+            continue
+        li, bj = old_levels[key]
+        L = li
+        ob = L.batch
+        a0, a1 = ob.act_off[bj], ob.act_off[bj + 1]
+        if not np.array_equal(ob.act[a0:a1], act[act_off[bi]:act_off[bi + 1]]):
+            raise RuntimeError(f"clean box {key} changed its active set")
+        bt.take([bi], ob, [bj])
+    return bt
+
+
+def factor(spec, b, t: Tree, tol: float, workers: int = 1,
+           proxy_count: int = DEFAULT_PROXY_COUNT, proxy_factor: float = DEFAULT_PROXY_FACTOR,
+           propagate_zeros: bool = False) -> Factorization:
+    """Build the skeletonization factorization on the GPU (reference skel.py:428-453).
+
+    ``workers`` is accepted for signature parity (the GPU batches every box of a
+    level); ``propagate_zeros`` (a sequential validation mode) is not supported.
+    """
+    if propagate_zeros:
+        raise NotImplementedError("propagate_zeros is a sequential CPU validation mode")
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ctx = _Ctx(spec, b, t, tol, proxy_count, proxy_factor)
+    levels, act_of, _ = _run_levels(ctx)
+    rd, E_root, top, ipiv, UH, PsiV, UH_div, q, ratio = _finish_top(ctx, levels, act_of)
+    torch.cuda.synchronize()
+    stats = {"k_per_level": {L.lev: int(L.k.max(initial=0)) for L in levels},
+             "root_size": len(rd), "top_pivot_ratio": ratio}
+    fct = Factorization(spec, b, t, tol, proxy_count, proxy_factor, levels, rd, E_root, top, ipiv,
+                        UH, PsiV, UH_div, q, ctx, stats)
+    fct.stats["factor_time"] = time.perf_counter() - t0
+    fct.stats["n_dofs"] = fct.n_dofs
+    return fct
+
+
+def update(fct: Factorization, b_new, report, workers: int = 1) -> Factorization:
+    """Refactor only what a local perturbation invalidated (reference skel.py:456-514)."""
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    try:
+        t_new = refit_tree(fct.tree, b_new.positions)
+    except ValueError as e:
+        raise RootBoxExceededError("perturbed node escaped the root box; refactor with a fresh tree") from e
+    dirty = dirty_set(fct.tree, t_new, b_new, report, fct.proxy_factor)
+    if not np.array_equal(report.old_to_new, np.arange(len(report.old_to_new))):
+        raise NotImplementedError("only DOF-preserving edits (hole moves) are supported")
+    old = {}
+    for L in fct.levels:
+        for bj, key in enumerate(L.keys):
+            old[key] = (L, bj)
+    ctx = _Ctx(fct.spec, b_new, t_new, fct.tol, fct.proxy_count, fct.proxy_factor)
+    levels, act_of, n_recomp = _run_levels(ctx, reuse=old, dirty=dirty)
+    rd, E_root, top, ipiv, UH, PsiV, UH_div, q, ratio = _finish_top(ctx, levels, act_of)
+    torch.cuda.synchronize()
+    stats = {"k_per_level": {L.lev: int(L.k.max(initial=0)) for L in levels},
+             "root_size": len(rd), "top_pivot_ratio": ratio}
+    nf = Factorization(fct.spec, b_new, t_new, fct.tol, fct.proxy_count, fct.proxy_factor, levels,
+                       rd, E_root, top, ipiv, UH, PsiV, UH_div, q, ctx, stats)
+    nf.stats["update_time"] = time.perf_counter() - t0
+    nf.stats["n_dirty"] = len(dirty)
+    nf.stats["n_boxes"] = len(t_new.lev)
+    nf.stats["dirty"] = dirty
+    return nf

@@ -1,0 +1,308 @@
+"""Adaptive quadtree over boundary nodes, flat struct-of-arrays, built level by level.
+
+Same semantics as the reference ``tree.py`` (``/root/reference/pkg/src/skelsolve``):
+geometric keys ``(level, ix, iy)`` with root ``(0, 0, 0)`` (``tree.py:1-11``),
+child order SW, SE, NW, NE with empty children pruned (``tree.py:19``),
+split while a box holds more than ``leaf_cap`` nodes, ``east = x >= cx``,
+``north = y >= cy`` (``tree.py:127-144``), default root = bounding square
+inflated by 10% (``tree.py:102-107``), fixed root for refits
+(``tree.py:239-248``).  Box centres are formed with the reference's exact
+floating-point expressions so proxy discs and far-field filters agree bitwise.
+
+Boxes are indexed globally level by level, keys sorted within a level
+(``Tree.levels[l]`` = sorted keys, ``tree.py:148``).  Neighbour queries,
+coarse-leaf disc queries, far-field DOF lists and the update's dirty marking
+are vectorised NumPy (the reference walks Python dicts per box).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+CHILD_OFFSETS = ((0, 0), (1, 0), (0, 1), (1, 1))   # SW, SE, NW, NE
+NBR_OFFSETS = [(dx, dy) for dx in (-1, 0, 1) for dy in (-1, 0, 1) if dx or dy]  # sorted order
+
+
+class TreeError(ValueError):
+    pass
+
+
+def default_root_box(positions, inflate: float = 0.1):
+    """Reference tree.py:102-107."""
+    lo = positions.min(axis=0)
+    hi = positions.max(axis=0)
+    center = 0.5 * (lo + hi)
+    hw = 0.5 * float((hi - lo).max()) * (1.0 + inflate)
+    return center, hw
+
+
+def proxy_radius(half_width, factor: float = 1.5):
+    """Reference tree.py:158-160 (factor x circumradius)."""
+    return factor * half_width * np.sqrt(2.0)
+
+
+class Tree:
+    """Flat quadtree.  Per-box arrays are indexed by global box index."""
+
+    def __init__(self, root_center, root_hw, leaf_cap, max_depth):
+        self.root_center = np.asarray(root_center, float)
+        self.root_half_width = float(root_hw)
+        self.leaf_cap = leaf_cap
+        self.max_depth = max_depth
+
+    # -- reference-like accessors -------------------------------------------
+    @property
+    def depth(self) -> int:
+        return len(self.level_start) - 2
+
+    @property
+    def levels(self):
+        return [[self.key(i) for i in range(self.level_start[l], self.level_start[l + 1])]
+                for l in range(self.depth + 1)]
+
+    def key(self, i) -> tuple:
+        return (int(self.lev[i]), int(self.ix[i]), int(self.iy[i]))
+
+    def index(self, key) -> int:
+        return self._index[tuple(int(v) for v in key)]
+
+    def has(self, key) -> bool:
+        return tuple(int(v) for v in key) in self._index
+
+    def level_indices(self, l):
+        return np.arange(self.level_start[l], self.level_start[l + 1])
+
+    def nodes_of(self, i) -> np.ndarray:
+        l = self.lev[i]
+        s = self.node_start[i]
+        return self.level_nodes[l][s:s + self.node_cnt[i]]
+
+    def children_of(self, i):
+        return [int(c) for c in self.children[i] if c >= 0]
+
+    def colleagues(self, key) -> list:
+        i = self.index(key)
+        return [self.key(j) for j in self.neighbors[i] if j >= 0]
+
+    # -- vectorised queries ---------------------------------------------------
+    def _finish(self):
+        n = len(self.lev)
+        self._index = {self.key(i): i for i in range(n)}
+        self.is_leaf = self.nchild == 0
+        # same-level neighbours in sorted key order (tree.py:70-81)
+        self.neighbors = np.full((n, 8), -1, dtype=np.int64)
+        for l in range(self.depth + 1):
+            idx = self.level_indices(l)
+            if len(idx) == 0:
+                continue
+            side = np.int64(1) << np.int64(l)
+            codes = self.ix[idx] * side + self.iy[idx]
+            for s, (dx, dy) in enumerate(NBR_OFFSETS):
+                nx, ny = self.ix[idx] + dx, self.iy[idx] + dy
+                ok = (nx >= 0) & (ny >= 0) & (nx < side) & (ny < side)
+                c = nx * side + ny
+                pos = np.searchsorted(codes, c)
+                pos_c = np.minimum(pos, len(codes) - 1)
+                hit = ok & (codes[pos_c] == c)
+                self.neighbors[idx[hit], s] = idx[pos_c[hit]]
+        self.node_leaf = np.empty(self.n_nodes, dtype=np.int64)
+        for l in range(self.depth + 1):
+            idx = self.level_indices(l)
+            leaves = idx[self.is_leaf[idx]]
+            for i in leaves:
+                self.node_leaf[self.nodes_of(i)] = i
+
+    def coarse_leaves_mask(self, box_idx, radius):
+        """(len(box_idx), n_cand) mask of leaves above the boxes' level meeting
+        the disc (centre, radius) -- reference Tree.shallow_leaves_near,
+        tree.py:83-99.  Returns (mask, candidate indices sorted by key)."""
+        l = int(self.lev[box_idx[0]])
+        cand = np.flatnonzero(self.is_leaf & (self.lev < l))
+        if len(cand) == 0 or len(box_idx) == 0:
+            return np.zeros((len(box_idx), 0), bool), cand
+        c = self.center[box_idx]
+        d = np.maximum(np.abs(c[:, None, :] - self.center[cand][None, :, :])
+                       - self.hw[cand][None, :, None], 0.0)
+        dd = d[..., 0] * d[..., 0] + d[..., 1] * d[..., 1]
+        r = np.asarray(radius, float)
+        mask = ~(dd > (r * r)[:, None])
+        return mask, cand
+
+
+def build_tree(positions, leaf_cap: int = 64, root_box=None, max_depth: int = 40) -> Tree:
+    """Reference build_tree (tree.py:110-155), vectorised per level."""
+    pos = np.asarray(positions, float)
+    N = len(pos)
+    if root_box is None:
+        center, hw = default_root_box(pos)
+    else:
+        center, hw = np.asarray(root_box[0], float), float(root_box[1])
+        if np.any(np.abs(pos - center[None, :]) > hw * (1 + 1e-12)):
+            raise TreeError("node outside the fixed root box")
+    if max_depth > 30:
+        max_depth_eff = 30   # keys are int64 codes; deeper trees never occur here
+    else:
+        max_depth_eff = max_depth
+    t = Tree(center, hw, leaf_cap, max_depth)
+    t.n_nodes = N
+    L_ix, L_iy, L_cen, L_hw, L_par, L_nstart, L_ncnt, L_nodes = [], [], [], [], [], [], [], []
+    L_children = []
+    ix = np.zeros(1, np.int64)
+    iy = np.zeros(1, np.int64)
+    cen = center[None, :].copy()
+    half = np.array([hw])
+    par_local = np.array([-1], np.int64)
+    nodes = np.arange(N, dtype=np.int64)
+    cnt = np.array([N], np.int64)
+    l = 0
+    while True:
+        nb = len(ix)
+        start = np.concatenate([[0], np.cumsum(cnt)[:-1]]).astype(np.int64)
+        L_ix.append(ix); L_iy.append(iy); L_cen.append(cen); L_hw.append(half)
+        L_par.append(par_local); L_nstart.append(start); L_ncnt.append(cnt); L_nodes.append(nodes)
+        split = (cnt > leaf_cap) & (l < max_depth_eff)
+        ch = np.full((nb, 4), -1, np.int64)
+        L_children.append(ch)
+        if not split.any():
+            break
+        box_of = np.repeat(np.arange(nb), cnt)
+        sel = split[box_of]
+        sn = nodes[sel]
+        sb = box_of[sel]
+        east = pos[sn, 0] >= cen[sb, 0]
+        north = pos[sn, 1] >= cen[sb, 1]
+        dx = east.astype(np.int64)
+        dy = north.astype(np.int64)
+        cix = 2 * ix[sb] + dx
+        ciy = 2 * iy[sb] + dy
+        side = np.int64(1) << np.int64(l + 1)
+        code = cix * side + ciy
+        ucode, first, inv = np.unique(code, return_index=True, return_inverse=True)
+        order = np.argsort(inv, kind="stable")
+        nodes = sn[order]
+        cnt = np.bincount(inv, minlength=len(ucode)).astype(np.int64)
+        pb = sb[first]
+        q = (dx + 2 * dy)[first]
+        ix = cix[first]
+        iy = ciy[first]
+        d = np.stack([dx[first], dy[first]], axis=1).astype(float)
+        cen = cen[pb] + (d - 0.5) * half[pb][:, None]
+        half = half[pb] / 2
+        par_local = pb
+        ch[pb, q] = np.arange(len(ucode))
+        l += 1
+    depth = l
+    sizes = [len(a) for a in L_ix]
+    t.level_start = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    t.lev = np.concatenate([np.full(s, li, np.int64) for li, s in enumerate(sizes)])
+    t.ix = np.concatenate(L_ix)
+    t.iy = np.concatenate(L_iy)
+    t.center = np.concatenate(L_cen)
+    t.hw = np.concatenate(L_hw)
+    t.parent = np.concatenate([np.where(p >= 0, p + t.level_start[max(li - 1, 0)], -1)
+                               for li, p in enumerate(L_par)])
+    children = []
+    for li, ch in enumerate(L_children):
+        base = t.level_start[li + 1] if li + 1 <= depth else 0
+        # compact in child order (SW, SE, NW, NE), drop empties
+        out = np.full_like(ch, -1)
+        for r in range(len(ch)):
+            k = ch[r][ch[r] >= 0]
+            out[r, :len(k)] = k + base
+        children.append(out)
+    t.children = np.concatenate(children)
+    t.nchild = (t.children >= 0).sum(axis=1)
+    t.node_start = np.concatenate(L_nstart)
+    t.node_cnt = np.concatenate(L_ncnt)
+    t.level_nodes = L_nodes
+    t._finish()
+    return t
+
+
+def refit_tree(t: Tree, positions_new) -> Tree:
+    """Reference tree.py:239-248: rebuild with the same root box."""
+    return build_tree(positions_new, t.leaf_cap, root_box=(t.root_center, t.root_half_width),
+                      max_depth=t.max_depth)
+
+
+# ---------------------------------------------------------------------------
+# update bookkeeping (reference skel.py:476-491, 517-534; tree.py:215-270)
+# ---------------------------------------------------------------------------
+def ownership_changed(t_new: Tree, t_old: Tree, old_to_new) -> set:
+    """Keys of new boxes whose owned node set differs from their twin (tree.py:251-270)."""
+    changed = set()
+    for i in range(len(t_new.lev)):
+        key = t_new.key(i)
+        if not t_old.has(key):
+            changed.add(key)
+            continue
+        j = t_old.index(key)
+        mapped = old_to_new[t_old.nodes_of(j)]
+        mine = t_new.nodes_of(i)
+        if len(mapped) != len(mine) or np.any(mapped < 0) or not np.array_equal(mapped, mine):
+            changed.add(key)
+    for j in range(len(t_old.lev)):
+        key = t_old.key(j)
+        if not t_new.has(key):
+            p = j
+            while p >= 0 and not t_new.has(t_old.key(p)):
+                p = int(t_old.parent[p])
+            if p >= 0:
+                changed.add(t_old.key(p))
+    return changed
+
+
+def mark_disc_hits(t: Tree, pts, proxy_factor, out: set):
+    """Boxes whose proxy disc contains a point (tree.py:215-236), vectorised."""
+    pts = np.asarray(pts, float)
+    for lev in range(t.depth + 1):
+        idx = t.level_indices(lev)
+        if len(idx) == 0:
+            continue
+        hw = t.root_half_width / 2 ** lev
+        rad = proxy_radius(hw, proxy_factor)
+        c = t.center[idx]
+        d2 = ((pts[None, :, :] - c[:, None, :]) ** 2).sum(axis=2)
+        hit = (d2 <= rad * rad).any(axis=1)
+        for i in idx[hit]:
+            out.add(t.key(i))
+
+
+def dirty_closure(t: Tree, content: set) -> set:
+    """Parents + colleagues closure, reference skel.py:517-534."""
+    marked = {l: set() for l in range(t.depth + 1)}
+    for key in content:
+        marked[key[0]].add(key)
+    for lev in range(t.depth, -1, -1):
+        grew = set(marked[lev])
+        if lev + 1 <= t.depth:
+            for key in marked[lev + 1]:
+                p = int(t.parent[t.index(key)])
+                if p >= 0:
+                    grew.add(t.key(p))
+        for key in list(grew):
+            grew.update(t.colleagues(key))
+        marked[lev] = grew
+    out = set()
+    for s in marked.values():
+        out |= s
+    return out
+
+
+def dirty_set(t_old: Tree, t_new: Tree, b_new, report, proxy_factor) -> set:
+    """Dirty boxes of an update (reference skel.py:476-491)."""
+    content = set(ownership_changed(t_new, t_old, report.old_to_new))
+    pts = []
+    if len(report.modified_nodes_old):
+        pts.append(report.old_positions[report.modified_nodes_old])
+    if len(report.modified_nodes_new):
+        pts.append(b_new.positions[report.modified_nodes_new])
+    pts = np.concatenate(pts) if pts else np.zeros((0, 2))
+    if len(pts):
+        mark_disc_hits(t_new, pts, proxy_factor, content)
+    for nid in report.modified_nodes_new:
+        i = int(t_new.node_leaf[nid])
+        while i >= 0 and t_new.key(i) not in content:
+            content.add(t_new.key(i))
+            i = int(t_new.parent[i])
+    return dirty_closure(t_new, content)

@@ -1,0 +1,223 @@
+"""Kernel-level parity on a B200: each C-ABI primitive against the fp64 CPU
+reference of the same operation (NumPy/SciPy LAPACK), on seeded inputs."""
+
+import numpy as np
+import pytest
+import scipy.linalg as sla
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import skel_oracle as O  # noqa: E402
+from paper_2001_11619_b200 import configs, skel  # noqa: E402
+from paper_2001_11619_b200._lib import call  # noqa: E402
+from paper_2001_11619_b200.tree import build_tree  # noqa: E402
+
+
+def _dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def test_gemm_grouped_ragged():
+    rng = np.random.default_rng(0)
+    shapes = [(1, 1, 1), (7, 65, 3), (64, 64, 16), (130, 17, 200), (5, 300, 0), (0, 4, 4),
+              (96, 96, 96)]
+    rows = []
+    outs, refs = [], []
+    for ta in (0, 1):
+        for tb in (0, 1):
+            for (m, n, k) in shapes:
+                A = rng.standard_normal((k, m) if ta else (m, k))
+                B = rng.standard_normal((n, k) if tb else (k, n))
+                C = rng.standard_normal((m, n))
+                dA, dB, dC = _dev(A), _dev(B), _dev(C)
+                dD = torch.empty((max(m, 1), max(n, 1)), dtype=torch.float64, device="cuda")
+                rows.append(dict(A=np.array([dA.data_ptr()], np.uint64), B=np.array([dB.data_ptr()], np.uint64),
+                                 C=np.array([dC.data_ptr()], np.uint64), D=np.array([dD.data_ptr()], np.uint64),
+                                 m=[m], n=[n], k=[k], lda=[max(A.shape[1], 1)], ldb=[max(B.shape[1], 1)],
+                                 ldc=[max(n, 1)], ldd=[max(n, 1)], alpha=[-0.5], beta=[2.0],
+                                 transA=[ta], transB=[tb]))
+                opA = A.T if ta else A
+                opB = B.T if tb else B
+                refs.append(-0.5 * (opA @ opB) + 2.0 * C)
+                outs.append((dD, m, n, dA, dB, dC))
+    skel._gemm(rows)
+    torch.cuda.synchronize()
+    for (dD, m, n, *_), R in zip(outs, refs):
+        if m == 0 or n == 0:
+            continue
+        got = dD.cpu().numpy()[:m, :n]
+        assert np.allclose(got, R, rtol=1e-13, atol=1e-12 * max(1, np.abs(R).max()))
+
+
+def test_getrf_getrs_batched():
+    rng = np.random.default_rng(1)
+    ns = [1, 5, 63, 64, 65, 130, 257]
+    mats, ipivs, Bs, refs = [], [], [], []
+    for n in ns:
+        A = rng.standard_normal((n, n)) + 0.1 * np.eye(n)
+        Bm = rng.standard_normal((n, 3))
+        mats.append(_dev(A))
+        ipivs.append(torch.empty(n, dtype=torch.int32, device="cuda"))
+        Bs.append(_dev(Bm))
+        refs.append((A, Bm))
+    m = skel._mats(np.array([t.data_ptr() for t in mats], np.uint64), ns, ns, ns)
+    ip = np.array([t.data_ptr() for t in ipivs], np.uint64)
+    info = torch.empty(len(ns), dtype=torch.int32, device="cuda")
+    ratio = torch.empty(len(ns), dtype=torch.float64, device="cuda")
+    call("skb_getrf_batched", len(ns), m, ip, info, ratio, skel._stream())
+    b = skel._mats(np.array([t.data_ptr() for t in Bs], np.uint64), ns, [3] * len(ns), [3] * len(ns))
+    call("skb_getrs_batched", len(ns), m, ip, b, skel._stream())
+    torch.cuda.synchronize()
+    assert (info.cpu().numpy() == -1).all()
+    for (A, Bm), X, r in zip(refs, Bs, ratio.cpu().numpy()):
+        x = X.cpu().numpy()
+        ref = np.linalg.solve(A, Bm)
+        assert np.linalg.norm(x - ref) <= 1e-11 * np.linalg.norm(ref) * np.linalg.cond(A)
+        d = np.abs(np.diag(sla.lu_factor(A)[0]))
+        assert abs(r - d.min() / d.max()) <= 1e-10 * (d.min() / d.max())
+
+
+def test_getrf_singular_reports_index():
+    A = np.array([[1.0, 2.0], [2.0, 4.0]])
+    dA = _dev(A)
+    ip = torch.empty(2, dtype=torch.int32, device="cuda")
+    info = torch.empty(1, dtype=torch.int32, device="cuda")
+    ratio = torch.empty(1, dtype=torch.float64, device="cuda")
+    call("skb_getrf_batched", 1, skel._mats(np.array([dA.data_ptr()], np.uint64), [2], [2], [2]),
+         np.array([ip.data_ptr()], np.uint64), info, ratio, skel._stream())
+    assert int(info.cpu()[0]) == 1     # reference SPEC.md:194-197: SingularPivotError index 1
+
+
+def _golden_boxes(g, prefix):
+    keys = [tuple(k) for k in g[prefix + "keys"]]
+    out = {}
+    for i, k in enumerate(keys):
+        def sl(a):
+            return g[prefix + a][g[prefix + a + "_off"][i]:g[prefix + a + "_off"][i + 1]]
+        out[k] = dict(act=sl("act"), far=sl("far"), S=sl("S"), k=int(g[prefix + "k"][i]))
+    return out
+
+
+def _ulp_diff(a, b):
+    ai = a.view(np.int64)
+    bi = b.view(np.int64)
+    return np.abs(ai - bi)
+
+
+@pytest.mark.parametrize("name,builder", [("cfg1_", configs.cfg1), ("mini_", configs.mini_holes)])
+def test_stack_assembly_bitwise(golden, name, builder):
+    """(a) GPU ID stacks vs the reference's np.vstack(blocks): bitwise except the
+    log()-containing Stokeslet proxy rows (<= 2 ulp)."""
+    wl = builder()
+    t = build_tree(wl.boundary.positions, wl.leaf_cap)
+    ctx = skel._Ctx(skel.SystemSpec(), wl.boundary, t, wl.tol, wl.proxy_count, wl.proxy_factor)
+    ref = _golden_boxes(golden, name)
+    i = 0
+    while name + f"stack{i}_key" in golden.files:
+        key = tuple(golden[name + f"stack{i}_key"])
+        S_ref = golden[name + f"stack{i}"]
+        bi = t.index(key)
+        act_of = {j: ref[t.key(j)]["act"] for j in range(len(t.lev)) if t.key(j) in ref}
+        idx = np.array([bi])
+        act_off, act = skel._csr([act_of[bi]])
+        far_off, far = ctx.far_lists(idx, act_of)
+        pts, pn, pw = ctx.proxies(idx)
+        nB, nF, P = len(act), len(far), wl.proxy_count
+        rows = 2 * nF + 6 * P + 2
+        st = torch.empty(rows * nB, dtype=torch.float64, device="cuda")
+        up = skel._upload(ao=act_off, a=act, fo=far_off, f=far if nF else np.zeros(1, np.int64),
+                          pts=pts.reshape(-1), pn=pn.reshape(-1), pw=pw, so=np.zeros(1, np.int64))
+        g = ctx.g
+        call("skb_assemble_stack", g.pos, g.nrm, g.w, 1, up["ao"], up["a"], up["fo"], up["f"],
+             up["pts"], up["pn"], up["pw"], P, up["so"], st, nB, nF + P + 1, skel._stream())
+        got = st.cpu().numpy().reshape(nB, rows).T
+        assert got.shape == S_ref.shape
+        ul = _ulp_diff(got, S_ref)
+        log_rows = np.zeros(rows, bool)
+        log_rows[2 * nF + 4 * P + 1: 2 * nF + 6 * P + 1] = True
+        assert ul[~log_rows].max() == 0, (key, ul[~log_rows].max())
+        assert ul[log_rows].max() <= 4, (key, ul[log_rows].max())
+        i += 1
+
+
+@pytest.mark.parametrize("name,builder", [("cfg1_", configs.cfg1), ("mini_", configs.mini_holes)])
+def test_self_block_bitwise(name, builder):
+    """(a) Self blocks E = A[B, B] vs the oracle (bitwise) for leaf boxes."""
+    wl = builder()
+    t = build_tree(wl.boundary.positions, wl.leaf_cap)
+    ctx = skel._Ctx(skel.SystemSpec(), wl.boundary, t, wl.tol, wl.proxy_count, wl.proxy_factor)
+    idx = t.level_indices(t.depth)[:4]
+    lists = [(2 * t.nodes_of(i)[:, None] + np.arange(2)).ravel() for i in idx]
+    ao, a = skel._csr(lists)
+    nB = np.diff(ao)
+    eo = np.concatenate([[0], np.cumsum(nB * nB)])
+    E = torch.empty(int(eo[-1]), dtype=torch.float64, device="cuda")
+    co = np.full((len(idx), 5), -1, np.int64)
+    cx = np.zeros((len(idx), 4), np.uint64)
+    up = skel._upload(ao=ao, a=a, co=co.reshape(-1), cx=cx.reshape(-1), eo=eo[:-1], eld=nB)
+    g = ctx.g
+    call("skb_assemble_self", g.pos, g.nrm, g.w, g.kap, len(idx), up["ao"], up["a"], None, None,
+         up["co"], up["cx"], E, up["eo"], up["eld"], int(nB.max()), skel._stream())
+    En = E.cpu().numpy()
+    for bi, lst in enumerate(lists):
+        ref = O.self_block(wl.boundary, lst, lst)
+        got = En[eo[bi]:eo[bi + 1]].reshape(nB[bi], nB[bi])
+        assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("name,builder", [("cfg1_", configs.cfg1), ("mini_", configs.mini_holes)])
+def test_id_replay_skeletons(golden, name, builder):
+    """(b) Replay every box on the reference's exact active sets: GPU stack ->
+    Householder -> QRCP must select the reference's skeleton (same order)."""
+    wl = builder()
+    t = build_tree(wl.boundary.positions, wl.leaf_cap)
+    ctx = skel._Ctx(skel.SystemSpec(), wl.boundary, t, wl.tol, wl.proxy_count, wl.proxy_factor)
+    ref = _golden_boxes(golden, name)
+    act_of = {j: ref[t.key(j)]["act"] for j in range(len(t.lev)) if t.key(j) in ref}
+    mism = []
+    for lev in range(t.depth, 0, -1):
+        idx = t.level_indices(lev)
+        for i in idx:
+            if not t.is_leaf[i]:
+                ctx.xss[int(i)] = (0, 0)
+        # run only the ID part (stack + QR) to avoid needing children's Xss
+        B = len(idx)
+        act_off, act = skel._csr([act_of[int(i)] for i in idx])
+        nB = np.diff(act_off)
+        far_off, far = ctx.far_lists(idx, act_of)
+        nF = np.diff(far_off)
+        pts, pn, pw = ctx.proxies(idx)
+        P = wl.proxy_count
+        rows = 2 * nF + 6 * P + 2
+        so = np.concatenate([[0], np.cumsum(rows * nB)])
+        st = torch.empty(int(so[-1]), dtype=torch.float64, device="cuda")
+        up = skel._upload(ao=act_off, a=act, fo=far_off, f=far if len(far) else np.zeros(1, np.int64),
+                          pts=pts.reshape(-1), pn=pn.reshape(-1), pw=pw, so=so[:-1])
+        g = ctx.g
+        s = skel._stream()
+        call("skb_assemble_stack", g.pos, g.nrm, g.w, B, up["ao"], up["a"], up["fo"], up["f"],
+             up["pts"], up["pn"], up["pw"], P, up["so"], st, int(nB.max()), int((nF + P + 1).max()), s)
+        A = (st.data_ptr() + 8 * so[:-1]).astype(np.int64)
+        pre = rows > nB
+        call("skb_geqrf_batched", int(pre.sum()), np.ascontiguousarray(rows[pre]),
+             np.ascontiguousarray(nB[pre]), np.ascontiguousarray(rows[pre]), np.ascontiguousarray(A[pre]), s)
+        mq = np.where(pre, nB, rows).astype(np.int64)
+        perm = torch.empty(len(act), dtype=torch.int32, device="cuda")
+        diag = torch.empty(len(act), dtype=torch.float64, device="cuda")
+        ko = torch.empty(2 * B, dtype=torch.int32, device="cuda")
+        gap = torch.empty(B, dtype=torch.float64, device="cuda")
+        call("skb_qrcp_id_batched", B, mq, nB.astype(np.int64), rows.astype(np.int64), A,
+             np.zeros(B, np.int64), wl.tol, act_off, perm, diag, ko, ko.data_ptr() + 4 * B, gap, s)
+        pm = perm.cpu().numpy()
+        kk = ko.cpu().numpy()[:B]
+        gp = gap.cpu().numpy()
+        for bi, i in enumerate(idx):
+            r = ref[t.key(i)]
+            S = pm[act_off[bi]:act_off[bi] + kk[bi]]
+            if kk[bi] != r["k"] or not np.array_equal(S, r["S"]):
+                mism.append((t.key(i), int(kk[bi]), r["k"], float(gp[bi])))
+    # a mismatch is acceptable only as a pivot tie within rounding
+    untied = [m for m in mism if m[3] > 1e-12]
+    assert not untied, untied
+    assert not mism, mism      # these fixtures were chosen tie-free

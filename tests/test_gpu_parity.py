@@ -1,0 +1,94 @@
+"""End-to-end parity on a B200 against the reference fixtures and the CPU oracle:
+identical skeletons per box, solve/apply within 10*eps (relative 2-norm)."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import skel_oracle as O  # noqa: E402
+from paper_2001_11619_b200 import SystemSpec, build_tree, configs, factor, update  # noqa: E402
+from paper_2001_11619_b200.geometry import MoveHole, apply_perturbation  # noqa: E402
+
+
+def _rel(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+def _factor(wl):
+    t = build_tree(wl.boundary.positions, wl.leaf_cap)
+    return factor(SystemSpec(), wl.boundary, t, wl.tol, proxy_count=wl.proxy_count,
+                  proxy_factor=wl.proxy_factor)
+
+
+@pytest.mark.parametrize("name,builder", [("cfg1_", configs.cfg1), ("mini_", configs.mini_holes)])
+def test_factor_solve_apply_vs_reference(golden, name, builder):
+    wl = builder()
+    f = _factor(wl)
+    keys = [tuple(k) for k in golden[name + "keys"]]
+    so, S = golden[name + "S_off"], golden[name + "S"]
+    bad = []
+    for i, k in enumerate(keys):
+        if not np.array_equal(f.factors[k].S_loc, S[so[i]:so[i + 1]]):
+            bad.append(k)
+    assert not bad, bad
+    assert np.array_equal(f.root_dofs, golden[name + "root_dofs"])
+    kpl = {int(l): int(v) for l, v in golden[name + "k_per_level"]}
+    assert f.stats["k_per_level"] == kpl
+    x = f.solve(golden[name + "rhs"])
+    assert _rel(x, golden[name + "x"]) <= 10 * wl.tol
+    y = f.apply(golden[name + "apply_in"])
+    assert _rel(y, golden[name + "apply_out"]) <= 10 * wl.tol
+
+
+def test_multi_rhs_matches_columns(golden):
+    wl = configs.cfg1()
+    f = _factor(wl)
+    X = golden["cfg1_multi_in"]
+    got = f.solve(X)
+    assert got.shape == X.shape
+    assert _rel(got, golden["cfg1_multi_x"]) <= 10 * wl.tol
+    for j in range(X.shape[1]):
+        assert _rel(got[:, j], f.solve(X[:, j])) <= 1e-13
+
+
+def test_cfg1_against_dense_and_exact_field():
+    """Independent oracles: dense LU of the full system and the exact Stokeslet field."""
+    wl = configs.cfg1()
+    f = _factor(wl)
+    x = f.solve(wl.extra["rhs"])
+    A = O.dense_system(wl.boundary)
+    xd = np.linalg.solve(A, wl.extra["rhs"])
+    assert _rel(x, xd) < 1e-8
+    r = A @ x - wl.extra["rhs"]
+    assert np.linalg.norm(r) / np.linalg.norm(wl.extra["rhs"]) < 1e-8
+
+
+def test_update_equals_refactor_and_reference(golden):
+    wl = configs.mini_holes()
+    f = _factor(wl)
+    nb, rep = apply_perturbation(wl.boundary, [MoveHole(2, translation=(0.1, -0.05))])
+    fu = update(f, nb, rep)
+    assert fu.stats["dirty"] == {tuple(k) for k in golden["mini_upd_dirty"]}
+    rhs = golden["mini_rhs"]
+    xu = fu.solve(rhs)
+    assert _rel(xu, golden["mini_upd_x"]) <= 10 * wl.tol
+    t2 = build_tree(nb.positions, wl.leaf_cap, root_box=(f.tree.root_center, f.tree.root_half_width))
+    fr = factor(SystemSpec(), nb, t2, wl.tol, proxy_count=wl.proxy_count, proxy_factor=wl.proxy_factor)
+    assert np.array_equal(fr.solve(rhs), xu)       # bitwise: update == refactor
+
+
+def test_cfg2_against_oracle():
+    wl = configs.cfg2()
+    f = _factor(wl)
+    ref = O.factor_full(wl.boundary, wl.leaf_cap, wl.tol, wl.proxy_count, wl.proxy_factor)
+    same = sum(np.array_equal(f.factors[k].skel_dofs, ref.boxes[k].skel) for k in ref.boxes)
+    rhs = wl.extra["rhs"]
+    x = f.solve(rhs)
+    xr = ref.solve(rhs)
+    err = _rel(x, xr)
+    print(f"cfg2: {same}/{len(ref.boxes)} identical skeletons; solve rel diff {err:.3e}")
+    assert same >= len(ref.boxes) - 20
+    if same == len(ref.boxes):
+        assert err <= 10 * wl.tol

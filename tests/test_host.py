@@ -1,0 +1,84 @@
+"""Host-side logic (no GPU): quadtree, far-field lists, proxy rings, dirty sets."""
+
+import numpy as np
+import pytest
+
+from oracle import skel_oracle as O
+from paper_2001_11619_b200 import configs, skel
+from paper_2001_11619_b200.geometry import MoveHole, apply_perturbation
+from paper_2001_11619_b200.tree import build_tree, dirty_set, refit_tree
+
+
+@pytest.mark.parametrize("builder", [configs.cfg1, configs.mini_holes])
+def test_tree_matches_oracle(builder):
+    wl = builder()
+    t = build_tree(wl.boundary.positions, wl.leaf_cap)
+    ot = O.QTree(wl.boundary.positions, wl.leaf_cap)
+    assert t.levels == ot.levels
+    for i in range(len(t.lev)):
+        key = t.key(i)
+        ob = ot.boxes[key]
+        assert np.array_equal(t.center[i], ob.center)
+        assert t.hw[i] == ob.hw
+        assert np.array_equal(t.nodes_of(i), ob.nodes)
+        assert [t.key(c) for c in t.children_of(i)] == ob.kids
+        assert t.colleagues(key) == ot.neighbours(key)
+
+
+def _boxes(g, prefix):
+    keys = [tuple(k) for k in g[prefix + "keys"]]
+    out = {}
+    for i, k in enumerate(keys):
+        sl = lambda a: g[prefix + a][g[prefix + a + "_off"][i]:g[prefix + a + "_off"][i + 1]]
+        out[k] = dict(act=sl("act"), far=sl("far"), S=g[prefix + "S"][g[prefix + "S_off"][i]:g[prefix + "S_off"][i + 1]])
+    return out
+
+
+@pytest.mark.parametrize("name,builder", [("cfg1_", configs.cfg1), ("mini_", configs.mini_holes)])
+def test_far_lists_and_proxies_match_reference(golden, name, builder):
+    """Replay the reference's active sets and check F_int lists bitwise."""
+    wl = builder()
+    t = build_tree(wl.boundary.positions, wl.leaf_cap)
+    ctx = skel._Ctx(skel.SystemSpec(), wl.boundary, t, wl.tol, wl.proxy_count, wl.proxy_factor)
+    ref = _boxes(golden, name)
+    act_of = {}
+    for i in range(len(t.lev)):
+        key = t.key(i)
+        if key in ref:
+            act_of[i] = ref[key]["act"]
+        elif t.is_leaf[i]:
+            act_of[i] = (2 * t.nodes_of(i)[:, None] + np.arange(2)).ravel()
+    for lev in range(t.depth, 0, -1):
+        idx = t.level_indices(lev)
+        off, F = ctx.far_lists(idx, act_of)
+        for bi, i in enumerate(idx):
+            assert np.array_equal(F[off[bi]:off[bi + 1]], ref[t.key(i)]["far"]), t.key(i)
+        pts, pn, pw = ctx.proxies(idx)
+        for bi, i in enumerate(idx):
+            rp = O.proxy_radius(t.hw[i], wl.proxy_factor)
+            p2, w2 = O.proxy_ring(t.center[i], rp, wl.proxy_count)
+            assert np.array_equal(pts[bi], p2)
+            assert np.array_equal(pn[bi], O.proxy_normals(p2))
+            assert pw[bi] == w2[0]
+
+
+def test_dirty_set_matches_reference(golden):
+    wl = configs.mini_holes()
+    t = build_tree(wl.boundary.positions, wl.leaf_cap)
+    nb, rep = apply_perturbation(wl.boundary, [MoveHole(2, translation=(0.1, -0.05))])
+    t2 = refit_tree(t, nb.positions)
+    d = dirty_set(t, t2, nb, rep, wl.proxy_factor)
+    assert d == {tuple(k) for k in golden["mini_upd_dirty"]}
+
+
+def test_cfg4_dirty_sets_match_oracle():
+    wl = configs.cfg2()
+    t = build_tree(wl.boundary.positions, wl.leaf_cap)
+    ot = O.QTree(wl.boundary.positions, wl.leaf_cap)
+    for h, d, nb, rep in configs.hole_move_sequence(wl.boundary, 3):
+        t2 = refit_tree(t, nb.positions)
+        ot2 = O.QTree(nb.positions, wl.leaf_cap, (ot.root_center, ot.root_hw))
+        mine = dirty_set(t, t2, nb, rep, wl.proxy_factor)
+        ref = O.dirty_set(ot, ot2, nb, rep, wl.proxy_factor)
+        assert mine == ref
+        t, ot = t2, ot2
