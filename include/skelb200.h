@@ -57,6 +57,16 @@ typedef struct SkbMat {
 
 int skb_version(void);
 
+/* Live per-kernel-family timing with CUDA events on the launching stream
+ * (families: 0 assemble, 1 geqrf, 2 qrcp, 3 id_T, 4 gemm, 5 getrf, 6 trsm,
+ * 7 data movement).  skb_prof_read fills 8-entry arrays (ms summed over
+ * launches, launch counts, flops/bytes registered via skb_prof_add and by the
+ * GEMM itself) and optionally resets.  Off by default (zero overhead).      */
+int skb_prof_enable(int32_t on);
+int skb_prof_add(int32_t family, double flops, double bytes);
+int skb_prof_read(double* ms_out, int64_t* count_out, double* flops_out, double* bytes_out,
+                  int32_t reset);
+
 /* Grouped fp64 GEMM on DMMA (mma.sync m8n8k4 f64) tiles.
  * Replaces the NumPy '@' products of skel.py:321-334, 389-396, 140-163,
  * 182, 188, 199-201, 214-215.                                               */

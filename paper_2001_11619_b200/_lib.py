@@ -29,6 +29,9 @@ _f64 = ctypes.c_double
 
 SIGNATURES = {
     "skb_version": [],
+    "skb_prof_enable": [_i32],
+    "skb_prof_add": [_i32, _f64, _f64],
+    "skb_prof_read": [_vp, _vp, _vp, _vp, _i32],
     "skb_gemm_grouped": [_vp, _i64, _vp],
     "skb_assemble_stack": [_vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp,
                            _vp, _i64, _i64, _vp],
@@ -100,3 +103,33 @@ def ptr(x) -> int | None:
     if isinstance(x, np.ndarray):
         return x.ctypes.data
     return x.data_ptr()
+
+
+FAMILIES = ("assemble", "geqrf", "qrcp", "id_T", "gemm", "getrf", "trsm", "move")
+
+
+PROF_ON = False
+
+
+def prof_enable(on: bool = True):
+    global PROF_ON
+    PROF_ON = bool(on)
+    call("skb_prof_enable", 1 if on else 0)
+
+
+def prof_add(family: str, flops: float = 0.0, nbytes: float = 0.0):
+    """Register algorithmic work for a family (only while profiling)."""
+    if PROF_ON:
+        call("skb_prof_add", FAMILIES.index(family), float(flops), float(nbytes))
+
+
+def prof_read(reset: bool = True) -> dict:
+    """Per-family {ms, launches, flops, bytes} from the live event timers."""
+    n = len(FAMILIES)
+    ms = np.zeros(n)
+    cnt = np.zeros(n, np.int64)
+    fl = np.zeros(n)
+    by = np.zeros(n)
+    call("skb_prof_read", ms, cnt, fl, by, 1 if reset else 0)
+    return {f: {"ms": float(ms[i]), "launches": int(cnt[i]), "flops": float(fl[i]),
+                "bytes": float(by[i])} for i, f in enumerate(FAMILIES)}

@@ -228,6 +228,7 @@ extern "C" int skb_assemble_stack(const double* pos, const double* nrm, const do
   Geo g{(const double2*)pos, (const double2*)nrm, w};
   int64_t work = max_cols * max_items;
   dim3 grid(grid_cap((work + 255) / 256, 4096), (unsigned)nbox);
+  ProfScope ps(F_ASSEMBLE, (cudaStream_t)stream);
   k_assemble_stack<<<grid, 256, 0, (cudaStream_t)stream>>>(
       g, act_off, act, far_off, far, (const double2*)ppts, (const double2*)pnrm, pw, P, stack_off,
       stack);
@@ -245,6 +246,7 @@ extern "C" int skb_assemble_self(const double* pos, const double* nrm, const dou
   if (nbox > 65535) return 2;
   Geo g{(const double2*)pos, (const double2*)nrm, w};
   dim3 grid(grid_cap((max_n * max_n + 255) / 256, 4096), (unsigned)nbox);
+  ProfScope ps(F_ASSEMBLE, (cudaStream_t)stream);
   k_assemble_self<<<grid, 256, 0, (cudaStream_t)stream>>>(g, kappa, act_off, act, perm_off, perm,
                                                           child_off, child_xss, E, E_off, E_ld);
   SKB_LAUNCH_CHECK();

@@ -3,6 +3,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+#include <vector>
+
 #include "../../include/skelb200.h"
 
 #define SKB_RET(expr)                                              \
@@ -46,5 +49,33 @@ inline int upload(const T* host, int64_t n, cudaStream_t s, T** dev) {
 inline int grid_cap(int64_t want, int64_t cap) {
   return (int)(want < 1 ? 1 : (want > cap ? cap : want));
 }
+
+// ---- live per-kernel-family timing (CUDA events on the launching stream) ----
+enum Family { F_ASSEMBLE = 0, F_GEQRF, F_QRCP, F_IDT, F_GEMM, F_GETRF, F_TRSM, F_MOVE, F_NFAM };
+
+struct Prof {
+  bool on = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[F_NFAM];
+  std::vector<cudaEvent_t> pool;
+  double flops[F_NFAM] = {0};
+  double bytes[F_NFAM] = {0};
+  cudaEvent_t get() {
+    if (!pool.empty()) { cudaEvent_t e = pool.back(); pool.pop_back(); return e; }
+    cudaEvent_t e; cudaEventCreate(&e); return e;
+  }
+};
+Prof& prof();
+
+struct ProfScope {
+  int fam;
+  cudaStream_t s;
+  cudaEvent_t a{}, b{};
+  ProfScope(int f, cudaStream_t st) : fam(f), s(st) {
+    if (prof().on) { a = prof().get(); b = prof().get(); cudaEventRecord(a, s); }
+  }
+  ~ProfScope() {
+    if (prof().on) { cudaEventRecord(b, s); prof().ev[fam].push_back({a, b}); }
+  }
+};
 
 }  // namespace skb

@@ -130,7 +130,9 @@ k_gemm_grouped(const SkbGemm* __restrict__ probs, int nprob) {
 int gemm_grouped(SkbGemm* probs, int64_t nprob, cudaStream_t s) {
   if (nprob <= 0) return 0;
   int64_t tiles = 0;
+  double fl = 0.0;
   for (int64_t i = 0; i < nprob; ++i) {
+    fl += 2.0 * (double)probs[i].m * (double)probs[i].n * (double)probs[i].k;
     probs[i].tile_begin = tiles;
     if (probs[i].m > 0 && probs[i].n > 0)
       tiles += ((probs[i].m + BM - 1) / BM) * ((probs[i].n + BN - 1) / BN);
@@ -140,7 +142,11 @@ int gemm_grouped(SkbGemm* probs, int64_t nprob, cudaStream_t s) {
   SkbGemm* d = nullptr;
   int rc = upload(probs, nprob, s, &d);
   if (rc) return rc;
-  k_gemm_grouped<<<(unsigned)tiles, GEMM_THREADS, 0, s>>>(d, (int)nprob);
+  {
+    ProfScope ps(F_GEMM, s);
+    k_gemm_grouped<<<(unsigned)tiles, GEMM_THREADS, 0, s>>>(d, (int)nprob);
+  }
+  if (prof().on) prof().flops[F_GEMM] += fl;
   cudaError_t e = cudaGetLastError();
   cudaFreeAsync(d, s);
   return e == cudaSuccess ? 0 : -(int)e;

@@ -33,16 +33,28 @@ __device__ __forceinline__ AbsMax absmax_merge(AbsMax a, AbsMax b) {
   return (b.v > a.v || (b.v == a.v && b.idx < a.idx)) ? b : a;
 }
 
+// dgetf2 on the panel A[j0:n, j0:j0+jb], staged column-major in shared memory
+// (contiguous column scans for the pivot search), then the panel's row
+// interchanges are applied to the columns outside the panel (dlaswp).
 template <int NT>
 __global__ void __launch_bounds__(NT) k_getf2_panel(const LuPanel* __restrict__ descs) {
-  __shared__ AbsMax red[NT / 32 + 1];
+  extern __shared__ double P[];
+  __shared__ AbsMax red[NT / 32];
   const LuPanel D = descs[blockIdx.x];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int64_t c = 0; c < D.jb; ++c) {
-    const int64_t col = D.j0 + c;
+  const int64_t rows = D.n - D.j0;
+  const int jb = (int)D.jb;
+  for (int64_t e = threadIdx.x; e < rows * jb; e += NT) {
+    const int64_t r = e / jb, c = e - r * jb;
+    P[c * rows + r] = D.A[(D.j0 + r) * D.ld + D.j0 + c];
+  }
+  __syncthreads();
+  int info = -1;
+  for (int c = 0; c < jb; ++c) {
+    const double* col = P + (int64_t)c * rows;
     AbsMax loc{-1.0, INT64_MAX};
-    for (int64_t r = col + threadIdx.x; r < D.n; r += NT) {
-      const double v = fabs(D.A[r * D.ld + col]);
+    for (int64_t r = c + threadIdx.x; r < rows; r += NT) {
+      const double v = fabs(col[r]);
       if (v > loc.v) { loc.v = v; loc.idx = r; }
     }
 #pragma unroll
@@ -50,39 +62,48 @@ __global__ void __launch_bounds__(NT) k_getf2_panel(const LuPanel* __restrict__ 
       AbsMax y{__shfl_xor_sync(0xffffffffu, loc.v, o), __shfl_xor_sync(0xffffffffu, loc.idx, o)};
       loc = absmax_merge(loc, y);
     }
-    __syncthreads();
     if (lane == 0) red[warp] = loc;
     __syncthreads();
-    if (threadIdx.x == 0) {
-      AbsMax r = red[0];
-      for (int w = 1; w < NT / 32; ++w) r = absmax_merge(r, red[w]);
-      red[NT / 32] = r;
+    AbsMax best = red[0];
+#pragma unroll
+    for (int w = 1; w < NT / 32; ++w) best = absmax_merge(best, red[w]);
+    const int64_t p = best.idx;
+    const double piv = col[p];
+    if (threadIdx.x == 0) D.ipiv[D.j0 + c] = (int32_t)(D.j0 + p);
+    if (piv == 0.0) {
+      if (info < 0) info = (int)(D.j0 + c);
+      __syncthreads();
+      continue;
     }
-    __syncthreads();
-    const int64_t p = red[NT / 32].idx;
-    const double piv = D.A[p * D.ld + col];
-    if (threadIdx.x == 0) {
-      D.ipiv[col] = (int32_t)p;
-      if (piv == 0.0 && *D.info < 0) *D.info = (int32_t)col;
-    }
-    if (piv == 0.0) { __syncthreads(); continue; }
-    if (p != col) {
-      double* ra = D.A + col * D.ld;
-      double* rb = D.A + p * D.ld;
-      for (int64_t j = threadIdx.x; j < D.n; j += NT) {
-        const double t = ra[j]; ra[j] = rb[j]; rb[j] = t;
-      }
+    if (p != c && threadIdx.x < jb) {
+      double* a = P + (int64_t)threadIdx.x * rows;
+      const double t = a[c]; a[c] = a[p]; a[p] = t;
     }
     __syncthreads();
     const double rinv = 1.0 / piv;
-    const double* urow = D.A + col * D.ld;
-    for (int64_t r = col + 1 + threadIdx.x; r < D.n; r += NT) {
-      double* row = D.A + r * D.ld;
-      const double l = row[col] * rinv;
-      row[col] = l;
-      for (int64_t cc = col + 1; cc < D.j0 + D.jb; ++cc) row[cc] -= l * urow[cc];
+    for (int64_t r = c + 1 + threadIdx.x; r < rows; r += NT) {
+      const double l = col[r] * rinv;
+      P[(int64_t)c * rows + r] = l;
+      for (int cc = c + 1; cc < jb; ++cc) P[(int64_t)cc * rows + r] -= l * P[(int64_t)cc * rows + c];
     }
     __syncthreads();
+  }
+  for (int64_t e = threadIdx.x; e < rows * jb; e += NT) {
+    const int64_t r = e / jb, c = e - r * jb;
+    D.A[(D.j0 + r) * D.ld + D.j0 + c] = P[c * rows + r];
+  }
+  if (threadIdx.x == 0 && info >= 0 && *D.info < 0) *D.info = info;
+  // dlaswp on the columns left and right of the panel
+  for (int64_t col = threadIdx.x; col < D.n - jb; col += NT) {
+    const int64_t cg = col < D.j0 ? col : col + jb;
+    for (int c = 0; c < jb; ++c) {
+      const int64_t p = D.ipiv[D.j0 + c];
+      if (p != D.j0 + c) {
+        double* x = D.A + (D.j0 + c) * D.ld + cg;
+        double* y = D.A + p * D.ld + cg;
+        const double t = *x; *x = *y; *y = t;
+      }
+    }
   }
 }
 
@@ -147,6 +168,7 @@ static int launch_trsm(std::vector<TrsmDesc>& td, bool upper, cudaStream_t s) {
   TrsmDesc* d = nullptr;
   int rc = upload(td.data(), (int64_t)td.size(), s, &d);
   if (rc) return rc;
+  ProfScope ps(F_TRSM, s);
   for (int64_t b0 = 0; b0 < (int64_t)td.size(); b0 += 65535) {
     const int64_t nb = std::min<int64_t>(65535, (int64_t)td.size() - b0);
     dim3 grid((unsigned)((maxc + 255) / 256), (unsigned)nb);
@@ -279,19 +301,32 @@ int getrf_batched(int64_t nbox, const SkbMat* a, const int64_t* ipiv, int32_t* i
     const size_t smem = sizeof(double) * (size_t)max_small * (max_small + 1);
     SKB_RET(cudaFuncSetAttribute(k_getrf_small<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
-    k_getrf_small<256><<<(unsigned)sl.size(), 256, smem, s>>>(ds);
+    {
+      ProfScope ps(F_GETRF, s);
+      k_getrf_small<256><<<(unsigned)sl.size(), 256, smem, s>>>(ds);
+    }
     SKB_LAUNCH_CHECK();
     cudaFreeAsync(ds, s);
   }
   std::vector<LuPanel> pd;
   std::vector<TrsmDesc> td;
   std::vector<SkbGemm> gd;
-  for (int64_t j0 = 0; j0 < max_n; j0 += LB) {
+  // panel width: as wide as shared memory allows for the tallest panel (<= 64)
+  constexpr size_t kPanelSmem = 220 * 1024;
+  int64_t PB = LB;
+  while (PB > 8 && (size_t)max_n * PB * sizeof(double) > kPanelSmem) PB /= 2;
+  if (max_n > 0) {
+    SKB_RET(cudaFuncSetAttribute(k_getf2_panel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kPanelSmem));
+  }
+  for (int64_t j0 = 0; j0 < max_n; j0 += PB) {
     pd.clear(); td.clear(); gd.clear();
+    int64_t max_rows = 0;
     for (int64_t b = 0; b < nbox; ++b) {
       const int64_t n = a[b].rows;
       if (j0 >= n || n <= kSmallLU) continue;
-      const int64_t jb = std::min<int64_t>(LB, n - j0), n2 = n - j0 - jb;
+      const int64_t jb = std::min<int64_t>(PB, n - j0), n2 = n - j0 - jb;
+      max_rows = std::max(max_rows, n - j0);
       double* A = a[b].ptr;
       const int64_t ld = a[b].ld;
       pd.push_back(LuPanel{A, n, ld, j0, jb, reinterpret_cast<int32_t*>(ipiv[b]), info_out + b});
@@ -308,7 +343,11 @@ int getrf_batched(int64_t nbox, const SkbMat* a, const int64_t* ipiv, int32_t* i
     }
     LuPanel* dp = nullptr;
     if ((rc = upload(pd.data(), (int64_t)pd.size(), s, &dp))) return rc;
-    k_getf2_panel<256><<<(unsigned)pd.size(), 256, 0, s>>>(dp);
+    {
+      ProfScope ps(F_GETRF, s);
+      const size_t smem = sizeof(double) * (size_t)max_rows * (size_t)PB;
+      k_getf2_panel<512><<<(unsigned)pd.size(), 512, smem, s>>>(dp);
+    }
     SKB_LAUNCH_CHECK();
     cudaFreeAsync(dp, s);
     if ((rc = launch_trsm(td, false, s))) return rc;
@@ -432,6 +471,7 @@ int getrs_batched(int64_t nbox, const SkbMat* lu, const int64_t* ipiv, const Skb
     for (int64_t b0 = 0; b0 < (int64_t)sd.size(); b0 += 65535) {
       const int64_t nb = std::min<int64_t>(65535, (int64_t)sd.size() - b0);
       dim3 grid((unsigned)((max_c + 127) / 128), (unsigned)nb);
+      ProfScope ps(F_TRSM, s);
       k_apply_ipiv<<<grid, 128, 0, s>>>(d + b0);
     }
     SKB_LAUNCH_CHECK();

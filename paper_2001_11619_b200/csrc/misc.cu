@@ -123,6 +123,7 @@ extern "C" int skb_copy2d_batched(int64_t nbox, const SkbMat* dst, const SkbMat*
   int rc = upload(dst, nbox, s, &dd);
   if (rc) return rc;
   if ((rc = upload(src, nbox, s, &ds))) return rc;
+  ProfScope ps(F_MOVE, s);
   for (int64_t b0 = 0; b0 < nbox; b0 += 65535) {
     const int64_t nb = std::min<int64_t>(65535, nbox - b0);
     dim3 grid(grid_cap((maxe + 255) / 256, 1024), (unsigned)nb);
@@ -142,6 +143,7 @@ extern "C" int skb_gather_rows(int64_t nbox, const int64_t* idx_off, const int64
   if (nbox <= 0 || max_rows <= 0 || max_cols <= 0) return 0;
   if (nbox > 65535) return 2;
   dim3 grid(grid_cap((max_rows * max_cols + 255) / 256, 2048), (unsigned)nbox);
+  ProfScope ps(F_MOVE, (cudaStream_t)stream);
   k_gather_rows<<<grid, 256, 0, (cudaStream_t)stream>>>(idx_off, idx, col_off, col, ncols, src,
                                                         src_ld, dst, dst_off, dst_ld);
   SKB_LAUNCH_CHECK();
@@ -157,6 +159,7 @@ extern "C" int skb_scatter_rows(int64_t nbox, const int64_t* idx_off, const int6
   if (nbox <= 0 || max_rows <= 0 || max_cols <= 0) return 0;
   if (nbox > 65535) return 2;
   dim3 grid(grid_cap((max_rows * max_cols + 255) / 256, 2048), (unsigned)nbox);
+  ProfScope ps(F_MOVE, (cudaStream_t)stream);
   k_scatter_rows<<<grid, 256, 0, (cudaStream_t)stream>>>(idx_off, idx, col_off, col, ncols, src,
                                                          src_off, src_ld, dst, dst_ld, accumulate,
                                                          alpha);
@@ -182,4 +185,48 @@ extern "C" int skb_diag_fill(int64_t n, double* dst, int64_t ld, double diag_val
   return 0;
 }
 
+namespace skb {
+Prof& prof() {
+  static Prof p;
+  return p;
+}
+}  // namespace skb
+
 extern "C" int skb_version(void) { return 1; }
+
+extern "C" int skb_prof_enable(int32_t on) {
+  skb::prof().on = on != 0;
+  return 0;
+}
+
+extern "C" int skb_prof_add(int32_t fam, double flops, double bytes) {
+  if (fam < 0 || fam >= skb::F_NFAM) return 1;
+  skb::prof().flops[fam] += flops;
+  skb::prof().bytes[fam] += bytes;
+  return 0;
+}
+
+extern "C" int skb_prof_read(double* ms_out, int64_t* count_out, double* flops_out,
+                             double* bytes_out, int32_t reset) {
+  auto& P = skb::prof();
+  for (int f = 0; f < skb::F_NFAM; ++f) {
+    double ms = 0.0;
+    for (auto& e : P.ev[f]) {
+      float t = 0.f;
+      cudaEventSynchronize(e.second);
+      cudaEventElapsedTime(&t, e.first, e.second);
+      ms += t;
+    }
+    ms_out[f] = ms;
+    count_out[f] = (int64_t)P.ev[f].size();
+    flops_out[f] = P.flops[f];
+    bytes_out[f] = P.bytes[f];
+    if (reset) {
+      for (auto& e : P.ev[f]) { P.pool.push_back(e.first); P.pool.push_back(e.second); }
+      P.ev[f].clear();
+      P.flops[f] = 0.0;
+      P.bytes[f] = 0.0;
+    }
+  }
+  return 0;
+}

@@ -120,6 +120,109 @@ def _csr(arrays):
     return off, flat
 
 
+IO = {"h2d": 0, "d2h": 0}      # host<->device bytes moved by this module
+
+
+def _d2h(t: torch.Tensor) -> np.ndarray:
+    IO["d2h"] += t.numel() * t.element_size()
+    return t.cpu().numpy()
+
+
+def _seg_gather(src, starts, lens):
+    """Concatenate src[starts[j]:starts[j]+lens[j]] for all j (vectorised)."""
+    lens = np.asarray(lens, np.int64)
+    off = np.zeros(len(lens) + 1, np.int64)
+    np.cumsum(lens, out=off[1:])
+    tot = int(off[-1])
+    if tot == 0:
+        return off, src[:0].copy()
+    idx = np.repeat(np.asarray(starts, np.int64) - off[:-1], lens) + np.arange(tot)
+    return off, src[idx]
+
+
+class ActStore:
+    """Active / skeleton DOF lists of every tree box as segments of one flat
+    array (vectorised replacement of the reference's per-box ``bx.active`` /
+    ``bx.skel`` arrays, skel.py:243-256)."""
+
+    def __init__(self, t: Tree):
+        nbox = len(t.lev)
+        cap = 2 * t.n_nodes * (t.depth + 3) + 16
+        self.big = np.empty(cap, np.int64)
+        self.fill = 0
+        self.a_start = np.zeros(nbox, np.int64)
+        self.a_len = np.zeros(nbox, np.int64)
+        self.s_start = np.zeros(nbox, np.int64)
+        self.s_len = np.zeros(nbox, np.int64)
+        self.xss = np.zeros(nbox, np.uint64)
+        leaves = np.flatnonzero(t.is_leaf)
+        # leaf actives: dofs 2*node + {0,1} of the sorted owned nodes (skel.py:243-249)
+        for l in range(t.depth + 1):
+            li = leaves[t.lev[leaves] == l]
+            if len(li) == 0:
+                continue
+            off, nodes = _seg_gather(t.level_nodes[l], t.node_start[li], t.node_cnt[li])
+            dofs = (2 * nodes[:, None] + np.arange(2)[None, :]).ravel()
+            self.a_start[li] = self._append(dofs) + 2 * off[:-1]
+            self.a_len[li] = 2 * t.node_cnt[li]
+
+    @classmethod
+    def replay(cls, t: Tree, act_of: dict) -> "ActStore":
+        """Store with given active sets (per-level replay of recorded inputs)."""
+        st = cls(t)
+        for i, a in act_of.items():
+            st.a_start[i] = st._append(np.asarray(a, np.int64))
+            st.a_len[i] = len(a)
+        return st
+
+    def _append(self, arr):
+        n = len(arr)
+        if self.fill + n > len(self.big):
+            nb = np.empty(max(2 * len(self.big), self.fill + n), np.int64)
+            nb[:self.fill] = self.big[:self.fill]
+            self.big = nb
+        o = self.fill
+        self.big[o:o + n] = arr
+        self.fill += n
+        return o
+
+    def act(self, i):
+        return self.big[self.a_start[i]:self.a_start[i] + self.a_len[i]]
+
+    def skel(self, i):
+        return self.big[self.s_start[i]:self.s_start[i] + self.s_len[i]]
+
+    def acts(self, idx):
+        return _seg_gather(self.big, self.a_start[idx], self.a_len[idx])
+
+    def set_internal(self, t: Tree, idx):
+        """Internal boxes: active = concat of children's skeletons in child order."""
+        idx = np.asarray(idx, np.int64)
+        idx = idx[~t.is_leaf[idx]]
+        if len(idx) == 0:
+            return
+        ch = t.children[idx]
+        valid = ch >= 0
+        cflat = ch[valid]
+        off, dofs = _seg_gather(self.big, self.s_start[cflat], self.s_len[cflat])
+        base = self._append(dofs)
+        lens = np.where(valid, self.s_len[np.maximum(ch, 0)], 0)
+        tot = lens.sum(axis=1)
+        st = np.zeros(len(idx), np.int64)
+        np.cumsum(tot[:-1], out=st[1:])
+        self.a_start[idx] = base + st
+        self.a_len[idx] = tot
+
+    def set_skel(self, idx, act_off, act, perm, k):
+        """skel = act[perm[:k]] per box (vectorised)."""
+        pos_off, pos = _seg_gather(perm.astype(np.int64), act_off[:-1], k)
+        owner_base = np.repeat(act_off[:-1], k)
+        sk = act[owner_base + pos]
+        base = self._append(sk)
+        self.s_start[idx] = base + pos_off[:-1]
+        self.s_len[idx] = k
+
+
 def _upload(**arrays):
     """One pinned H2D copy for several host arrays; returns device views."""
     dev = _dev()
@@ -134,6 +237,7 @@ def _upload(**arrays):
     for k, a, o in items:
         hn[o:o + a.nbytes] = a.view(np.uint8).reshape(-1)
     d = host.to(dev, non_blocking=True)
+    IO["h2d"] += total
     out = {}
     for k, a, o in items:
         tdt = {np.dtype(np.int64): torch.int64, np.dtype(np.float64): torch.float64,
@@ -175,6 +279,9 @@ def _addr(t: torch.Tensor) -> int:
 # device geometry
 # ---------------------------------------------------------------------------
 class DeviceBoundary:
+    """Boundary SoA arrays resident in HBM.  ``Boundary._skb_device = DeviceBoundary(b)``
+    keeps them resident across factor() calls (device-resident benchmark mode)."""
+
     def __init__(self, b):
         up = _upload(pos=np.ascontiguousarray(b.positions, np.float64),
                      nrm=np.ascontiguousarray(b.normals, np.float64),
@@ -212,13 +319,14 @@ class BoxBatch:
     def r(self):
         return self.nB - self.k
 
-    def skel_lists(self):
-        return [self.act[self.act_off[b] + self.perm[self.act_off[b]:self.act_off[b] + self.k[b]]]
-                for b in range(len(self.idx))]
+    def skel_csr(self):
+        off, pos = _seg_gather(self.perm.astype(np.int64), self.act_off[:-1], self.k)
+        return off, self.act[np.repeat(self.act_off[:-1], self.k) + pos]
 
-    def red_lists(self):
-        return [self.act[self.act_off[b] + self.perm[self.act_off[b] + self.k[b]:self.act_off[b + 1]]]
-                for b in range(len(self.idx))]
+    def red_csr(self):
+        r = self.r
+        off, pos = _seg_gather(self.perm.astype(np.int64), self.act_off[:-1] + self.k, r)
+        return off, self.act[np.repeat(self.act_off[:-1], r) + pos]
 
     def take(self, sel, other, osel):
         """Overwrite boxes ``sel`` with ``other``'s boxes ``osel`` (same DOF layout)."""
@@ -246,10 +354,8 @@ class LevelFactors:
         self.keys = [tree.key(i) for i in self.idx]
         self.k = batch.k.copy()
         self.r = batch.r.copy()
-        sk = batch.skel_lists()
-        rd = batch.red_lists()
-        self.sd_off, self.sd = _csr(sk)
-        self.rd_off, self.rd = _csr(rd)
+        self.sd_off, self.sd = batch.skel_csr()
+        self.rd_off, self.rd = batch.red_csr()
         self.cols_off, self.cols = cols_off, cols
         self.ncols = np.diff(cols_off)
         up = _upload(sd_off=self.sd_off, sd=self.sd if len(self.sd) else np.zeros(1, np.int64),
@@ -273,18 +379,20 @@ class _Ctx:
         self.dof_xy = np.repeat(b.positions, 2, axis=0)
         th = 2 * np.pi * np.arange(self.P) / self.P
         self.cs = np.stack([np.cos(th), np.sin(th)], axis=1)
-        self.xss = {}        # tree box index -> (device address, k)
         self.stats = {"kernel_s": {}}
 
     @property
     def g(self) -> DeviceBoundary:
         if self._g is None:
-            self._g = DeviceBoundary(self.b)
+            cached = getattr(self.b, "_skb_device", None)
+            self._g = cached if cached is not None else DeviceBoundary(self.b)
         return self._g
 
     # -- host bookkeeping ---------------------------------------------------
-    def far_lists(self, idx, act_of):
-        """F_int per box (reference _Compressor.far_dofs, skel.py:258-280)."""
+    def far_lists(self, idx, store: "ActStore"):
+        """F_int per box (reference _Compressor.far_dofs, skel.py:258-280):
+        colleagues (sorted keys) then coarser leaves meeting the proxy disc
+        (sorted keys), filtered by strict distance < r_p from the box centre."""
         t = self.t
         rp = proxy_radius(t.hw[idx], self.factor)
         nbr = t.neighbors[idx]
@@ -300,9 +408,8 @@ class _Ctx:
         B = len(idx)
         if len(ps) == 0:
             return np.zeros(B + 1, np.int64), np.zeros(0, np.int64)
-        parts = [act_of[s] for s in ps]
-        lens = np.fromiter((len(p) for p in parts), np.int64, len(parts))
-        flat = np.concatenate(parts)
+        lens = store.a_len[ps]
+        _, flat = _seg_gather(store.big, store.a_start[ps], lens)
         owner = np.repeat(pb, lens)
         d = self.dof_xy[flat] - t.center[idx][owner]
         d2 = (d ** 2).sum(axis=1)
@@ -326,33 +433,31 @@ class _Ctx:
         pw = 2 * np.pi * rp / self.P
         return pts, pn, pw
 
-    def child_desc(self, idx, act_of):
+    def child_desc(self, idx, store: "ActStore"):
+        """Children's skeleton offsets (active order) and Xss addresses."""
+        idx = np.asarray(idx, np.int64)
+        ch = self.t.children[idx]
+        valid = ch >= 0
+        kc = np.where(valid, store.s_len[np.maximum(ch, 0)], 0)
         co = np.full((len(idx), 5), -1, np.int64)
-        cx = np.zeros((len(idx), 4), np.uint64)
-        t = self.t
-        for bi, i in enumerate(idx):
-            ch = t.children_of(i)
-            if not ch:
-                continue
-            off = 0
-            co[bi, 0] = 0
-            for c, j in enumerate(ch):
-                p, kc = self.xss[j]
-                off += kc
-                co[bi, c + 1] = off
-                cx[bi, c] = p
+        inner = valid.any(axis=1)
+        cum = np.cumsum(kc, axis=1)
+        co[inner, 0] = 0
+        co[:, 1:] = np.where(valid, cum, -1)
+        co[~inner, 1:] = -1
+        cx = np.where(valid, store.xss[np.maximum(ch, 0)], np.uint64(0)).astype(np.uint64)
         return co, cx
 
     # -- device pipeline ----------------------------------------------------
-    def compress(self, idx, act_of, kmin=None) -> BoxBatch:
+    def compress(self, idx, store: "ActStore", kmin=None) -> BoxBatch:
         """Compress a batch of same-level boxes (reference compress_box, skel.py:293-338)."""
         t, P = self.t, self.P
         _Prof.start()
         idx = np.asarray(idx, np.int64)
         B = len(idx)
-        act_off, act = _csr([act_of[i] for i in idx])
+        act_off, act = store.acts(idx)
         nB = np.diff(act_off)
-        far_off, far = self.far_lists(idx, act_of)
+        far_off, far = self.far_lists(idx, store)
         nF = np.diff(far_off)
         pts, pn, pw = self.proxies(idx)
         rows = 2 * nF + 6 * P + 2
@@ -392,13 +497,24 @@ class _Ctx:
              ptr(diag_d), ptr(out_i), ptr(out_i) + 4 * B, ptr(gap_d), s)
         _Prof.tick("b_qrcp")
         bt = BoxBatch(idx, act_off, act)
-        bt.perm[:] = perm_d[:len(act)].cpu().numpy()      # sync point 1 (sizes for (c))
-        oi = out_i.cpu().numpy()
+        bt.perm[:] = _d2h(perm_d[:len(act)])      # sync point 1 (sizes for (c))
+        oi = _d2h(out_i)
         bt.k[:] = oi[:B]
         bt.steps[:] = oi[B:]
-        bt.gap[:] = gap_d.cpu().numpy()
+        bt.gap[:] = _d2h(gap_d)
         k = bt.k
         r = nB - k
+        if _lib.PROF_ON:
+            # algorithmic work: stack + self-block bytes written,
+            # Householder 2 m n^2 - 2/3 n^3, QRCP 2mn + sum_i 4 (m-i)(n-i-1)
+            _lib.prof_add("assemble", 0.0, 8.0 * float((rows * nB).sum() + (nB * nB).sum()))
+            mr, nr_ = rows[pre].astype(float), nB[pre].astype(float)
+            _lib.prof_add("geqrf", float((2 * mr * nr_ ** 2 - 2.0 / 3.0 * nr_ ** 3).sum()))
+            fq = 0.0
+            for mm, nn, st in zip(m_q, nB, bt.steps):
+                i_ = np.arange(st, dtype=float)
+                fq += 2.0 * mm * nn + float((4.0 * (mm - i_) * (nn - i_ - 1)).sum())
+            _lib.prof_add("qrcp", fq)
         # ---- factor storage (one slab) and scratch
         sz = np.stack([k * r, r * r, r * r, k * r, r * k, k * k], axis=1)
         tot = sz.sum(axis=1)
@@ -425,7 +541,7 @@ class _Ctx:
         call("skb_id_T_batched", B, A, lda, k.astype(np.int64), nB.astype(np.int64), perm_ptrs,
              bt.ptr["T"].astype(np.int64), s)
         # ---- permuted self blocks with children's Xss
-        co, cx = self.child_desc(idx, act_of)
+        co, cx = self.child_desc(idx, store)
         up2 = _upload(co=co.reshape(-1), cx=cx.reshape(-1), E_off=E_off[:-1], E_ld=nB.astype(np.int64))
         call("skb_assemble_self", ptr(self.g.pos), ptr(self.g.nrm), ptr(self.g.w), ptr(self.g.kap),
              B, ptr(up["act_off"]), ptr(up["act"]), ptr(up["act_off"]), ptr(perm_d),
@@ -472,14 +588,14 @@ class _Ctx:
         _gemm([dict(A=Xsr, B=Xrsdiv, C=Ess, D=bt.ptr["Xss"], m=k, n=k, k=r, lda=r, ldb=k,
                     ldc=nB, ldd=k, alpha=mone, beta=one)])
         _Prof.tick("c_getrs_xss")
-        bt.info[:] = info_d.cpu().numpy()                 # sync point 2 (migration check)
-        bt.ratio[:] = ratio_d.cpu().numpy()
+        bt.info[:] = _d2h(info_d)                 # sync point 2 (migration check)
+        bt.ratio[:] = _d2h(ratio_d)
         bt._scratch = None
         del stack, Ebuf, Xrs
         return bt
 
-    def compress_level(self, idx, act_of) -> BoxBatch:
-        bt = self.compress(idx, act_of)
+    def compress_level(self, idx, store) -> BoxBatch:
+        bt = self.compress(idx, store)
         # R -> S migration while the X_RR pivot ratio is below the floor (skel.py:317-330)
         while True:
             kk = bt.k
@@ -488,7 +604,7 @@ class _Ctx:
                 break
             sel = np.flatnonzero(bad)
             knew = np.minimum(bt.nB[sel], kk[sel] + np.maximum(1, (bt.nB[sel] - kk[sel]) // 8))
-            sub = self.compress(bt.idx[sel], act_of, kmin=knew)
+            sub = self.compress(bt.idx[sel], store, kmin=knew)
             bt.take(sel, sub, np.arange(len(sel)))
         return bt
 
@@ -833,33 +949,39 @@ class Factorization:
 # _finish_top and the drivers
 # ---------------------------------------------------------------------------
 def _hole_columns(t: Tree, b, idx):
-    """Augmentation columns touched by each box: 3 per hole with nodes in the box."""
-    if b.n_holes == 0:
-        return np.zeros(len(idx) + 1, np.int64), np.zeros(0, np.int64)
-    cof = b.curve_of_node()
-    lists = []
-    for i in idx:
-        cur = np.unique(cof[t.nodes_of(i)])
-        h = cur[cur >= 1] - 1
-        lists.append((3 * h[:, None] + np.arange(3)[None, :]).ravel())
-    return _csr(lists)
+    """Augmentation columns touched by each box: 3 per hole with nodes in the box
+    (PsiV rows of a box's DOFs are zero outside these columns)."""
+    idx = np.asarray(idx, np.int64)
+    B = len(idx)
+    if b.n_holes == 0 or B == 0:
+        return np.zeros(B + 1, np.int64), np.zeros(0, np.int64)
+    l = int(t.lev[idx[0]])
+    off, nodes = _seg_gather(t.level_nodes[l], t.node_start[idx], t.node_cnt[idx])
+    cur = np.searchsorted(b.offsets, nodes, side="right") - 1
+    owner = np.repeat(np.arange(B), np.diff(off))
+    key = np.unique(owner * (b.n_holes + 1) + cur)
+    bo, cv = key // (b.n_holes + 1), key % (b.n_holes + 1)
+    sel = cv >= 1
+    bo, h = bo[sel], cv[sel] - 1
+    cols = (3 * h[:, None] + np.arange(3)[None, :]).ravel()
+    cnt = np.bincount(bo, minlength=B) * 3
+    o = np.zeros(B + 1, np.int64)
+    np.cumsum(cnt, out=o[1:])
+    return o, cols.astype(np.int64)
 
 
-def _finish_top(ctx: _Ctx, levels, act_of):
+def _finish_top(ctx: _Ctx, levels, store):
     """Root block, augmentation sweep and corner LU (reference skel.py:364-425)."""
     t, b = ctx.t, ctx.b
     dev = _dev()
     s = _stream()
     root = 0
-    if t.is_leaf[root]:
-        rd = (2 * t.nodes_of(root)[:, None] + np.arange(2)[None, :]).ravel()
-    else:
-        rd = np.concatenate([ctx.skel_of[c] for c in t.children_of(root)])
-    act_of[root] = rd
+    store.set_internal(t, np.array([root]))
+    rd = store.act(root).copy()
     ns = len(rd)
     nd = 2 * b.n_nodes
     q = 3 * b.n_holes if ctx.spec.augmented(b) else 0
-    co, cx = ctx.child_desc(np.array([root]), act_of)
+    co, cx = ctx.child_desc(np.array([root]), store)
     E_root = torch.empty((max(ns, 1), max(ns, 1)), dtype=torch.float64, device=dev)
     up = _upload(ao=np.array([0, ns], np.int64), a=rd if ns else np.zeros(1, np.int64),
                  co=co.reshape(-1), cx=cx.reshape(-1), eo=np.zeros(1, np.int64),
@@ -990,49 +1112,35 @@ def _aug_level(L: LevelFactors, UH, PsiV, UH_div, schur, q):
     L._aug_keep2 = (buf, up)
 
 
-def _leaf_dofs(t, i):
-    return (2 * t.nodes_of(i)[:, None] + np.arange(2)[None, :]).ravel()
-
-
 def _run_levels(ctx: _Ctx, reuse=None, dirty=None):
     """Bottom-up level loop (reference factor skel.py:443-449 / update skel.py:502-509)."""
     t = ctx.t
-    act_of = {}
-    for i in np.flatnonzero(t.is_leaf):
-        act_of[int(i)] = _leaf_dofs(t, int(i))
-    ctx.skel_of = {}
+    store = ActStore(t)
+    ctx.store = store
     levels = []
     n_recomp = 0
     for lev in range(t.depth, 0, -1):
         idx = t.level_indices(lev)
-        for i in idx:
-            if not t.is_leaf[i]:
-                act_of[int(i)] = np.concatenate([ctx.skel_of[c] for c in t.children_of(i)])
+        store.set_internal(t, idx)            # assign_internal_actives, skel.py:251-256
         if reuse is None:
             todo = idx
         else:
             todo = np.array([i for i in idx if t.key(i) in dirty], np.int64)
-        bt_new = ctx.compress_level(todo, act_of) if len(todo) else None
+        bt_new = ctx.compress_level(todo, store) if len(todo) else None
         n_recomp += len(todo)
-        if reuse is None:
-            bt = bt_new
-        else:
-            bt = _merge_level(ctx, idx, act_of, todo, bt_new, reuse)
-        for bi, i in enumerate(bt.idx):
-            a0 = bt.act_off[bi]
-            kk = int(bt.k[bi])
-            ctx.skel_of[int(i)] = bt.act[a0 + bt.perm[a0:a0 + kk]]
-            ctx.xss[int(i)] = (int(bt.ptr["Xss"][bi]), kk)
+        bt = bt_new if reuse is None else _merge_level(ctx, idx, store, todo, bt_new, reuse)
+        store.set_skel(bt.idx, bt.act_off, bt.act, bt.perm, bt.k)
+        store.xss[bt.idx] = bt.ptr["Xss"]
         cols_off, cols = _hole_columns(t, ctx.b, bt.idx)
         levels.append(LevelFactors(lev, t, bt, cols_off, cols))
-    return levels, act_of, n_recomp
+    return levels, store, n_recomp
 
 
-def _merge_level(ctx, idx, act_of, todo, bt_new, old_levels):
+def _merge_level(ctx, idx, store, todo, bt_new, old_levels):
     """Level batch for an update: dirty boxes from bt_new, clean boxes share the
     old factor memory (reference run_level reuse path, skel.py:342-353)."""
     t = ctx.t
-    act_off, act = _csr([act_of[int(i)] for i in idx])
+    act_off, act = store.acts(idx)
     bt = BoxBatch(idx, act_off, act)
     pos_new = {int(i): j for j, i in enumerate(todo)}
     for bi, i in enumerate(idx):
@@ -1040,8 +1148,7 @@ def _merge_level(ctx, idx, act_of, todo, bt_new, old_levels):
         if int(i) in pos_new:
             bt.take([bi], bt_new, [pos_new[int(i)]])
             continue
-        li, bj = old_levels[key]
-        L = li
+        L, bj = old_levels[key]
         ob = L.batch
         a0, a1 = ob.act_off[bj], ob.act_off[bj + 1]
         if not np.array_equal(ob.act[a0:a1], act[act_off[bi]:act_off[bi + 1]]):
@@ -1063,8 +1170,8 @@ def factor(spec, b, t: Tree, tol: float, workers: int = 1,
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     ctx = _Ctx(spec, b, t, tol, proxy_count, proxy_factor)
-    levels, act_of, _ = _run_levels(ctx)
-    rd, E_root, top, ipiv, UH, PsiV, UH_div, q, ratio = _finish_top(ctx, levels, act_of)
+    levels, store, _ = _run_levels(ctx)
+    rd, E_root, top, ipiv, UH, PsiV, UH_div, q, ratio = _finish_top(ctx, levels, store)
     torch.cuda.synchronize()
     stats = {"k_per_level": {L.lev: int(L.k.max(initial=0)) for L in levels},
              "root_size": len(rd), "top_pivot_ratio": ratio}
@@ -1091,8 +1198,8 @@ def update(fct: Factorization, b_new, report, workers: int = 1) -> Factorization
         for bj, key in enumerate(L.keys):
             old[key] = (L, bj)
     ctx = _Ctx(fct.spec, b_new, t_new, fct.tol, fct.proxy_count, fct.proxy_factor)
-    levels, act_of, n_recomp = _run_levels(ctx, reuse=old, dirty=dirty)
-    rd, E_root, top, ipiv, UH, PsiV, UH_div, q, ratio = _finish_top(ctx, levels, act_of)
+    levels, store, n_recomp = _run_levels(ctx, reuse=old, dirty=dirty)
+    rd, E_root, top, ipiv, UH, PsiV, UH_div, q, ratio = _finish_top(ctx, levels, store)
     torch.cuda.synchronize()
     stats = {"k_per_level": {L.lev: int(L.k.max(initial=0)) for L in levels},
              "root_size": len(rd), "top_pivot_ratio": ratio}

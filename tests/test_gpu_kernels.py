@@ -121,7 +121,7 @@ def test_stack_assembly_bitwise(golden, name, builder):
         act_of = {j: ref[t.key(j)]["act"] for j in range(len(t.lev)) if t.key(j) in ref}
         idx = np.array([bi])
         act_off, act = skel._csr([act_of[bi]])
-        far_off, far = ctx.far_lists(idx, act_of)
+        far_off, far = ctx.far_lists(idx, skel.ActStore.replay(t, act_of))
         pts, pn, pw = ctx.proxies(idx)
         nB, nF, P = len(act), len(far), wl.proxy_count
         rows = 2 * nF + 6 * P + 2
@@ -178,14 +178,11 @@ def test_id_replay_skeletons(golden, name, builder):
     mism = []
     for lev in range(t.depth, 0, -1):
         idx = t.level_indices(lev)
-        for i in idx:
-            if not t.is_leaf[i]:
-                ctx.xss[int(i)] = (0, 0)
         # run only the ID part (stack + QR) to avoid needing children's Xss
         B = len(idx)
         act_off, act = skel._csr([act_of[int(i)] for i in idx])
         nB = np.diff(act_off)
-        far_off, far = ctx.far_lists(idx, act_of)
+        far_off, far = ctx.far_lists(idx, skel.ActStore.replay(t, act_of))
         nF = np.diff(far_off)
         pts, pn, pw = ctx.proxies(idx)
         P = wl.proxy_count

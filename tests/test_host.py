@@ -50,7 +50,7 @@ def test_far_lists_and_proxies_match_reference(golden, name, builder):
             act_of[i] = (2 * t.nodes_of(i)[:, None] + np.arange(2)).ravel()
     for lev in range(t.depth, 0, -1):
         idx = t.level_indices(lev)
-        off, F = ctx.far_lists(idx, act_of)
+        off, F = ctx.far_lists(idx, skel.ActStore.replay(t, act_of))
         for bi, i in enumerate(idx):
             assert np.array_equal(F[off[bi]:off[bi + 1]], ref[t.key(i)]["far"]), t.key(i)
         pts, pn, pw = ctx.proxies(idx)
