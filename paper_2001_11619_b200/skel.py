@@ -376,7 +376,8 @@ class _Ctx:
         if self.P < 8:
             raise ValueError("need at least 8 proxy nodes")
         self._g = None
-        self.dof_xy = np.repeat(b.positions, 2, axis=0)
+        self.px = np.ascontiguousarray(b.positions[:, 0])
+        self.py = np.ascontiguousarray(b.positions[:, 1])
         th = 2 * np.pi * np.arange(self.P) / self.P
         self.cs = np.stack([np.cos(th), np.sin(th)], axis=1)
         self.stats = {"kernel_s": {}}
@@ -398,9 +399,7 @@ class _Ctx:
         nbr = t.neighbors[idx]
         bl_n, s_n = np.nonzero(nbr >= 0)
         src_n = nbr[bl_n, s_n]
-        mask, cand = t.coarse_leaves_mask(idx, rp)
-        bl_c, c_c = np.nonzero(mask)
-        src_c = cand[c_c]
+        bl_c, src_c = t.coarse_leaves(idx, rp)
         pb = np.concatenate([bl_n, bl_c]).astype(np.int64)
         ps = np.concatenate([src_n, src_c]).astype(np.int64)
         order = np.argsort(pb, kind="stable")
@@ -411,8 +410,11 @@ class _Ctx:
         lens = store.a_len[ps]
         _, flat = _seg_gather(store.big, store.a_start[ps], lens)
         owner = np.repeat(pb, lens)
-        d = self.dof_xy[flat] - t.center[idx][owner]
-        d2 = (d ** 2).sum(axis=1)
+        # ((dof_pos - c)**2).sum(axis=1) of skel.py:279, same rounding: dx*dx + dy*dy
+        node = flat >> 1
+        dx = self.px[node] - t.center[idx, 0][owner]
+        dy = self.py[node] - t.center[idx, 1][owner]
+        d2 = dx * dx + dy * dy
         keep = d2 < (rp * rp)[owner]
         F = flat[keep]
         cnt = np.bincount(owner[keep], minlength=B)
@@ -948,23 +950,26 @@ class Factorization:
 # ---------------------------------------------------------------------------
 # _finish_top and the drivers
 # ---------------------------------------------------------------------------
-def _hole_columns(t: Tree, b, idx):
+def _hole_columns(t: Tree, b, idx, pairs=None):
     """Augmentation columns touched by each box: 3 per hole with nodes in the box
     (PsiV rows of a box's DOFs are zero outside these columns)."""
     idx = np.asarray(idx, np.int64)
     B = len(idx)
     if b.n_holes == 0 or B == 0:
         return np.zeros(B + 1, np.int64), np.zeros(0, np.int64)
-    l = int(t.lev[idx[0]])
-    off, nodes = _seg_gather(t.level_nodes[l], t.node_start[idx], t.node_cnt[idx])
-    cur = np.searchsorted(b.offsets, nodes, side="right") - 1
-    owner = np.repeat(np.arange(B), np.diff(off))
-    key = np.unique(owner * (b.n_holes + 1) + cur)
-    bo, cv = key // (b.n_holes + 1), key % (b.n_holes + 1)
-    sel = cv >= 1
-    bo, h = bo[sel], cv[sel] - 1
+    if pairs is None:
+        pairs = t.hole_pairs(np.asarray(b.offsets, np.int64))
+    pb, pc = pairs
+    pos = np.searchsorted(pb, idx)
+    end = np.searchsorted(pb, idx, side="right")
+    lens = end - pos
+    off, sel = _seg_gather(np.arange(len(pb)), pos, lens)
+    cur = pc[sel]
+    holes = cur >= 1
+    owner = np.repeat(np.arange(B), lens)[holes]
+    h = cur[holes] - 1
     cols = (3 * h[:, None] + np.arange(3)[None, :]).ravel()
-    cnt = np.bincount(bo, minlength=B) * 3
+    cnt = np.bincount(owner, minlength=B) * 3
     o = np.zeros(B + 1, np.int64)
     np.cumsum(cnt, out=o[1:])
     return o, cols.astype(np.int64)
@@ -1108,8 +1113,8 @@ def _aug_level(L: LevelFactors, UH, PsiV, UH_div, schur, q):
         np.cumsum(np.bincount(rows, minlength=q), out=row_off[1:])
         up3 = _upload(ro=row_off, ct=contrib[order].astype(np.int64))
         call("skb_schur_accumulate", q, ptr(up3["ro"]), ptr(up3["ct"]), base, ptr(schur), s)
-        L._aug_keep = up3
-    L._aug_keep2 = (buf, up)
+    # buf/up are released here: the caching allocator is stream-ordered, so the
+    # memory is reused only after the kernels above have run
 
 
 def _run_levels(ctx: _Ctx, reuse=None, dirty=None):
@@ -1117,6 +1122,7 @@ def _run_levels(ctx: _Ctx, reuse=None, dirty=None):
     t = ctx.t
     store = ActStore(t)
     ctx.store = store
+    pairs = t.hole_pairs(np.asarray(ctx.b.offsets, np.int64)) if ctx.b.n_holes else None
     levels = []
     n_recomp = 0
     for lev in range(t.depth, 0, -1):
@@ -1131,7 +1137,7 @@ def _run_levels(ctx: _Ctx, reuse=None, dirty=None):
         bt = bt_new if reuse is None else _merge_level(ctx, idx, store, todo, bt_new, reuse)
         store.set_skel(bt.idx, bt.act_off, bt.act, bt.perm, bt.k)
         store.xss[bt.idx] = bt.ptr["Xss"]
-        cols_off, cols = _hole_columns(t, ctx.b, bt.idx)
+        cols_off, cols = _hole_columns(t, ctx.b, bt.idx, pairs)
         levels.append(LevelFactors(lev, t, bt, cols_off, cols))
     return levels, store, n_recomp
 

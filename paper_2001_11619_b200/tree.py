@@ -112,10 +112,65 @@ class Tree:
             for i in leaves:
                 self.node_leaf[self.nodes_of(i)] = i
 
+    def coarse_leaves(self, box_idx, radius):
+        """Leaves above the boxes' level meeting the disc (centre, radius), as
+        (box position, leaf index) pairs sorted by key per box -- reference
+        Tree.shallow_leaves_near, tree.py:83-99.  Candidates come from the
+        level grid (every box of a coarser level covering a cell the disc's
+        bounding square touches), then the reference's box-disc test."""
+        box_idx = np.asarray(box_idx, np.int64)
+        B = len(box_idx)
+        if B == 0:
+            return np.zeros(0, np.int64), np.zeros(0, np.int64)
+        L = int(self.lev[box_idx[0]])
+        c = self.center[box_idx]
+        r = np.asarray(radius, float)
+        origin = self.root_center - self.root_half_width
+        side = np.int64(1) << np.int64(L)
+        cell = 2.0 * self.root_half_width / float(side)
+        lo = np.floor((c - r[:, None] - origin[None, :]) / cell).astype(np.int64)
+        hi = np.floor((c + r[:, None] - origin[None, :]) / cell).astype(np.int64)
+        lo = np.clip(lo, 0, side - 1)
+        hi = np.clip(hi, 0, side - 1)
+        pb_all, pc_all = [], []
+        for lp in range(L):
+            idx_l = self.level_indices(lp)
+            if len(idx_l) == 0:
+                continue
+            sh = np.int64(L - lp)
+            s_l = np.int64(1) << np.int64(lp)
+            clo, chi = lo >> sh, hi >> sh            # cell ranges covered at level lp
+            codes_l = self.ix[idx_l] * s_l + self.iy[idx_l]
+            wx = int((chi[:, 0] - clo[:, 0]).max()) + 1
+            wy = int((chi[:, 1] - clo[:, 1]).max()) + 1
+            for ox in range(wx):
+                for oy in range(wy):
+                    cx = clo[:, 0] + ox
+                    cy = clo[:, 1] + oy
+                    dup = (cx > chi[:, 0]) | (cy > chi[:, 1])
+                    code = cx * s_l + cy
+                    pos = np.searchsorted(codes_l, code)
+                    pos_c = np.minimum(pos, len(codes_l) - 1)
+                    hit = (~dup) & (codes_l[pos_c] == code)
+                    j = idx_l[pos_c[hit]]
+                    leaf = self.is_leaf[j]
+                    pb_all.append(np.flatnonzero(hit)[leaf])
+                    pc_all.append(j[leaf])
+        if not pb_all:
+            return np.zeros(0, np.int64), np.zeros(0, np.int64)
+        pb = np.concatenate(pb_all)
+        pc = np.concatenate(pc_all)
+        if len(pb) == 0:
+            return pb, pc
+        d = np.maximum(np.abs(c[pb] - self.center[pc]) - self.hw[pc][:, None], 0.0)
+        keep = ~(d[:, 0] * d[:, 0] + d[:, 1] * d[:, 1] > r[pb] * r[pb])
+        pb, pc = pb[keep], pc[keep]
+        # sort by (box, key); global index order == key order (levels ascending, keys sorted)
+        order = np.lexsort((pc, pb))
+        return pb[order], pc[order]
+
     def coarse_leaves_mask(self, box_idx, radius):
-        """(len(box_idx), n_cand) mask of leaves above the boxes' level meeting
-        the disc (centre, radius) -- reference Tree.shallow_leaves_near,
-        tree.py:83-99.  Returns (mask, candidate indices sorted by key)."""
+        """Dense variant (box x all coarser leaves), kept for tests."""
         l = int(self.lev[box_idx[0]])
         cand = np.flatnonzero(self.is_leaf & (self.lev < l))
         if len(cand) == 0 or len(box_idx) == 0:
@@ -127,6 +182,43 @@ class Tree:
         r = np.asarray(radius, float)
         mask = ~(dd > (r * r)[:, None])
         return mask, cand
+
+    def hole_pairs(self, curve_offsets):
+        """(box, curve) membership for every box, propagated leaves -> root."""
+        nbox = len(self.lev)
+        leaves = np.flatnonzero(self.is_leaf)
+        boxes, curves = [], []
+        for l in range(self.depth + 1):
+            li = leaves[self.lev[leaves] == l]
+            if len(li) == 0:
+                continue
+            st = self.node_start[li]
+            cnt = self.node_cnt[li]
+            off = np.zeros(len(li) + 1, np.int64)
+            np.cumsum(cnt, out=off[1:])
+            idx = np.repeat(st - off[:-1], cnt) + np.arange(off[-1])
+            nodes = self.level_nodes[l][idx]
+            cur = np.searchsorted(curve_offsets, nodes, side="right") - 1
+            boxes.append(np.repeat(li, cnt))
+            curves.append(cur)
+        b = np.concatenate(boxes)
+        cv = np.concatenate(curves)
+        nc = int(len(curve_offsets))
+        key = np.unique(b * nc + cv)
+        b, cv = key // nc, key % nc
+        allb, allc = [b], [cv]
+        cur_b, cur_c = b, cv
+        while True:
+            par = self.parent[cur_b]
+            ok = par >= 0
+            if not ok.any():
+                break
+            key = np.unique(par[ok] * nc + cur_c[ok])
+            cur_b, cur_c = key // nc, key % nc
+            allb.append(cur_b)
+            allc.append(cur_c)
+        key = np.unique(np.concatenate(allb) * nc + np.concatenate(allc))
+        return key // nc, key % nc
 
 
 def build_tree(positions, leaf_cap: int = 64, root_box=None, max_depth: int = 40) -> Tree:
