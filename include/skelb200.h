@@ -194,6 +194,16 @@ int skb_schur_accumulate(int64_t q, const int64_t* row_off, const int64_t* contr
 int skb_diag_fill(int64_t n, double* dst, int64_t ld, double diag_val, const double* src,
                   int64_t src_ld, double scale, void* stream);
 
+/* Exact augmented system product y = M x by direct summation (reference
+ * kernels.system_matvec, kernels.py:393-414): y[:2N] = (-1/2 I + D + N) mu + H lam,
+ * y[2N:] = Psi^T mu - lam.  x, y: (2N + 3p) x nrhs row-major; curve_off_dev:
+ * device int64 node offsets of the p+2 curve boundaries.  Residual oracle for
+ * the large configurations.                           */
+int skb_system_matvec(const double* pos, const double* nrm, const double* w, const double* kappa,
+                      int64_t n_nodes, const double* hole_centers, int64_t n_holes,
+                      const int64_t* curve_off_dev, const double* x, int64_t nrhs, double* y,
+                      void* stream);
+
 /* dst[idx[i]*ld + c] = value for i < nidx, c < ncols (the nonroot mask of
  * skel.py:181-188 applied by zeroing root rows of a copy). unused: NULL.    */
 int skb_fill_rows(int64_t nidx, const int64_t* idx, double* dst, int64_t ld, const void* unused,

@@ -10,6 +10,6 @@ from .geometry import (Boundary, Curve, GeometryError, MoveHole, PerturbationRep
                        apply_perturbation)
 from .tree import Tree, TreeError, build_tree, default_root_box, proxy_radius, refit_tree
 from .skel import (BoxFactors, Factorization, RootBoxExceededError, SingularPivotError, STOKES,
-                   SystemSpec, factor, update)
+                   SystemSpec, factor, system_matvec, update)
 
 __version__ = "0.1.0"

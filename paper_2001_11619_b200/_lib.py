@@ -52,6 +52,7 @@ SIGNATURES = {
     "skb_schur_accumulate": [_i64, _vp, _vp, _vp, _vp, _vp],
     "skb_diag_fill": [_i64, _vp, _i64, _f64, _vp, _i64, _f64, _vp],
     "skb_fill_rows": [_i64, _vp, _vp, _i64, _vp, _i64, _f64, _vp],
+    "skb_system_matvec": [_vp, _vp, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _i64, _vp, _vp],
 }
 
 _LIB = None

@@ -22,6 +22,7 @@ SOURCES = {
     "qr.cu": [],
     "lu.cu": [],
     "misc.cu": [],
+    "matvec.cu": [],
 }
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
           "--expt-relaxed-constexpr"]

@@ -1,0 +1,185 @@
+// Exact (uncompressed) augmented system product y = M x by direct summation --
+// reference kernels.system_matvec (kernels.py:393-414) built on eval_block
+// (kernels.py:89-130), stokeslet_rotlet_columns (kernels.py:201-223) and
+// build_augmentation's Psi (kernels.py:226-246):
+//   y[:nd] = (-1/2 I + D + N) mu + H lam,   y[nd:] = Psi^T mu - lam.
+// The residual oracle for the large configs (cfg3/cfg5), where the CPU
+// row-chunked product takes hours.  O(N^2) pairs, smem-tiled sources,
+// one thread per target node, RHS processed in chunks of 4 columns.
+#include "common.cuh"
+
+namespace skb {
+
+constexpr int MV_T = 128;   // targets per block / sources per tile
+constexpr int MV_R = 4;     // RHS per pass
+#define MV_PI 3.141592653589793
+
+// s[h] = sum_j w_j n_j . mu_j over all nodes (the rank-one completion N)
+__global__ void k_mv_ndot(const double2* __restrict__ nrm, const double* __restrict__ w,
+                          int64_t n, const double* __restrict__ x, int64_t nr, int64_t r0,
+                          int rc, double* __restrict__ out) {
+  __shared__ double red[MV_R][MV_T];
+  double acc[MV_R] = {0, 0, 0, 0};
+  for (int64_t j = blockIdx.x * (int64_t)MV_T + threadIdx.x; j < n; j += (int64_t)gridDim.x * MV_T) {
+    const double2 nj = nrm[j];
+    const double wj = w[j];
+    for (int q = 0; q < rc; ++q) {
+      const double m0 = x[(2 * j) * nr + r0 + q], m1 = x[(2 * j + 1) * nr + r0 + q];
+      acc[q] += wj * (nj.x * m0 + nj.y * m1);
+    }
+  }
+  for (int q = 0; q < MV_R; ++q) red[q][threadIdx.x] = acc[q];
+  __syncthreads();
+  for (int o = MV_T / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o)
+      for (int q = 0; q < MV_R; ++q) red[q][threadIdx.x] += red[q][threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0)
+    for (int q = 0; q < rc; ++q) out[blockIdx.x * MV_R + q] = red[q][0];
+}
+
+__global__ void __launch_bounds__(MV_T)
+k_mv_direct(const double2* __restrict__ pos, const double2* __restrict__ nrm,
+            const double* __restrict__ w, const double* __restrict__ kappa, int64_t n,
+            const double2* __restrict__ ctr, int64_t p, const double* __restrict__ x, int64_t nr,
+            int64_t r0, int rc, const double* __restrict__ ndot_parts, int nparts,
+            double* __restrict__ y) {
+  __shared__ double2 sp[MV_T], sn[MV_T];
+  __shared__ double sw[MV_T];
+  __shared__ double sx[MV_T][2 * MV_R];
+  __shared__ double s_nd[MV_R];
+  const int64_t i = blockIdx.x * (int64_t)MV_T + threadIdx.x;
+  if (threadIdx.x < MV_R) {
+    double s = 0.0;
+    for (int b = 0; b < nparts; ++b) s += ndot_parts[b * MV_R + threadIdx.x];
+    s_nd[threadIdx.x] = s;
+  }
+  const bool act = i < n;
+  const double2 pi = act ? pos[i] : make_double2(0, 0);
+  const double2 ni = act ? nrm[i] : make_double2(0, 0);
+  double a0[MV_R] = {0, 0, 0, 0}, a1[MV_R] = {0, 0, 0, 0};
+  for (int64_t j0 = 0; j0 < n; j0 += MV_T) {
+    __syncthreads();
+    const int64_t j = j0 + threadIdx.x;
+    if (j < n) {
+      sp[threadIdx.x] = pos[j];
+      sn[threadIdx.x] = nrm[j];
+      sw[threadIdx.x] = w[j];
+      for (int q = 0; q < rc; ++q) {
+        sx[threadIdx.x][2 * q] = x[(2 * j) * nr + r0 + q];
+        sx[threadIdx.x][2 * q + 1] = x[(2 * j + 1) * nr + r0 + q];
+      }
+    }
+    __syncthreads();
+    const int jn = (int)((n - j0) < MV_T ? (n - j0) : MV_T);
+    if (!act) continue;
+    for (int jj = 0; jj < jn; ++jj) {
+      const int64_t jg = j0 + jj;
+      const double2 pj = sp[jj], nj = sn[jj];
+      const double wj = sw[jj];
+      double k00, k01, k10, k11;
+      if (jg == i) {
+        // smooth-curve limit -(kappa/(2 pi)) tau tau^T, tau = (-n_y, n_x)
+        const double c = -(kappa[i] / (2.0 * MV_PI)) * wj;
+        const double t0 = -nj.y, t1 = nj.x;
+        k00 = c * t0 * t0; k01 = c * t0 * t1; k10 = c * t1 * t0; k11 = c * t1 * t1;
+      } else {
+        const double rx = pi.x - pj.x, ry = pi.y - pj.y;
+        const double r2 = rx * rx + ry * ry;
+        const double c = (rx * nj.x + ry * nj.y) / (MV_PI * r2 * r2) * wj;
+        k00 = c * rx * rx; k01 = c * rx * ry; k10 = k01; k11 = c * ry * ry;
+      }
+      for (int q = 0; q < MV_R; ++q) {
+        if (q >= rc) break;
+        const double m0 = sx[jj][2 * q], m1 = sx[jj][2 * q + 1];
+        a0[q] += k00 * m0 + k01 * m1;
+        a1[q] += k10 * m0 + k11 * m1;
+      }
+    }
+  }
+  if (!act) return;
+  for (int q = 0; q < rc; ++q) {
+    const double mu0 = x[(2 * i) * nr + r0 + q], mu1 = x[(2 * i + 1) * nr + r0 + q];
+    double y0 = a0[q] + ni.x * s_nd[q] - 0.5 * mu0;
+    double y1 = a1[q] + ni.y * s_nd[q] - 0.5 * mu1;
+    // H lam: Stokeslet (2 columns) + rotlet per hole centre
+    const double pref = 1.0 / (4.0 * MV_PI);
+    for (int64_t h = 0; h < p; ++h) {
+      const double2 c = ctr[h];
+      const double rx = pi.x - c.x, ry = pi.y - c.y;
+      const double r2 = rx * rx + ry * ry;
+      const double lg = -0.5 * log(r2);
+      const double l0 = x[(2 * n + 3 * h) * nr + r0 + q];
+      const double l1 = x[(2 * n + 3 * h + 1) * nr + r0 + q];
+      const double l2 = x[(2 * n + 3 * h + 2) * nr + r0 + q];
+      y0 += pref * (lg + rx * rx / r2) * l0 + pref * (rx * ry / r2) * l1 + pref * (-ry) / r2 * l2;
+      y1 += pref * (ry * rx / r2) * l0 + pref * (lg + ry * ry / r2) * l1 + pref * rx / r2 * l2;
+    }
+    y[(2 * i) * nr + r0 + q] = y0;
+    y[(2 * i + 1) * nr + r0 + q] = y1;
+  }
+}
+
+// y[nd + 3h + t] = sum over hole-h nodes of Psi rows . mu  - lam  (one block per hole)
+__global__ void k_mv_psi(const double2* __restrict__ pos, const double* __restrict__ w,
+                         const int64_t* __restrict__ curve_off, int64_t n,
+                         const double* __restrict__ x, int64_t nr, int64_t r0, int rc,
+                         double* __restrict__ y) {
+  __shared__ double red[3][MV_T];
+  const int64_t h = blockIdx.x;
+  const int64_t a = curve_off[h + 1], b = curve_off[h + 2];
+  for (int q = 0; q < rc; ++q) {
+    double s0 = 0, s1 = 0, s2 = 0;
+    for (int64_t j = a + threadIdx.x; j < b; j += MV_T) {
+      const double m0 = x[(2 * j) * nr + r0 + q], m1 = x[(2 * j + 1) * nr + r0 + q];
+      const double wj = w[j];
+      const double2 pj = pos[j];
+      s0 += wj * m0;
+      s1 += wj * m1;
+      s2 += (-pj.y) * wj * m0 + pj.x * wj * m1;
+    }
+    red[0][threadIdx.x] = s0;
+    red[1][threadIdx.x] = s1;
+    red[2][threadIdx.x] = s2;
+    __syncthreads();
+    for (int o = MV_T / 2; o > 0; o >>= 1) {
+      if (threadIdx.x < o)
+        for (int t = 0; t < 3; ++t) red[t][threadIdx.x] += red[t][threadIdx.x + o];
+      __syncthreads();
+    }
+    if (threadIdx.x < 3) {
+      const int64_t row = 2 * n + 3 * h + threadIdx.x;
+      y[row * nr + r0 + q] = red[threadIdx.x][0] - x[row * nr + r0 + q];
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace skb
+
+using namespace skb;
+
+extern "C" int skb_system_matvec(const double* pos, const double* nrm, const double* w,
+                                 const double* kappa, int64_t n_nodes, const double* hole_centers,
+                                 int64_t n_holes, const int64_t* curve_off_dev, const double* x,
+                                 int64_t nrhs, double* y, void* stream) {
+  if (n_nodes <= 0 || nrhs <= 0) return 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int nparts = 148;
+  double* parts = nullptr;
+  SKB_RET(cudaMallocAsync((void**)&parts, sizeof(double) * nparts * MV_R, s));
+  for (int64_t r0 = 0; r0 < nrhs; r0 += MV_R) {
+    const int rc = (int)((nrhs - r0) < MV_R ? (nrhs - r0) : MV_R);
+    k_mv_ndot<<<nparts, MV_T, 0, s>>>((const double2*)nrm, w, n_nodes, x, nrhs, r0, rc, parts);
+    k_mv_direct<<<(unsigned)((n_nodes + MV_T - 1) / MV_T), MV_T, 0, s>>>(
+        (const double2*)pos, (const double2*)nrm, w, kappa, n_nodes, (const double2*)hole_centers,
+        n_holes, x, nrhs, r0, rc, parts, nparts, y);
+    if (n_holes > 0)
+      k_mv_psi<<<(unsigned)n_holes, MV_T, 0, s>>>((const double2*)pos, w, curve_off_dev, n_nodes,
+                                                   x, nrhs, r0, rc, y);
+  }
+  cudaError_t e = cudaGetLastError();
+  cudaFreeAsync(parts, s);
+  return e == cudaSuccess ? 0 : -(int)e;
+}

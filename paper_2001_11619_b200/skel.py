@@ -1216,3 +1216,27 @@ def update(fct: Factorization, b_new, report, workers: int = 1) -> Factorization
     nf.stats["n_boxes"] = len(t_new.lev)
     nf.stats["dirty"] = dirty
     return nf
+
+
+def system_matvec(spec, b, x):
+    """Exact augmented system product on the GPU (reference kernels.system_matvec,
+    kernels.py:393-414), direct O(N^2) summation; x: (dim,) or (dim, nrhs)."""
+    is_t = isinstance(x, torch.Tensor)
+    xa = x if is_t else np.asarray(x, float)
+    nd, q = 2 * b.n_nodes, 3 * b.n_holes if spec.augmented(b) else 0
+    if xa.shape[0] != nd + q:
+        raise ValueError("dimension mismatch")
+    dev = _dev()
+    X = (xa.to(device=dev, dtype=torch.float64) if is_t
+         else torch.from_numpy(np.ascontiguousarray(xa)).to(dev)).reshape(nd + q, -1).contiguous()
+    g = getattr(b, "_skb_device", None) or DeviceBoundary(b)
+    up = _upload(hc=np.ascontiguousarray(b.hole_centers, np.float64).reshape(-1)
+                 if b.n_holes else np.zeros(2),
+                 co=np.ascontiguousarray(b.offsets, np.int64))
+    Y = torch.empty_like(X)
+    call("skb_system_matvec", g.pos, g.nrm, g.w, g.kap, b.n_nodes, up["hc"], q // 3, up["co"], X,
+         X.shape[1], Y, _stream())
+    if is_t:
+        return Y.reshape(x.shape)
+    out = Y.cpu().numpy()
+    return out.reshape(np.asarray(x).shape)

@@ -218,3 +218,22 @@ def test_id_replay_skeletons(golden, name, builder):
     untied = [m for m in mism if m[3] > 1e-12]
     assert not untied, untied
     assert not mism, mism      # these fixtures were chosen tie-free
+
+
+@pytest.mark.parametrize("m,n", [(40, 17), (300, 100), (700, 130), (1500, 200), (2400, 96), (520, 384)])
+def test_geqrf_batched_R(m, n):
+    """Batched Householder pre-reduction: R^T R == A^T A and |diag(R)| matches LAPACK."""
+    rng = np.random.default_rng(m + n)
+    As = [rng.standard_normal((m, n)) @ np.diag(np.logspace(0, -12, n)), rng.standard_normal((m, n))]
+    dev = [torch.from_numpy(np.ascontiguousarray(a.T)).cuda() for a in As]   # column-major
+    ptrs = np.array([d.data_ptr() for d in dev], np.int64)
+    mm = np.full(2, m, np.int64)
+    nn = np.full(2, n, np.int64)
+    call("skb_geqrf_batched", 2, mm, nn, mm, ptrs, skel._stream())
+    torch.cuda.synchronize()
+    for a, d in zip(As, dev):
+        R = d.cpu().numpy().T[:n, :n]
+        assert np.allclose(np.tril(R, -1), 0.0)
+        Rref = sla.qr(a, mode="r")[0][:n]
+        assert np.allclose(np.abs(np.diag(R)), np.abs(np.diag(Rref)), rtol=1e-9, atol=1e-14 * np.abs(Rref).max())
+        assert np.allclose(np.abs(R), np.abs(Rref), rtol=1e-9, atol=1e-12 * np.abs(Rref).max())

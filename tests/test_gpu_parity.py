@@ -92,3 +92,17 @@ def test_cfg2_against_oracle():
     assert same >= len(ref.boxes) - 20
     if same == len(ref.boxes):
         assert err <= 10 * wl.tol
+
+
+@pytest.mark.parametrize("builder", [configs.cfg1, configs.mini_holes])
+def test_system_matvec_vs_oracle(builder):
+    """GPU direct-summation operator vs the oracle's exact_matvec (kernels.py:393-414)."""
+    from paper_2001_11619_b200 import system_matvec
+    wl = builder()
+    b = wl.boundary
+    dim = 2 * b.n_nodes + 3 * b.n_holes
+    X = np.random.default_rng(3).standard_normal((dim, 5))
+    Y = system_matvec(SystemSpec(), b, X)
+    for j in range(5):
+        ref = O.exact_matvec(b, X[:, j])
+        assert _rel(Y[:, j], ref) < 1e-12
