@@ -311,22 +311,32 @@ int getrf_batched(int64_t nbox, const SkbMat* a, const int64_t* ipiv, int32_t* i
   std::vector<LuPanel> pd;
   std::vector<TrsmDesc> td;
   std::vector<SkbGemm> gd;
-  // panel width: as wide as shared memory allows for the tallest panel (<= 64)
+  // panel width: a function of each matrix's own order only (so results do not
+  // depend on the batch composition): as wide as shared memory allows (<= 64)
   constexpr size_t kPanelSmem = 220 * 1024;
-  int64_t PB = LB;
-  while (PB > 8 && (size_t)max_n * PB * sizeof(double) > kPanelSmem) PB /= 2;
-  if (max_n > 0) {
+  auto pbw = [&](int64_t n) {
+    int64_t PB = LB;
+    while (PB > 8 && (size_t)n * PB * sizeof(double) > kPanelSmem) PB /= 2;
+    return PB;
+  };
+  int64_t rounds = 0;
+  for (int64_t b = 0; b < nbox; ++b)
+    if (a[b].rows > kSmallLU) rounds = std::max(rounds, (a[b].rows + pbw(a[b].rows) - 1) / pbw(a[b].rows));
+  if (rounds > 0) {
     SKB_RET(cudaFuncSetAttribute(k_getf2_panel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)kPanelSmem));
   }
-  for (int64_t j0 = 0; j0 < max_n; j0 += PB) {
+  for (int64_t rd_ = 0; rd_ < rounds; ++rd_) {
     pd.clear(); td.clear(); gd.clear();
-    int64_t max_rows = 0;
+    size_t smem = 0;
     for (int64_t b = 0; b < nbox; ++b) {
       const int64_t n = a[b].rows;
-      if (j0 >= n || n <= kSmallLU) continue;
+      if (n <= kSmallLU) continue;
+      const int64_t PB = pbw(n);
+      const int64_t j0 = rd_ * PB;
+      if (j0 >= n) continue;
       const int64_t jb = std::min<int64_t>(PB, n - j0), n2 = n - j0 - jb;
-      max_rows = std::max(max_rows, n - j0);
+      smem = std::max(smem, sizeof(double) * (size_t)(n - j0) * (size_t)PB);
       double* A = a[b].ptr;
       const int64_t ld = a[b].ld;
       pd.push_back(LuPanel{A, n, ld, j0, jb, reinterpret_cast<int32_t*>(ipiv[b]), info_out + b});
@@ -341,11 +351,11 @@ int getrf_batched(int64_t nbox, const SkbMat* a, const int64_t* ipiv, int32_t* i
         gd.push_back(g);
       }
     }
+    if (pd.empty()) continue;
     LuPanel* dp = nullptr;
     if ((rc = upload(pd.data(), (int64_t)pd.size(), s, &dp))) return rc;
     {
       ProfScope ps(F_GETRF, s);
-      const size_t smem = sizeof(double) * (size_t)max_rows * (size_t)PB;
       k_getf2_panel<512><<<(unsigned)pd.size(), 512, smem, s>>>(dp);
     }
     SKB_LAUNCH_CHECK();

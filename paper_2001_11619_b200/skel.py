@@ -329,16 +329,20 @@ class BoxBatch:
         return off, self.act[np.repeat(self.act_off[:-1], r) + pos]
 
     def take(self, sel, other, osel):
-        """Overwrite boxes ``sel`` with ``other``'s boxes ``osel`` (same DOF layout)."""
-        for s, o in zip(sel, osel):
-            a0, a1 = self.act_off[s], self.act_off[s + 1]
-            b0 = other.act_off[o]
-            self.perm[a0:a1] = other.perm[b0:b0 + (a1 - a0)]
-            self.k[s], self.gap[s], self.steps[s] = other.k[o], other.gap[o], other.steps[o]
-            self.ratio[s], self.info[s] = other.ratio[o], other.info[o]
-            for f in self.FIELDS:
-                self.ptr[f][s] = other.ptr[f][o]
-            self.ipiv[s] = other.ipiv[o]
+        """Overwrite boxes ``sel`` with ``other``'s boxes ``osel`` (same DOF layout), vectorised."""
+        sel = np.asarray(sel, np.int64)
+        osel = np.asarray(osel, np.int64)
+        if len(sel) == 0:
+            return
+        lens = self.nB[sel]
+        _, src = _seg_gather(np.arange(len(other.perm)), other.act_off[osel], lens)
+        _, dst = _seg_gather(np.arange(len(self.perm)), self.act_off[sel], lens)
+        self.perm[dst] = other.perm[src]
+        self.k[sel], self.gap[sel], self.steps[sel] = other.k[osel], other.gap[osel], other.steps[osel]
+        self.ratio[sel], self.info[sel] = other.ratio[osel], other.info[osel]
+        for f in self.FIELDS:
+            self.ptr[f][sel] = other.ptr[f][osel]
+        self.ipiv[sel] = other.ipiv[osel]
         have = {id(x) for x in self.slabs}
         self.slabs.extend(x for x in other.slabs if id(x) not in have)
 
@@ -349,6 +353,7 @@ class LevelFactors:
 
     def __init__(self, lev, tree, batch: BoxBatch, cols_off, cols):
         self.lev = lev
+        self.tree = tree
         self.batch = batch
         self.idx = batch.idx
         self.keys = [tree.key(i) for i in self.idx]
@@ -1131,7 +1136,7 @@ def _run_levels(ctx: _Ctx, reuse=None, dirty=None):
         if reuse is None:
             todo = idx
         else:
-            todo = np.array([i for i in idx if t.key(i) in dirty], np.int64)
+            todo = idx[np.fromiter((t.key(i) in dirty for i in idx), bool, len(idx))]
         bt_new = ctx.compress_level(todo, store) if len(todo) else None
         n_recomp += len(todo)
         bt = bt_new if reuse is None else _merge_level(ctx, idx, store, todo, bt_new, reuse)
@@ -1148,18 +1153,30 @@ def _merge_level(ctx, idx, store, todo, bt_new, old_levels):
     t = ctx.t
     act_off, act = store.acts(idx)
     bt = BoxBatch(idx, act_off, act)
-    pos_new = {int(i): j for j, i in enumerate(todo)}
-    for bi, i in enumerate(idx):
-        key = t.key(i)
-        if int(i) in pos_new:
-            bt.take([bi], bt_new, [pos_new[int(i)]])
-            continue
-        L, bj = old_levels[key]
+    is_new = np.isin(idx, todo)
+    if bt_new is not None and is_new.any():
+        pos = np.searchsorted(bt_new.idx, idx[is_new])
+        bt.take(np.flatnonzero(is_new), bt_new, pos)
+    clean = np.flatnonzero(~is_new)
+    if len(clean):
+        lev = int(t.lev[idx[0]])
+        L = old_levels[lev]
+        ot = L.tree
+        side = np.int64(1) << np.int64(lev)
+        oc = ot.ix[L.idx] * side + ot.iy[L.idx]
+        nc = t.ix[idx[clean]] * side + t.iy[idx[clean]]
+        pos = np.searchsorted(oc, nc)
+        if np.any(pos >= len(oc)) or np.any(oc[np.minimum(pos, len(oc) - 1)] != nc):
+            raise RuntimeError("clean box missing from the previous factorization")
         ob = L.batch
-        a0, a1 = ob.act_off[bj], ob.act_off[bj + 1]
-        if not np.array_equal(ob.act[a0:a1], act[act_off[bi]:act_off[bi + 1]]):
-            raise RuntimeError(f"clean box {key} changed its active set")
-        bt.take([bi], ob, [bj])
+        lens = bt.nB[clean]
+        if not np.array_equal(lens, ob.nB[pos]):
+            raise RuntimeError("clean box changed its active set")
+        _, a_new = _seg_gather(act, act_off[clean], lens)
+        _, a_old = _seg_gather(ob.act, ob.act_off[pos], lens)
+        if not np.array_equal(a_new, a_old):
+            raise RuntimeError("clean box changed its active set")
+        bt.take(clean, ob, pos)
     return bt
 
 
@@ -1199,10 +1216,7 @@ def update(fct: Factorization, b_new, report, workers: int = 1) -> Factorization
     dirty = dirty_set(fct.tree, t_new, b_new, report, fct.proxy_factor)
     if not np.array_equal(report.old_to_new, np.arange(len(report.old_to_new))):
         raise NotImplementedError("only DOF-preserving edits (hole moves) are supported")
-    old = {}
-    for L in fct.levels:
-        for bj, key in enumerate(L.keys):
-            old[key] = (L, bj)
+    old = {L.lev: L for L in fct.levels}
     ctx = _Ctx(fct.spec, b_new, t_new, fct.tol, fct.proxy_count, fct.proxy_factor)
     levels, store, n_recomp = _run_levels(ctx, reuse=old, dirty=dirty)
     rd, E_root, top, ipiv, UH, PsiV, UH_div, q, ratio = _finish_top(ctx, levels, store)

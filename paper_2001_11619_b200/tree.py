@@ -321,31 +321,57 @@ def refit_tree(t: Tree, positions_new) -> Tree:
 # update bookkeeping (reference skel.py:476-491, 517-534; tree.py:215-270)
 # ---------------------------------------------------------------------------
 def ownership_changed(t_new: Tree, t_old: Tree, old_to_new) -> set:
-    """Keys of new boxes whose owned node set differs from their twin (tree.py:251-270)."""
+    """Keys of new-tree boxes whose owned node set differs from their twin
+    (reference tree.py:251-270), compared level by level on node segments."""
+    old_to_new = np.asarray(old_to_new, np.int64)
     changed = set()
-    for i in range(len(t_new.lev)):
-        key = t_new.key(i)
-        if not t_old.has(key):
-            changed.add(key)
-            continue
-        j = t_old.index(key)
-        mapped = old_to_new[t_old.nodes_of(j)]
-        mine = t_new.nodes_of(i)
-        if len(mapped) != len(mine) or np.any(mapped < 0) or not np.array_equal(mapped, mine):
-            changed.add(key)
-    for j in range(len(t_old.lev)):
-        key = t_old.key(j)
-        if not t_new.has(key):
-            p = j
-            while p >= 0 and not t_new.has(t_old.key(p)):
-                p = int(t_old.parent[p])
-            if p >= 0:
-                changed.add(t_old.key(p))
+    for l in range(max(t_new.depth, t_old.depth) + 1):
+        in_new = t_new.level_indices(l) if l <= t_new.depth else np.zeros(0, np.int64)
+        in_old = t_old.level_indices(l) if l <= t_old.depth else np.zeros(0, np.int64)
+        side = np.int64(1) << np.int64(l)
+        cn = t_new.ix[in_new] * side + t_new.iy[in_new]
+        co = t_old.ix[in_old] * side + t_old.iy[in_old]
+        pos = np.searchsorted(co, cn)
+        pos_c = np.minimum(pos, max(len(co) - 1, 0))
+        twin = (len(co) > 0) & (co[pos_c] == cn) if len(co) else np.zeros(len(cn), bool)
+        for i in in_new[~twin]:
+            changed.add(t_new.key(i))
+        bn, bo = in_new[twin], in_old[pos_c[twin]]
+        if len(bn):
+            cnt_n, cnt_o = t_new.node_cnt[bn], t_old.node_cnt[bo]
+            same_cnt = cnt_n == cnt_o
+            bn2, bo2 = bn[same_cnt], bo[same_cnt]
+            for i in bn[~same_cnt]:
+                changed.add(t_new.key(i))
+            if len(bn2):
+                cnt = t_new.node_cnt[bn2]
+                off = np.zeros(len(bn2) + 1, np.int64)
+                np.cumsum(cnt, out=off[1:])
+                rel = np.arange(off[-1]) - np.repeat(off[:-1], cnt)
+                nn = t_new.level_nodes[l][np.repeat(t_new.node_start[bn2], cnt) + rel]
+                oo = old_to_new[t_old.level_nodes[l][np.repeat(t_old.node_start[bo2], cnt) + rel]]
+                diff = (nn != oo).astype(np.int64)
+                bad = np.add.reduceat(diff, off[:-1]) > 0 if off[-1] else np.zeros(len(bn2), bool)
+                bad &= cnt > 0
+                for i in bn2[bad]:
+                    changed.add(t_new.key(i))
+        # boxes that vanished: their nearest surviving ancestor changed
+        if len(in_old):
+            pos2 = np.searchsorted(cn, co) if len(cn) else np.zeros(len(co), np.int64)
+            pos2c = np.minimum(pos2, max(len(cn) - 1, 0))
+            gone = ~((len(cn) > 0) & (cn[pos2c] == co)) if len(cn) else np.ones(len(co), bool)
+            for j in in_old[gone]:
+                p = int(j)
+                while p >= 0 and not t_new.has(t_old.key(p)):
+                    p = int(t_old.parent[p])
+                if p >= 0:
+                    changed.add(t_old.key(p))
     return changed
 
 
 def mark_disc_hits(t: Tree, pts, proxy_factor, out: set):
-    """Boxes whose proxy disc contains a point (tree.py:215-236), vectorised."""
+    """Boxes whose proxy disc contains a point (tree.py:215-236): candidates from
+    the (2 reach + 1)^2 cell neighbourhood of each point, then the distance test."""
     pts = np.asarray(pts, float)
     for lev in range(t.depth + 1):
         idx = t.level_indices(lev)
@@ -353,11 +379,30 @@ def mark_disc_hits(t: Tree, pts, proxy_factor, out: set):
             continue
         hw = t.root_half_width / 2 ** lev
         rad = proxy_radius(hw, proxy_factor)
-        c = t.center[idx]
-        d2 = ((pts[None, :, :] - c[:, None, :]) ** 2).sum(axis=2)
-        hit = (d2 <= rad * rad).any(axis=1)
-        for i in idx[hit]:
-            out.add(t.key(i))
+        step = 2 * hw
+        origin = t.root_center - t.root_half_width
+        cells = np.floor((pts - origin[None, :]) / step).astype(np.int64)
+        reach = int(np.ceil(rad / step)) + 1
+        side = np.int64(1) << np.int64(lev)
+        codes = t.ix[idx] * side + t.iy[idx]
+        ucell = np.unique(cells[:, 0] * (side + 2 * reach + 2) + cells[:, 1])
+        cx = ucell // (side + 2 * reach + 2)
+        cy = ucell - cx * (side + 2 * reach + 2)
+        cand = []
+        for dx in range(-reach, reach + 1):
+            for dy in range(-reach, reach + 1):
+                nx, ny = cx + dx, cy + dy
+                ok = (nx >= 0) & (ny >= 0) & (nx < side) & (ny < side)
+                c = nx * side + ny
+                pos = np.searchsorted(codes, c)
+                pc = np.minimum(pos, len(codes) - 1)
+                hit = ok & (codes[pc] == c)
+                cand.append(idx[pc[hit]])
+        cand = np.unique(np.concatenate(cand)) if cand else np.zeros(0, np.int64)
+        for k in cand:
+            d2 = ((pts - t.center[k][None, :]) ** 2).sum(axis=1)
+            if (d2 <= rad * rad).any():
+                out.add(t.key(k))
 
 
 def dirty_closure(t: Tree, content: set) -> set:
