@@ -190,6 +190,10 @@ Prof& prof() {
   static Prof p;
   return p;
 }
+SideStreams& side() {
+  static SideStreams s;
+  return s;
+}
 }  // namespace skb
 
 extern "C" int skb_version(void) { return 1; }

@@ -319,6 +319,16 @@ class BoxBatch:
     def r(self):
         return self.nB - self.k
 
+    def resolve(self):
+        """Wait for the asynchronously copied X_RR pivot info of this batch."""
+        pend = getattr(self, "_pending", None)
+        if pend is not None:
+            info_h, ratio_h, ev = pend
+            ev.synchronize()
+            self.info[:] = info_h.numpy()
+            self.ratio[:] = ratio_h.numpy()
+            self._pending = None
+
     def skel_csr(self):
         off, pos = _seg_gather(self.perm.astype(np.int64), self.act_off[:-1], self.k)
         return off, self.act[np.repeat(self.act_off[:-1], self.k) + pos]
@@ -343,6 +353,9 @@ class BoxBatch:
         for f in self.FIELDS:
             self.ptr[f][sel] = other.ptr[f][osel]
         self.ipiv[sel] = other.ipiv[osel]
+        other.resolve()
+        self.resolve()
+        self.info[sel], self.ratio[sel] = other.info[osel], other.ratio[osel]
         have = {id(x) for x in self.slabs}
         self.slabs.extend(x for x in other.slabs if id(x) not in have)
 
@@ -595,25 +608,37 @@ class _Ctx:
         _gemm([dict(A=Xsr, B=Xrsdiv, C=Ess, D=bt.ptr["Xss"], m=k, n=k, k=r, lda=r, ldb=k,
                     ldc=nB, ldd=k, alpha=mone, beta=one)])
         _Prof.tick("c_getrs_xss")
-        bt.info[:] = _d2h(info_d)                 # sync point 2 (migration check)
-        bt.ratio[:] = _d2h(ratio_d)
-        bt._scratch = None
+        # X_RR pivot info for the migration rule: copied asynchronously, checked
+        # after the next level's QRCP sync (no extra host sync per level)
+        info_h = torch.empty(B, dtype=torch.int32, pin_memory=True)
+        ratio_h = torch.empty(B, dtype=torch.float64, pin_memory=True)
+        info_h.copy_(info_d, non_blocking=True)
+        ratio_h.copy_(ratio_d, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        IO["d2h"] += 12 * B
+        bt._pending = (info_h, ratio_h, ev)
         del stack, Ebuf, Xrs
         return bt
 
     def compress_level(self, idx, store) -> BoxBatch:
-        bt = self.compress(idx, store)
-        # R -> S migration while the X_RR pivot ratio is below the floor (skel.py:317-330)
+        return self.compress(idx, store)
+
+    def migrate(self, bt: "BoxBatch", store) -> bool:
+        """R -> S migration while the X_RR pivot ratio is below the floor
+        (reference skel.py:317-330).  Returns True when any box changed."""
+        changed = False
         while True:
+            bt.resolve()
             kk = bt.k
             bad = ((bt.info >= 0) | (bt.ratio < PIVOT_RATIO_FLOOR)) & (kk < bt.nB)
             if not bad.any():
-                break
+                return changed
             sel = np.flatnonzero(bad)
             knew = np.minimum(bt.nB[sel], kk[sel] + np.maximum(1, (bt.nB[sel] - kk[sel]) // 8))
             sub = self.compress(bt.idx[sel], store, kmin=knew)
             bt.take(sel, sub, np.arange(len(sel)))
-        return bt
+            changed = True
 
 
 # ---------------------------------------------------------------------------
@@ -1130,7 +1155,9 @@ def _run_levels(ctx: _Ctx, reuse=None, dirty=None):
     pairs = t.hole_pairs(np.asarray(ctx.b.offsets, np.int64)) if ctx.b.n_holes else None
     levels = []
     n_recomp = 0
-    for lev in range(t.depth, 0, -1):
+    prev = None          # (level, batch, fresh boxes) whose migration check is pending
+    lev = t.depth
+    while lev >= 1:
         idx = t.level_indices(lev)
         store.set_internal(t, idx)            # assign_internal_actives, skel.py:251-256
         if reuse is None:
@@ -1138,12 +1165,34 @@ def _run_levels(ctx: _Ctx, reuse=None, dirty=None):
         else:
             todo = idx[np.fromiter((t.key(i) in dirty for i in idx), bool, len(idx))]
         bt_new = ctx.compress_level(todo, store) if len(todo) else None
+        # the previous level's X_RR pivot ratios are available now (its kernels ran
+        # before this level's QRCP sync); a migration there invalidates this level
+        if prev is not None and prev[2] is not None and ctx.migrate(prev[2], store):
+            pl, pbt, pnew = prev
+            if pbt is not pnew:
+                pos = np.searchsorted(pbt.idx, pnew.idx)
+                pbt.take(pos, pnew, np.arange(len(pnew.idx)))
+            store.set_skel(pbt.idx, pbt.act_off, pbt.act, pbt.perm, pbt.k)
+            store.xss[pbt.idx] = pbt.ptr["Xss"]
+            levels[-1] = LevelFactors(pl, t, pbt, *_hole_columns(t, ctx.b, pbt.idx, pairs))
+            prev = (pl, pbt, None)
+            continue                          # redo this level on the corrected skeletons
         n_recomp += len(todo)
         bt = bt_new if reuse is None else _merge_level(ctx, idx, store, todo, bt_new, reuse)
         store.set_skel(bt.idx, bt.act_off, bt.act, bt.perm, bt.k)
         store.xss[bt.idx] = bt.ptr["Xss"]
         cols_off, cols = _hole_columns(t, ctx.b, bt.idx, pairs)
         levels.append(LevelFactors(lev, t, bt, cols_off, cols))
+        prev = (lev, bt, bt_new)
+        lev -= 1
+    if prev is not None and prev[2] is not None and ctx.migrate(prev[2], store):
+        pl, pbt, pnew = prev
+        if pbt is not pnew:
+            pos = np.searchsorted(pbt.idx, pnew.idx)
+            pbt.take(pos, pnew, np.arange(len(pnew.idx)))
+        store.set_skel(pbt.idx, pbt.act_off, pbt.act, pbt.perm, pbt.k)
+        store.xss[pbt.idx] = pbt.ptr["Xss"]
+        levels[-1] = LevelFactors(pl, t, pbt, *_hole_columns(t, ctx.b, pbt.idx, pairs))
     return levels, store, n_recomp
 
 

@@ -132,3 +132,32 @@ def test_cfg4_update_sequence_vs_oracle():
                 assert np.array_equal(xu, xr)
             assert _rel(xu, xr) < 1e-13
             assert _rel(xu, ocur.solve(rhs)) <= 10 * wl.tol
+
+
+def test_migration_path(monkeypatch):
+    """Exercise the R -> S migration rule (skel.py:317-330) with a raised
+    pivot-ratio floor.  The floor decision itself compares X_RR pivot ratios,
+    which differ by a few percent between LU implementations near the floor, so
+    the test checks the mechanism: migrated boxes get larger ranks (the next
+    pivots of the same QRCP), every box with equal rank on both sides has the
+    same skeleton as the oracle, and the solution stays within 10 eps."""
+    from paper_2001_11619_b200 import skel as S
+    wl = configs.mini_holes()
+    f0 = _factor(wl)
+    floor = 0.0172
+    monkeypatch.setattr(S, "PIVOT_RATIO_FLOOR", floor)
+    monkeypatch.setattr(O, "PIVOT_FLOOR", floor)
+    ref = O.factor_full(wl.boundary, wl.leaf_cap, wl.tol, wl.proxy_count, wl.proxy_factor)
+    f = _factor(wl)
+    grew = [k for k in ref.boxes if len(f.factors[k].S_loc) > len(f0.factors[k].S_loc)]
+    assert grew, "no migration on the GPU"
+    for k in grew:
+        k0 = len(f0.factors[k].S_loc)
+        assert np.array_equal(f.factors[k].S_loc[:k0], f0.factors[k].S_loc)   # same pivot sequence
+    same_k = [k for k in ref.boxes if len(f.factors[k].S_loc) == len(ref.boxes[k].S)
+              and np.array_equal(f.factors[k].b_dofs, ref.boxes[k].dofs)]
+    assert len(same_k) >= len(ref.boxes) - 4
+    for k in same_k:
+        assert np.array_equal(f.factors[k].S_loc, ref.boxes[k].S), k
+    rhs = wl.extra["rhs"]
+    assert _rel(f.solve(rhs), ref.solve(rhs)) <= 10 * wl.tol
