@@ -63,6 +63,14 @@ int skb_version(void);
  * launches, launch counts, flops/bytes registered via skb_prof_add and by the
  * GEMM itself) and optionally resets.  Off by default (zero overhead).      */
 int skb_prof_enable(int32_t on);
+
+/* CUDA-graph capture sessions: between begin and end, descriptor uploads are
+ * staged through a pinned arena (allocated by begin, before the capture starts)
+ * kept alive until skb_capture_release(id)
+ * (id returned by skb_capture_end), so a captured graph can be replayed.     */
+int skb_capture_begin(int64_t arena_bytes);
+int skb_capture_end(void);
+int skb_capture_release(int32_t session);
 int skb_prof_add(int32_t family, double flops, double bytes);
 int skb_prof_read(double* ms_out, int64_t* count_out, double* flops_out, double* bytes_out,
                   int32_t reset);

@@ -30,6 +30,9 @@ _f64 = ctypes.c_double
 SIGNATURES = {
     "skb_version": [],
     "skb_prof_enable": [_i32],
+    "skb_capture_begin": [_i64],
+    "skb_capture_end": [],
+    "skb_capture_release": [_i32],
     "skb_prof_add": [_i32, _f64, _f64],
     "skb_prof_read": [_vp, _vp, _vp, _vp, _i32],
     "skb_gemm_grouped": [_vp, _i64, _vp],
@@ -92,6 +95,8 @@ def call(name: str, *args):
             conv.append(a)
     rc = getattr(lib, name)(*conv)
     del conv
+    if name == "skb_capture_end":
+        return rc
     if rc != 0:
         raise SkbError(f"{name} returned {rc}")
     return rc

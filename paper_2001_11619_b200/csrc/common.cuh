@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <string.h>
 
 #include <utility>
 #include <vector>
@@ -36,13 +37,34 @@ __device__ __forceinline__ void dmma8x8x4(double& d0, double& d1, double a, doub
       : "d"(a), "d"(b));
 }
 
+// CUDA-graph capture support: while a capture session is open, descriptor
+// uploads are staged through pinned host blocks that live as long as the
+// session (the captured memcpy nodes read them at every replay).
+struct CaptureSession {
+  bool on = false;
+  char* arena = nullptr;       // pinned, allocated before the capture starts
+  size_t size = 0, used = 0;
+  std::vector<void*> pinned;   // arenas owned by this session
+};
+CaptureSession& capture();
+
 // Copy host descriptors to a stream-ordered device buffer (freed async by caller).
 template <typename T>
 inline int upload(const T* host, int64_t n, cudaStream_t s, T** dev) {
   *dev = nullptr;
   if (n <= 0) return 0;
   SKB_RET(cudaMallocAsync((void**)dev, sizeof(T) * n, s));
-  SKB_RET(cudaMemcpyAsync(*dev, host, sizeof(T) * n, cudaMemcpyHostToDevice, s));
+  if (capture().on) {
+    CaptureSession& C = capture();
+    const size_t off = (C.used + 255) & ~(size_t)255;
+    if (off + sizeof(T) * n > C.size) return 5;         // arena exhausted
+    void* h = C.arena + off;
+    C.used = off + sizeof(T) * n;
+    memcpy(h, host, sizeof(T) * n);
+    SKB_RET(cudaMemcpyAsync(*dev, h, sizeof(T) * n, cudaMemcpyHostToDevice, s));
+  } else {
+    SKB_RET(cudaMemcpyAsync(*dev, host, sizeof(T) * n, cudaMemcpyHostToDevice, s));
+  }
   return 0;
 }
 

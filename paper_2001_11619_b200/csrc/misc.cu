@@ -194,9 +194,42 @@ SideStreams& side() {
   static SideStreams s;
   return s;
 }
+CaptureSession& capture() {
+  static CaptureSession c;
+  return c;
+}
+static std::vector<std::vector<void*>> g_sessions;
 }  // namespace skb
 
 extern "C" int skb_version(void) { return 1; }
+
+extern "C" int skb_capture_begin(int64_t arena_bytes) {
+  auto& C = skb::capture();
+  C.pinned.clear();
+  C.size = (size_t)(arena_bytes > 0 ? arena_bytes : (16 << 20));
+  C.used = 0;
+  void* h = nullptr;
+  cudaError_t e = cudaHostAlloc(&h, C.size, cudaHostAllocDefault);
+  if (e != cudaSuccess) return -(int)e;
+  C.arena = (char*)h;
+  C.pinned.push_back(h);
+  C.on = true;
+  return 0;
+}
+
+extern "C" int skb_capture_end(void) {
+  skb::capture().on = false;
+  skb::g_sessions.push_back(skb::capture().pinned);
+  skb::capture().pinned.clear();
+  return (int)skb::g_sessions.size();          // session id (1-based)
+}
+
+extern "C" int skb_capture_release(int32_t session) {
+  if (session < 1 || session > (int)skb::g_sessions.size()) return 1;
+  for (void* h : skb::g_sessions[session - 1]) cudaFreeHost(h);
+  skb::g_sessions[session - 1].clear();
+  return 0;
+}
 
 extern "C" int skb_prof_enable(int32_t on) {
   skb::prof().on = on != 0;
