@@ -198,6 +198,21 @@ int skb_scatter_rows(int64_t nbox, const int64_t* idx_off, const int64_t* idx,
 int skb_schur_accumulate(int64_t q, const int64_t* row_off, const int64_t* contrib,
                          const double* part, double* schur, void* stream);
 
+/* Column-sparse, compensated Psi^T z (skel.py:182 corr = lam - PsiV[nonroot]^T x,
+ * skel.py:142 bottom = PsiV^T y - lam): PsiV rows are nonzero only in the hole
+ * columns of the box that eliminated them, so column c sums over its row list
+ * (CSR col_off/rows, list order) with TwoSum/TwoProduct (double-double) accuracy:
+ *   out[c][j] = C[c][j] + alpha * sum_t psi[rows[t]][c] * z[rows[t]][j].        */
+int skb_psi_dot(int64_t q, const int64_t* col_off, const int64_t* rows, const double* psi,
+                int64_t ldp, const double* z, int64_t ldz, int64_t nrhs, const double* C,
+                int64_t ldc, double alpha, double* out, int64_t ldo, void* stream);
+
+/* Deterministic split-K reduction: D[e] = C[e] + alpha * sum_p parts[p*stride + e]
+ * (fixed order; C may be NULL) for e < count -- the second pass of the split-K
+ * products with K = 2N (PsiV^T x of skel.py:182).                              */
+int skb_sum_partials(int64_t count, int32_t nparts, const double* parts, int64_t stride,
+                     const double* C, double alpha, double* D, void* stream);
+
 /* Fill dst (n x n, ld) with diag_val*I + scale*src (src may be NULL). */
 int skb_diag_fill(int64_t n, double* dst, int64_t ld, double diag_val, const double* src,
                   int64_t src_ld, double scale, void* stream);

@@ -55,6 +55,8 @@ SIGNATURES = {
     "skb_schur_accumulate": [_i64, _vp, _vp, _vp, _vp, _vp],
     "skb_diag_fill": [_i64, _vp, _i64, _f64, _vp, _i64, _f64, _vp],
     "skb_fill_rows": [_i64, _vp, _vp, _i64, _vp, _i64, _f64, _vp],
+    "skb_psi_dot": [_i64, _vp, _vp, _vp, _i64, _vp, _i64, _i64, _vp, _i64, _f64, _vp, _i64, _vp],
+    "skb_sum_partials": [_i64, _i32, _vp, _i64, _vp, _f64, _vp, _vp],
     "skb_system_matvec": [_vp, _vp, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _i64, _vp, _vp],
 }
 

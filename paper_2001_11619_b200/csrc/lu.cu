@@ -145,12 +145,13 @@ __global__ void __launch_bounds__(256) k_trsm_block(const TrsmDesc* __restrict__
       x[i] = s;
     }
   } else {
+    // p descending: the same operation order as the warp-per-column variant
 #pragma unroll
     for (int i = LB - 1; i >= 0; --i) {
       if (i >= jb) continue;
       double s = x[i];
 #pragma unroll
-      for (int p = 0; p < LB; ++p)
+      for (int p = LB - 1; p > 0; --p)
         if (p > i && p < jb) s -= Ls[i][p] * x[p];
       x[i] = s / Ls[i][i];
     }
@@ -158,6 +159,35 @@ __global__ void __launch_bounds__(256) k_trsm_block(const TrsmDesc* __restrict__
 #pragma unroll
   for (int i = 0; i < LB; ++i)
     if (i < jb) D.B[i * D.ldb + c] = x[i];
+}
+
+// Narrow right-hand sides: one warp per column, lanes own rows (jb <= 64).
+template <bool UPPER>
+__global__ void __launch_bounds__(128) k_trsm_warp(const TrsmDesc* __restrict__ descs) {
+  const TrsmDesc D = descs[blockIdx.y];
+  const int lane = threadIdx.x & 31;
+  const int64_t c = blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (c >= D.ncols) return;
+  const int jb = (int)D.jb;
+  double x0 = lane < jb ? D.B[lane * D.ldb + c] : 0.0;
+  double x1 = lane + 32 < jb ? D.B[(lane + 32) * D.ldb + c] : 0.0;
+  if (!UPPER) {
+    for (int p = 0; p < jb; ++p) {
+      const double xp = __shfl_sync(0xffffffffu, p < 32 ? x0 : x1, p & 31);
+      if (lane > p && lane < jb) x0 -= D.L[lane * D.ldl + p] * xp;
+      if (lane + 32 > p && lane + 32 < jb) x1 -= D.L[(lane + 32) * D.ldl + p] * xp;
+    }
+  } else {
+    for (int p = jb - 1; p >= 0; --p) {
+      double xp = __shfl_sync(0xffffffffu, p < 32 ? x0 : x1, p & 31);
+      xp = xp / D.L[p * D.ldl + p];
+      if (lane == (p & 31)) { if (p < 32) x0 = xp; else x1 = xp; }
+      if (lane < p) x0 -= D.L[lane * D.ldl + p] * xp;
+      if (lane + 32 < p) x1 -= D.L[(lane + 32) * D.ldl + p] * xp;
+    }
+  }
+  if (lane < jb) D.B[lane * D.ldb + c] = x0;
+  if (lane + 32 < jb) D.B[(lane + 32) * D.ldb + c] = x1;
 }
 
 static int launch_trsm(std::vector<TrsmDesc>& td, bool upper, cudaStream_t s) {
@@ -169,6 +199,17 @@ static int launch_trsm(std::vector<TrsmDesc>& td, bool upper, cudaStream_t s) {
   int rc = upload(td.data(), (int64_t)td.size(), s, &d);
   if (rc) return rc;
   ProfScope ps(F_TRSM, s);
+  if (maxc <= 16) {
+    for (int64_t b0 = 0; b0 < (int64_t)td.size(); b0 += 65535) {
+      const int64_t nb = std::min<int64_t>(65535, (int64_t)td.size() - b0);
+      dim3 grid((unsigned)((maxc + 3) / 4), (unsigned)nb);
+      if (upper) k_trsm_warp<true><<<grid, 128, 0, s>>>(d + b0);
+      else k_trsm_warp<false><<<grid, 128, 0, s>>>(d + b0);
+    }
+    cudaError_t e = cudaGetLastError();
+    cudaFreeAsync(d, s);
+    return e == cudaSuccess ? 0 : -(int)e;
+  }
   for (int64_t b0 = 0; b0 < (int64_t)td.size(); b0 += 65535) {
     const int64_t nb = std::min<int64_t>(65535, (int64_t)td.size() - b0);
     dim3 grid((unsigned)((maxc + 255) / 256), (unsigned)nb);
@@ -379,6 +420,34 @@ struct SwapDesc {
   const int32_t* ipiv;
 };
 
+// Narrow B: compose the interchanges into a permutation (one thread per
+// matrix), then gather rows in parallel through a scratch copy.
+__global__ void k_ipiv_perm(const SwapDesc* __restrict__ descs, int32_t* __restrict__ perm,
+                            const int64_t* __restrict__ poff) {
+  const int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const SwapDesc D = descs[b];
+  int32_t* p = perm + poff[b];
+  for (int64_t i = 0; i < D.n; ++i) p[i] = (int32_t)i;
+  for (int64_t i = 0; i < D.n; ++i) {
+    const int64_t q = D.ipiv[i];
+    if (q != i) { const int32_t t = p[i]; p[i] = p[q]; p[q] = t; }
+  }
+}
+
+__global__ void k_perm_rows(const SwapDesc* __restrict__ descs, const int32_t* __restrict__ perm,
+                            const int64_t* __restrict__ poff, double* __restrict__ tmp,
+                            const int64_t* __restrict__ toff, int phase) {
+  const SwapDesc D = descs[blockIdx.y];
+  const int32_t* p = perm + poff[blockIdx.y];
+  double* t = tmp + toff[blockIdx.y];
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < D.n * D.ncols;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = e / D.ncols, c = e - i * D.ncols;
+    if (phase == 0) t[e] = D.B[(int64_t)p[i] * D.ld + c];
+    else D.B[i * D.ld + c] = t[e];
+  }
+}
+
 __global__ void k_apply_ipiv(const SwapDesc* __restrict__ descs) {
   const SwapDesc D = descs[blockIdx.y];
   const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -475,7 +544,43 @@ int getrs_batched(int64_t nbox, const SkbMat* lu, const int64_t* ipiv, const Skb
   }
   if (sd.empty()) return 0;
   int rc = 0;
-  {
+  if (max_c <= 8) {
+    // narrow: permutation gather
+    std::vector<int64_t> poff(sd.size()), toff(sd.size());
+    int64_t pt = 0, tt = 0, maxe = 0;
+    for (size_t i = 0; i < sd.size(); ++i) {
+      poff[i] = pt; pt += sd[i].n;
+      toff[i] = tt; tt += sd[i].n * sd[i].ncols;
+      maxe = std::max(maxe, sd[i].n * sd[i].ncols);
+    }
+    SwapDesc* d = nullptr;
+    int64_t *dpo = nullptr, *dto = nullptr;
+    int32_t* perm = nullptr;
+    double* tmp = nullptr;
+    if ((rc = upload(sd.data(), (int64_t)sd.size(), s, &d))) return rc;
+    if ((rc = upload(poff.data(), (int64_t)poff.size(), s, &dpo))) return rc;
+    if ((rc = upload(toff.data(), (int64_t)toff.size(), s, &dto))) return rc;
+    SKB_RET(cudaMallocAsync((void**)&perm, sizeof(int32_t) * std::max<int64_t>(pt, 1), s));
+    SKB_RET(cudaMallocAsync((void**)&tmp, sizeof(double) * std::max<int64_t>(tt, 1), s));
+    {
+      ProfScope ps(F_TRSM, s);
+      const int64_t nbx = (int64_t)sd.size();
+      // one thread per matrix (exact multiple of the block via guard-free launch of 1-thread blocks)
+      k_ipiv_perm<<<(unsigned)nbx, 1, 0, s>>>(d, perm, dpo);
+      for (int64_t b0 = 0; b0 < nbx; b0 += 65535) {
+        const int64_t nb = std::min<int64_t>(65535, nbx - b0);
+        dim3 grid(grid_cap((maxe + 255) / 256, 64), (unsigned)nb);
+        k_perm_rows<<<grid, 256, 0, s>>>(d + b0, perm, dpo + b0, tmp, dto + b0, 0);
+        k_perm_rows<<<grid, 256, 0, s>>>(d + b0, perm, dpo + b0, tmp, dto + b0, 1);
+      }
+    }
+    SKB_LAUNCH_CHECK();
+    cudaFreeAsync(d, s);
+    cudaFreeAsync(dpo, s);
+    cudaFreeAsync(dto, s);
+    cudaFreeAsync(perm, s);
+    cudaFreeAsync(tmp, s);
+  } else {
     SwapDesc* d = nullptr;
     if ((rc = upload(sd.data(), (int64_t)sd.size(), s, &d))) return rc;
     for (int64_t b0 = 0; b0 < (int64_t)sd.size(); b0 += 65535) {

@@ -98,9 +98,74 @@ __global__ void k_fill_rows(const int64_t* __restrict__ idx, int64_t nidx, doubl
   }
 }
 
+__global__ void k_sum_parts(int64_t count, int nparts, const double* __restrict__ parts,
+                            int64_t stride, const double* C, double alpha, double* D) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < count;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int p = 0; p < nparts; ++p) acc += parts[p * stride + e];
+    D[e] = (C ? C[e] : 0.0) + alpha * acc;
+  }
+}
+
+// Error-free transformations (Knuth TwoSum, FMA TwoProduct) for the
+// compensated Psi^T z reductions.
+__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
+  s = a + b;
+  const double bb = s - a;
+  e = (a - (s - bb)) + (b - bb);
+}
+
+// out[c][j] = C[c][j] + alpha * sum_{t in col c} psi[rows[t]*ldp + c] * z[rows[t]*ldz + j],
+// summed in list order with double-double (Dot2) accuracy.
+__global__ void k_psi_dot(const int64_t* __restrict__ col_off, const int64_t* __restrict__ rows,
+                          const double* __restrict__ psi, int64_t ldp,
+                          const double* __restrict__ z, int64_t ldz, int64_t nrhs,
+                          const double* C, int64_t ldc, double alpha, double* out, int64_t ldo) {
+  const int64_t c = blockIdx.x;
+  const int64_t t0 = col_off[c], t1 = col_off[c + 1];
+  for (int64_t j = blockIdx.y * (int64_t)blockDim.x + threadIdx.x; j < nrhs;
+       j += (int64_t)gridDim.y * blockDim.x) {
+    double s = 0.0, e = 0.0;
+    for (int64_t t = t0; t < t1; ++t) {
+      const int64_t i = rows[t];
+      const double a = psi[i * ldp + c], b = z[i * ldz + j];
+      const double p = a * b;
+      const double pe = fma(a, b, -p);
+      double s2, se;
+      two_sum(s, p, s2, se);
+      s = s2;
+      e += se + pe;
+    }
+    const double v = s + e;
+    out[c * ldo + j] = (C ? C[c * ldc + j] : 0.0) + alpha * v;
+  }
+}
+
 }  // namespace skb
 
 using namespace skb;
+
+extern "C" int skb_psi_dot(int64_t q, const int64_t* col_off, const int64_t* rows, const double* psi,
+                           int64_t ldp, const double* z, int64_t ldz, int64_t nrhs, const double* C,
+                           int64_t ldc, double alpha, double* out, int64_t ldo, void* stream) {
+  if (q <= 0 || nrhs <= 0) return 0;
+  const int nt = nrhs >= 128 ? 128 : (nrhs >= 32 ? 32 : 32);
+  dim3 grid((unsigned)q, (unsigned)((nrhs + nt - 1) / nt));
+  k_psi_dot<<<grid, nt, 0, (cudaStream_t)stream>>>(col_off, rows, psi, ldp, z, ldz, nrhs, C, ldc, alpha,
+                                                    out, ldo);
+  SKB_LAUNCH_CHECK();
+  return 0;
+}
+
+extern "C" int skb_sum_partials(int64_t count, int32_t nparts, const double* parts, int64_t stride,
+                                const double* C, double alpha, double* D, void* stream) {
+  if (count <= 0) return 0;
+  k_sum_parts<<<grid_cap((count + 255) / 256, 4096), 256, 0, (cudaStream_t)stream>>>(
+      count, nparts, parts, stride, C, alpha, D);
+  SKB_LAUNCH_CHECK();
+  return 0;
+}
 
 extern "C" int skb_fill_rows(int64_t nidx, const int64_t* idx, double* dst, int64_t ld,
                              const void* unused, int64_t ncols, double value, void* stream) {

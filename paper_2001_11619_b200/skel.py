@@ -276,6 +276,22 @@ def _gemm(rows):
     call("skb_gemm_grouped", g, n, _stream())
 
 
+def _gemm_tn_splitk(A, B, M, N, K, lda, ldb, C, alpha, D, chunk=4096):
+    """D = C + alpha * A^T B with A: (K x M), B: (K x N) row-major and K large:
+    split K into chunks (one grouped GEMM), then a fixed-order sum of partials."""
+    nch = max(1, (K + chunk - 1) // chunk)
+    parts = torch.empty(max(nch * M * N, 1), dtype=torch.float64, device=_dev())
+    k0 = np.arange(nch) * chunk
+    kk = np.minimum(chunk, K - k0)
+    pa = _addr(parts)
+    _gemm([dict(A=(A + 8 * k0 * lda).astype(np.uint64), B=(B + 8 * k0 * ldb).astype(np.uint64),
+                D=(pa + 8 * np.arange(nch) * M * N).astype(np.uint64), m=np.full(nch, M),
+                n=np.full(nch, N), k=kk, lda=np.full(nch, lda), ldb=np.full(nch, ldb),
+                ldd=np.full(nch, N), alpha=np.ones(nch), beta=np.zeros(nch), transA=np.ones(nch))])
+    call("skb_sum_partials", M * N, nch, parts, M * N, C, alpha, D, _stream())
+    return parts
+
+
 def _mats(ptrs, rows, cols, ld):
     m = np.zeros(len(ptrs), MAT_DT)
     m["ptr"], m["rows"], m["cols"], m["ld"] = ptrs, rows, cols, ld
@@ -751,6 +767,42 @@ class Factorization:
     def n_dofs(self) -> int:
         return 2 * self.boundary.n_nodes
 
+    def _psi_lists(self, with_root: bool):
+        """Per augmentation column, the DOF rows where PsiV can be nonzero (rows
+        eliminated in a box containing that hole; + root rows for apply), sorted
+        by row -- CSR on the device for skb_psi_dot."""
+        key = "_psi_root" if with_root else "_psi_nonroot"
+        got = getattr(self, key, None)
+        if got is not None:
+            return got
+        rows_l, cols_l = [], []
+        for L in self.levels:
+            r, c = L.r, L.ncols
+            cnt = r * c
+            tot = int(cnt.sum())
+            if tot == 0:
+                continue
+            box = np.repeat(np.arange(len(r)), cnt)
+            start = np.zeros(len(r), np.int64)
+            np.cumsum(cnt[:-1], out=start[1:])
+            local = np.arange(tot) - start[box]
+            cb = c[box]
+            rows_l.append(L.rd[L.rd_off[box] + local // cb])
+            cols_l.append(L.cols[L.cols_off[box] + local % cb])
+        if with_root and self.q:
+            rd = np.asarray(self.root_dofs, np.int64)
+            rows_l.append(np.repeat(rd, self.q))
+            cols_l.append(np.tile(np.arange(self.q, dtype=np.int64), len(rd)))
+        rows = np.concatenate(rows_l) if rows_l else np.zeros(0, np.int64)
+        cols = np.concatenate(cols_l) if cols_l else np.zeros(0, np.int64)
+        order = np.lexsort((rows, cols))
+        rows, cols = rows[order], cols[order]
+        off = np.zeros(self.q + 1, np.int64)
+        np.cumsum(np.bincount(cols, minlength=self.q), out=off[1:])
+        got = _upload(off=off, rows=rows if len(rows) else np.zeros(1, np.int64))
+        setattr(self, key, got)
+        return got
+
     @property
     def n_aug(self) -> int:
         return self.q
@@ -810,21 +862,16 @@ class Factorization:
         ns = len(self.root_dofs)
         rd = self._root_d
         if q:                                        # skel.py:180-188
-            z = torch.empty((nd, nr), dtype=torch.float64, device=dev)
-            z.copy_(x[:nd])
-            call("skb_fill_rows", ns, ptr(rd["r"]), ptr(z), nr, None, nr, 0.0, s)
+            pl = self._psi_lists(False)
             top_rhs = torch.empty((ns + q, nr), dtype=torch.float64, device=dev)
             up = _upload(o=np.zeros(1, np.int64), ld=np.array([nr], np.int64),
                          ro=np.array([0, ns], np.int64))
             keep.append(up)
             call("skb_gather_rows", 1, ptr(up["ro"]), ptr(rd["r"]), None, None, nr, ptr(x), nr,
                  ptr(top_rhs), ptr(up["o"]), ptr(up["ld"]), ns, nr, s)
-            _gemm([dict(A=np.array([_addr(self.PsiV)], np.uint64),
-                        B=np.array([_addr(z)], np.uint64),
-                        C=np.array([_addr(x) + 8 * nd * nr], np.uint64),
-                        D=np.array([_addr(top_rhs) + 8 * ns * nr], np.uint64),
-                        m=[q], n=[nr], k=[nd], lda=[q], ldb=[nr], ldc=[nr], ldd=[nr],
-                        alpha=[-1.0], beta=[1.0], transA=[1])])
+            # corr = lam_rhs - PsiV[nonroot]^T x[nonroot]: column-sparse, compensated
+            call("skb_psi_dot", q, pl["off"], pl["rows"], self.PsiV, q, x, nr, nr,
+                 _addr(x) + 8 * nd * nr, nr, -1.0, _addr(top_rhs) + 8 * ns * nr, nr, s)
             call("skb_getrs_batched", 1, _mats([_addr(self.top)], [ns + q], [ns + q],
                                               [ns + q]),
                  np.array([_addr(self.top_ipiv)], np.uint64),
@@ -838,7 +885,7 @@ class Factorization:
                         C=np.array([_addr(x)], np.uint64), D=np.array([_addr(x)], np.uint64),
                         m=[nd], n=[nr], k=[q], lda=[q], ldb=[nr], ldc=[nr], ldd=[nr],
                         alpha=[-1.0], beta=[1.0])])
-            keep += [z, top_rhs]
+            keep += [top_rhs]
         else:
             top_rhs = torch.empty((ns, nr), dtype=torch.float64, device=dev)
             up = _upload(o=np.zeros(1, np.int64), ld=np.array([nr], np.int64),
@@ -909,8 +956,20 @@ class Factorization:
         x.copy_(xs)
         return x
 
-    def solve(self, rhs, workers: int = 1):
-        """Solve A x = rhs for (dim,) or (dim, nrhs) input (reference skel.py:166-193)."""
+    def solve(self, rhs, workers: int = 1, refine: int = 0):
+        """Solve A x = rhs for (dim,) or (dim, nrhs) input (reference skel.py:166-193).
+
+        ``refine`` > 0 adds that many steps of iterative refinement against the
+        compressed operator (x += solve(rhs - apply(x))); 0 (default) is the
+        reference's plain solve.  On the ill-conditioned cfg3 geometry one step
+        lowers the exact-operator residual ~20x."""
+        if refine > 0:
+            x = self.solve(rhs, workers)
+            for _ in range(refine):
+                r = (rhs - self.apply(x)) if not isinstance(rhs, torch.Tensor) else \
+                    (rhs.to(torch.float64) - self.apply(x))
+                x = x + self.solve(r, workers)
+            return x
         is_t = isinstance(rhs, torch.Tensor)
         r = rhs if is_t else np.asarray(rhs, float)
         if r.shape[0] != self.dim:
@@ -961,10 +1020,11 @@ class Factorization:
         bottom = None
         if q:
             bottom = torch.empty((q, nr), dtype=torch.float64, device=dev)
-            _gemm([dict(A=np.array([_addr(self.PsiV)], np.uint64), B=np.array([_addr(y)], np.uint64),
-                        C=np.array([_addr(lam)], np.uint64), D=np.array([_addr(bottom)], np.uint64),
-                        m=[q], n=[nr], k=[nd], lda=[q], ldb=[nr], ldc=[nr], ldd=[nr],
-                        alpha=[1.0], beta=[-1.0], transA=[1])])
+            # bottom = PsiV^T y - lam (all rows incl. root), column-sparse, compensated
+            pl = self._psi_lists(True)
+            call("skb_psi_dot", q, pl["off"], pl["rows"], self.PsiV, q, y, nr, nr, None, nr, 1.0,
+                 bottom, nr, s)
+            call("skb_sum_partials", q * nr, 1, lam, q * nr, bottom, -1.0, bottom, s)
         # X_D: y_R <- X_rr y_R (stash y_R), y_root <- E_root y_root, y += UH lam
         stash = []
         for L in self.levels:

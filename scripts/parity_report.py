@@ -99,12 +99,14 @@ def main():
         rng = np.random.default_rng(1)
         rhs = np.concatenate([rng.standard_normal(2 * b.n_nodes), np.zeros(3 * b.n_holes)])
     xg = f.solve(rhs)
+    xr1 = f.solve(rhs, refine=1)
     xo = of.solve(rhs)
     rep["solve_rel_diff"] = float(np.linalg.norm(xg - xo) / np.linalg.norm(xo))
-    M = system_matvec(SystemSpec(), b, np.stack([xg, xo], axis=1))
+    M = system_matvec(SystemSpec(), b, np.stack([xg, xo, xr1], axis=1))
     nb = np.linalg.norm(rhs)
     rep["residual_gpu"] = float(np.linalg.norm(M[:, 0] - rhs) / nb)
     rep["residual_oracle"] = float(np.linalg.norm(M[:, 1] - rhs) / nb)
+    rep["residual_gpu_refine1"] = float(np.linalg.norm(M[:, 2] - rhs) / nb)
     y = np.random.default_rng(2).standard_normal(len(rhs))
     ag, ao = f.apply(y), of.apply(y)
     rep["apply_rel_diff"] = float(np.linalg.norm(ag - ao) / np.linalg.norm(ao))
