@@ -48,6 +48,51 @@ struct CaptureSession {
 };
 CaptureSession& capture();
 
+// Pinned staging ring for descriptor uploads (asynchronous H2D copies).  The
+// ring is split into slots; a slot is reused only after the event recorded by
+// the last copy that read it has completed.
+struct PinnedRing {
+  static constexpr size_t kSize = 64u << 20, kSlot = 1u << 20, kSlots = kSize / kSlot;
+  char* base = nullptr;
+  size_t head = 0;
+  cudaEvent_t ev[kSlots];
+  bool used[kSlots] = {false};
+};
+PinnedRing& ring();
+
+inline int ring_stage(const void* host, size_t bytes, cudaStream_t s, void* dev) {
+  PinnedRing& R = ring();
+  if (!R.base) {
+    // keep stream-ordered allocations cached in the pool across synchronisations
+    int dev = 0;
+    cudaMemPool_t pool;
+    SKB_RET(cudaGetDevice(&dev));
+    SKB_RET(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t thr = ~0ull;
+    SKB_RET(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    SKB_RET(cudaHostAlloc((void**)&R.base, PinnedRing::kSize, cudaHostAllocDefault));
+    for (size_t i = 0; i < PinnedRing::kSlots; ++i)
+      SKB_RET(cudaEventCreateWithFlags(&R.ev[i], cudaEventDisableTiming));
+  }
+  if (bytes > PinnedRing::kSize / 2) {      // oversized: plain (pageable) copy
+    SKB_RET(cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, s));
+    return 0;
+  }
+  size_t off = (R.head + 255) & ~(size_t)255;
+  if (off + bytes > PinnedRing::kSize) off = 0;
+  const size_t s0 = off / PinnedRing::kSlot, s1 = (off + bytes - 1) / PinnedRing::kSlot;
+  for (size_t k = s0; k <= s1; ++k)
+    if (R.used[k]) SKB_RET(cudaEventSynchronize(R.ev[k]));
+  memcpy(R.base + off, host, bytes);
+  SKB_RET(cudaMemcpyAsync(dev, R.base + off, bytes, cudaMemcpyHostToDevice, s));
+  for (size_t k = s0; k <= s1; ++k) {
+    SKB_RET(cudaEventRecord(R.ev[k], s));
+    R.used[k] = true;
+  }
+  R.head = off + bytes;
+  return 0;
+}
+
 // Copy host descriptors to a stream-ordered device buffer (freed async by caller).
 template <typename T>
 inline int upload(const T* host, int64_t n, cudaStream_t s, T** dev) {
@@ -63,7 +108,8 @@ inline int upload(const T* host, int64_t n, cudaStream_t s, T** dev) {
     memcpy(h, host, sizeof(T) * n);
     SKB_RET(cudaMemcpyAsync(*dev, h, sizeof(T) * n, cudaMemcpyHostToDevice, s));
   } else {
-    SKB_RET(cudaMemcpyAsync(*dev, host, sizeof(T) * n, cudaMemcpyHostToDevice, s));
+    const int rc = ring_stage(host, sizeof(T) * n, s, *dev);
+    if (rc) return rc;
   }
   return 0;
 }

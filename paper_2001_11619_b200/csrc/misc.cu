@@ -263,6 +263,10 @@ CaptureSession& capture() {
   static CaptureSession c;
   return c;
 }
+PinnedRing& ring() {
+  static PinnedRing r;
+  return r;
+}
 static std::vector<std::vector<void*>> g_sessions;
 }  // namespace skb
 

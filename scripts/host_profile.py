@@ -22,4 +22,4 @@ torch.cuda.synchronize()
 pr.disable()
 print("factor_time", f.stats["factor_time"])
 st = pstats.Stats(pr)
-st.sort_stats("tottime").print_stats(25)
+st.sort_stats("tottime").print_stats(30)
