@@ -83,9 +83,25 @@ def load(path: str = LIB_PATH):
     return lib
 
 
+CALL_TIMES: dict | None = None     # set to {} to accumulate host time per entry point
+
+
 def call(name: str, *args):
     """Invoke an entry point; numpy arrays are passed by address and kept alive
     for the duration of the call, torch tensors by data_ptr()."""
+    if CALL_TIMES is not None:
+        import time as _t
+        t0 = _t.perf_counter()
+        try:
+            return _call(name, *args)
+        finally:
+            c = CALL_TIMES.setdefault(name, [0, 0.0])
+            c[0] += 1
+            c[1] += _t.perf_counter() - t0
+    return _call(name, *args)
+
+
+def _call(name: str, *args):
     lib = load()
     conv = []
     for a in args:

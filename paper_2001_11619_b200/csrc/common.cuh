@@ -55,8 +55,9 @@ struct PinnedRing {
   static constexpr size_t kSize = 64u << 20, kSlot = 1u << 20, kSlots = kSize / kSlot;
   char* base = nullptr;
   size_t head = 0;
+  uint64_t lap = 1;
   cudaEvent_t ev[kSlots];
-  bool used[kSlots] = {false};
+  uint64_t slot_lap[kSlots] = {0};   // lap of the last copy recorded on the slot's event
 };
 PinnedRing& ring();
 
@@ -79,15 +80,17 @@ inline int ring_stage(const void* host, size_t bytes, cudaStream_t s, void* dev)
     return 0;
   }
   size_t off = (R.head + 255) & ~(size_t)255;
-  if (off + bytes > PinnedRing::kSize) off = 0;
+  if (off + bytes > PinnedRing::kSize) { off = 0; ++R.lap; }
   const size_t s0 = off / PinnedRing::kSlot, s1 = (off + bytes - 1) / PinnedRing::kSlot;
+  // only data written in a previous lap can still be in flight in this region
   for (size_t k = s0; k <= s1; ++k)
-    if (R.used[k]) SKB_RET(cudaEventSynchronize(R.ev[k]));
+    if (R.slot_lap[k] != 0 && R.slot_lap[k] < R.lap) SKB_RET(cudaEventSynchronize(R.ev[k]));
   memcpy(R.base + off, host, bytes);
   SKB_RET(cudaMemcpyAsync(dev, R.base + off, bytes, cudaMemcpyHostToDevice, s));
+  // the slot's event tracks its latest copy; it is waited on only one lap later
   for (size_t k = s0; k <= s1; ++k) {
     SKB_RET(cudaEventRecord(R.ev[k], s));
-    R.used[k] = true;
+    R.slot_lap[k] = R.lap;
   }
   R.head = off + bytes;
   return 0;

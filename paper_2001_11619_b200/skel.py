@@ -86,6 +86,7 @@ class _Prof:
     enabled = bool(int(__import__("os").environ.get("SKB_PROFILE", "0")))
     acc: dict = {}
     _t = 0.0
+    _lt = 0.0
 
     @classmethod
     def start(cls):
@@ -1117,7 +1118,44 @@ def _hole_columns(t: Tree, b, idx, pairs=None):
     return o, cols.astype(np.int64)
 
 
-def _finish_top(ctx: _Ctx, levels, store):
+class _AugPipe:
+    """U sweep on H / V^T sweep on Psi (reference _finish_top, skel.py:379-396),
+    run per level on a side stream as soon as the level's factors are final, so
+    it overlaps the factorisation of the levels above."""
+
+    def __init__(self, ctx: _Ctx):
+        b = ctx.b
+        self.q = 3 * b.n_holes if ctx.spec.augmented(b) else 0
+        if not self.q:
+            return
+        dev = _dev()
+        nd, q = 2 * b.n_nodes, self.q
+        self.UH = torch.empty((nd, q), dtype=torch.float64, device=dev)
+        self.PsiV = torch.empty((nd, q), dtype=torch.float64, device=dev)
+        self.UH_div = torch.zeros((nd, q), dtype=torch.float64, device=dev)
+        self.schur = torch.zeros((q, q), dtype=torch.float64, device=dev)
+        self._hc = torch.from_numpy(np.ascontiguousarray(b.hole_centers, np.float64)).to(dev)
+        call("skb_assemble_aug", ptr(ctx.g.pos), ptr(ctx.g.w), b.n_nodes, ptr(self._hc), b.n_holes,
+             np.ascontiguousarray(b.offsets, np.int64), ptr(self.UH), ptr(self.PsiV), _stream())
+        self.stream = torch.cuda.Stream()
+
+    def submit(self, L: "LevelFactors"):
+        if not self.q:
+            return
+        ev = torch.cuda.Event()
+        ev.record()
+        self.stream.wait_event(ev)
+        with torch.cuda.stream(self.stream):
+            _aug_level(L, self.UH, self.PsiV, self.UH_div, self.schur, self.q)
+
+    def join(self):
+        if self.q:
+            ev = torch.cuda.Event()
+            ev.record(self.stream)
+            torch.cuda.current_stream().wait_event(ev)
+
+
+def _finish_top(ctx: _Ctx, levels, store, pipe: "_AugPipe"):
     """Root block, augmentation sweep and corner LU (reference skel.py:364-425)."""
     t, b = ctx.t, ctx.b
     dev = _dev()
@@ -1138,17 +1176,10 @@ def _finish_top(ctx: _Ctx, levels, store):
          ptr(up["eo"]), ptr(up["eld"]), ns, s)
     UH = PsiV = UH_div = None
     if q:
-        UH = torch.empty((nd, q), dtype=torch.float64, device=dev)
-        PsiV = torch.empty((nd, q), dtype=torch.float64, device=dev)
-        UH_div = torch.zeros((nd, q), dtype=torch.float64, device=dev)
-        hc = torch.from_numpy(np.ascontiguousarray(b.hole_centers, np.float64)).to(dev)
-        call("skb_assemble_aug", ptr(ctx.g.pos), ptr(ctx.g.w), b.n_nodes, ptr(hc), b.n_holes,
-             np.ascontiguousarray(b.offsets, np.int64), ptr(UH), ptr(PsiV), s)
-        schur = torch.zeros((q, q), dtype=torch.float64, device=dev)
         _Prof.start()
-        for L in levels:
-            _aug_level(L, UH, PsiV, UH_div, schur, q)
+        pipe.join()                                  # sweeps were issued level by level
         _Prof.tick("d_aug_sweep")
+        UH, PsiV, UH_div, schur = pipe.UH, pipe.PsiV, pipe.UH_div, pipe.schur
         n = ns + q
         top = torch.empty((n, n), dtype=torch.float64, device=dev)
         call("skb_copy2d_batched", 1, _mats([_addr(top)], [ns], [ns], [n]),
@@ -1265,10 +1296,15 @@ def _run_levels(ctx: _Ctx, reuse=None, dirty=None):
     store = ActStore(t)
     ctx.store = store
     pairs = t.hole_pairs(np.asarray(ctx.b.offsets, np.int64)) if ctx.b.n_holes else None
+    pipe = _AugPipe(ctx)
+    ctx.pipe = pipe
     levels = []
     n_recomp = 0
     prev = None          # (level, batch, fresh boxes) whose migration check is pending
     lev = t.depth
+    if _Prof.enabled:
+        torch.cuda.synchronize()
+        _Prof._lt = time.perf_counter()
     while lev >= 1:
         idx = t.level_indices(lev)
         store.set_internal(t, idx)            # assign_internal_actives, skel.py:251-256
@@ -1289,7 +1325,13 @@ def _run_levels(ctx: _Ctx, reuse=None, dirty=None):
             levels[-1] = LevelFactors(pl, t, pbt, *_hole_columns(t, ctx.b, pbt.idx, pairs))
             prev = (pl, pbt, None)
             continue                          # redo this level on the corrected skeletons
+        if prev is not None:
+            pipe.submit(levels[-1])           # previous level final: start its aug sweep
         n_recomp += len(todo)
+        if _Prof.enabled:
+            torch.cuda.synchronize()
+            _Prof.acc[f"level{lev}"] = time.perf_counter() - _Prof._lt
+            _Prof._lt = time.perf_counter()
         bt = bt_new if reuse is None else _merge_level(ctx, idx, store, todo, bt_new, reuse)
         store.set_skel(bt.idx, bt.act_off, bt.act, bt.perm, bt.k)
         store.xss[bt.idx] = bt.ptr["Xss"]
@@ -1305,6 +1347,8 @@ def _run_levels(ctx: _Ctx, reuse=None, dirty=None):
         store.set_skel(pbt.idx, pbt.act_off, pbt.act, pbt.perm, pbt.k)
         store.xss[pbt.idx] = pbt.ptr["Xss"]
         levels[-1] = LevelFactors(pl, t, pbt, *_hole_columns(t, ctx.b, pbt.idx, pairs))
+    if levels:
+        pipe.submit(levels[-1])
     return levels, store, n_recomp
 
 
@@ -1355,7 +1399,7 @@ def factor(spec, b, t: Tree, tol: float, workers: int = 1,
     t0 = time.perf_counter()
     ctx = _Ctx(spec, b, t, tol, proxy_count, proxy_factor)
     levels, store, _ = _run_levels(ctx)
-    rd, E_root, top, ipiv, UH, PsiV, UH_div, q, ratio = _finish_top(ctx, levels, store)
+    rd, E_root, top, ipiv, UH, PsiV, UH_div, q, ratio = _finish_top(ctx, levels, store, ctx.pipe)
     torch.cuda.synchronize()
     stats = {"k_per_level": {L.lev: int(L.k.max(initial=0)) for L in levels},
              "root_size": len(rd), "top_pivot_ratio": ratio}
@@ -1380,7 +1424,7 @@ def update(fct: Factorization, b_new, report, workers: int = 1) -> Factorization
     old = {L.lev: L for L in fct.levels}
     ctx = _Ctx(fct.spec, b_new, t_new, fct.tol, fct.proxy_count, fct.proxy_factor)
     levels, store, n_recomp = _run_levels(ctx, reuse=old, dirty=dirty)
-    rd, E_root, top, ipiv, UH, PsiV, UH_div, q, ratio = _finish_top(ctx, levels, store)
+    rd, E_root, top, ipiv, UH, PsiV, UH_div, q, ratio = _finish_top(ctx, levels, store, ctx.pipe)
     torch.cuda.synchronize()
     stats = {"k_per_level": {L.lev: int(L.k.max(initial=0)) for L in levels},
              "root_size": len(rd), "top_pivot_ratio": ratio}
