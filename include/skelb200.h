@@ -71,6 +71,13 @@ int skb_prof_enable(int32_t on);
 int skb_capture_begin(int64_t arena_bytes);
 int skb_capture_end(void);
 int skb_capture_release(int32_t session);
+
+/* Host -> device copy of a small host block (level descriptors, index lists)
+ * on `stream`, staged through the library's pinned ring (per-stream events
+ * guard slot reuse) or, inside a capture session, its arena.  The host block
+ * may be reused as soon as the call returns.  Replaces the implicit uploads
+ * of the reference's NumPy arrays (skel.py:293-338 operate on host arrays).  */
+int skb_h2d(const void* host, int64_t bytes, void* dev, void* stream);
 int skb_prof_add(int32_t family, double flops, double bytes);
 int skb_prof_read(double* ms_out, int64_t* count_out, double* flops_out, double* bytes_out,
                   int32_t reset);

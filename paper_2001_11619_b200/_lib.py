@@ -33,6 +33,7 @@ SIGNATURES = {
     "skb_capture_begin": [_i64],
     "skb_capture_end": [],
     "skb_capture_release": [_i32],
+    "skb_h2d": [_vp, _i64, _vp, _vp],
     "skb_prof_add": [_i32, _f64, _f64],
     "skb_prof_read": [_vp, _vp, _vp, _vp, _i32],
     "skb_gemm_grouped": [_vp, _i64, _vp],

@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <utility>
@@ -49,15 +50,24 @@ struct CaptureSession {
 CaptureSession& capture();
 
 // Pinned staging ring for descriptor uploads (asynchronous H2D copies).  The
-// ring is split into slots; a slot is reused only after the event recorded by
-// the last copy that read it has completed.
+// ring is split into slots; a slot is rewritten (one lap later) only after
+// every copy that read it has completed.  Copies are issued on several streams
+// (compression, level, sweep streams) that progress independently, so each
+// slot keeps one event per stream that copied from it in the current lap.
 struct PinnedRing {
   static constexpr size_t kSize = 64u << 20, kSlot = 1u << 20, kSlots = kSize / kSlot;
+  static constexpr int kPerSlot = 8;
+  struct Slot {
+    uint64_t lap = 0;
+    int n = 0;
+    cudaStream_t st[kPerSlot];
+    cudaEvent_t ev[kPerSlot];
+  };
   char* base = nullptr;
   size_t head = 0;
   uint64_t lap = 1;
-  cudaEvent_t ev[kSlots];
-  uint64_t slot_lap[kSlots] = {0};   // lap of the last copy recorded on the slot's event
+  Slot slot[kSlots];
+  std::vector<cudaEvent_t> pool;
 };
 PinnedRing& ring();
 
@@ -72,8 +82,6 @@ inline int ring_stage(const void* host, size_t bytes, cudaStream_t s, void* dev)
     uint64_t thr = ~0ull;
     SKB_RET(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
     SKB_RET(cudaHostAlloc((void**)&R.base, PinnedRing::kSize, cudaHostAllocDefault));
-    for (size_t i = 0; i < PinnedRing::kSlots; ++i)
-      SKB_RET(cudaEventCreateWithFlags(&R.ev[i], cudaEventDisableTiming));
   }
   if (bytes > PinnedRing::kSize / 2) {      // oversized: plain (pageable) copy
     SKB_RET(cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, s));
@@ -82,15 +90,44 @@ inline int ring_stage(const void* host, size_t bytes, cudaStream_t s, void* dev)
   size_t off = (R.head + 255) & ~(size_t)255;
   if (off + bytes > PinnedRing::kSize) { off = 0; ++R.lap; }
   const size_t s0 = off / PinnedRing::kSlot, s1 = (off + bytes - 1) / PinnedRing::kSlot;
-  // only data written in a previous lap can still be in flight in this region
-  for (size_t k = s0; k <= s1; ++k)
-    if (R.slot_lap[k] != 0 && R.slot_lap[k] < R.lap) SKB_RET(cudaEventSynchronize(R.ev[k]));
+  // data written in a previous lap may still be in flight in this region
+  for (size_t k = s0; k <= s1; ++k) {
+    PinnedRing::Slot& S = R.slot[k];
+    if (S.lap != R.lap) {
+      for (int i = 0; i < S.n; ++i) {
+        SKB_RET(cudaEventSynchronize(S.ev[i]));
+        R.pool.push_back(S.ev[i]);
+      }
+      S.n = 0;
+      S.lap = R.lap;
+    }
+  }
   memcpy(R.base + off, host, bytes);
   SKB_RET(cudaMemcpyAsync(dev, R.base + off, bytes, cudaMemcpyHostToDevice, s));
-  // the slot's event tracks its latest copy; it is waited on only one lap later
   for (size_t k = s0; k <= s1; ++k) {
-    SKB_RET(cudaEventRecord(R.ev[k], s));
-    R.slot_lap[k] = R.lap;
+    PinnedRing::Slot& S = R.slot[k];
+    int i = 0;
+    while (i < S.n && S.st[i] != s) ++i;
+    if (i == S.n) {
+      if (S.n == PinnedRing::kPerSlot) {
+        // too many streams on one slot: drain the oldest entries now
+        for (int j = 0; j < S.n; ++j) SKB_RET(cudaEventSynchronize(S.ev[j]));
+        for (int j = 0; j < S.n; ++j) R.pool.push_back(S.ev[j]);
+        S.n = 0;
+        i = 0;
+      }
+      cudaEvent_t e;
+      if (R.pool.empty()) {
+        SKB_RET(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      } else {
+        e = R.pool.back();
+        R.pool.pop_back();
+      }
+      S.st[i] = s;
+      S.ev[i] = e;
+      S.n = i + 1;
+    }
+    SKB_RET(cudaEventRecord(S.ev[i], s));     // latest copy of stream s from this slot
   }
   R.head = off + bytes;
   return 0;

@@ -286,6 +286,21 @@ extern "C" int skb_capture_begin(int64_t arena_bytes) {
   return 0;
 }
 
+extern "C" int skb_h2d(const void* host, int64_t bytes, void* dev, void* stream) {
+  if (bytes <= 0) return 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  auto& C = skb::capture();
+  if (C.on) {
+    const size_t off = (C.used + 255) & ~(size_t)255;
+    if (off + (size_t)bytes > C.size) return 5;        // arena exhausted
+    memcpy(C.arena + off, host, (size_t)bytes);
+    C.used = off + (size_t)bytes;
+    SKB_RET(cudaMemcpyAsync(dev, C.arena + off, (size_t)bytes, cudaMemcpyHostToDevice, s));
+    return 0;
+  }
+  return skb::ring_stage(host, (size_t)bytes, s, dev);
+}
+
 extern "C" int skb_capture_end(void) {
   skb::capture().on = false;
   skb::g_sessions.push_back(skb::capture().pinned);

@@ -23,6 +23,8 @@ a reference-style ``BoxFactors`` view (host copies) on demand.
 
 from __future__ import annotations
 
+import gc
+import os
 import time
 from dataclasses import dataclass
 
@@ -79,6 +81,31 @@ def _stream():
     return torch.cuda.current_stream().cuda_stream
 
 
+_LEVEL_STREAM = []
+
+
+def _level_stream() -> torch.cuda.Stream:
+    """Stream of the per-level Schur-complement work (created once)."""
+    if not _LEVEL_STREAM:
+        _LEVEL_STREAM.append(torch.cuda.Stream())
+        # the compression chain (stack -> QR -> QRCP -> host sync) is the
+        # critical path: it runs on a high-priority stream
+        _LEVEL_STREAM.append(torch.cuda.Stream(priority=-1))
+    return _LEVEL_STREAM[0]
+
+
+def _aug_stream() -> torch.cuda.Stream:
+    _level_stream()
+    if len(_LEVEL_STREAM) < 3:
+        _LEVEL_STREAM.append(torch.cuda.Stream())
+    return _LEVEL_STREAM[2]
+
+
+def _compress_stream() -> torch.cuda.Stream:
+    _level_stream()
+    return _LEVEL_STREAM[1]
+
+
 class _Prof:
     """Optional per-stage wall-clock breakdown (SKB_PROFILE=1 synchronises
     after every stage; off by default so the pipeline stays asynchronous)."""
@@ -121,12 +148,16 @@ def _csr(arrays):
     return off, flat
 
 
-IO = {"h2d": 0, "d2h": 0}      # host<->device bytes moved by this module
+IO = {"h2d": 0, "d2h": 0, "wait_s": 0.0, "waits": 0}   # host<->device traffic / host waits
 
 
 def _d2h(t: torch.Tensor) -> np.ndarray:
     IO["d2h"] += t.numel() * t.element_size()
-    return t.cpu().numpy()
+    t0 = time.perf_counter()
+    out = t.cpu().numpy()
+    IO["wait_s"] += time.perf_counter() - t0
+    IO["waits"] += 1
+    return out
 
 
 def _seg_gather(src, starts, lens):
@@ -224,11 +255,29 @@ class ActStore:
         self.s_len[idx] = k
 
 
-_CAPTURE = {"arena": None, "used": 0}   # pinned host arena while a CUDA graph is captured
+
+
+class _CaptureArena:
+    """Owns a library capture session (the pinned descriptor arena a captured
+    graph replays from).  Released lazily, outside any capture: a destructor
+    may run from the garbage collector in the middle of another capture."""
+    _pending = []
+
+    def __init__(self, sess):
+        self.sess = int(sess)
+
+    def __del__(self):
+        _CaptureArena._pending.append(self.sess)
+
+    @classmethod
+    def flush(cls):
+        while cls._pending:
+            call("skb_capture_release", cls._pending.pop())
 
 
 def _upload(**arrays):
-    """One pinned H2D copy for several host arrays; returns device views."""
+    """One H2D copy for several host arrays (staged by the library's pinned
+    ring, or its capture arena inside a CUDA-graph capture); returns device views."""
     dev = _dev()
     items, total = [], 0
     for k, a in arrays.items():
@@ -236,26 +285,19 @@ def _upload(**arrays):
         total = (total + 15) // 16 * 16
         items.append((k, a, total))
         total += a.nbytes
-    if _CAPTURE["arena"] is not None:
-        ar = _CAPTURE["arena"]
-        o = (_CAPTURE["used"] + 255) // 256 * 256
-        if o + max(total, 16) > ar.numel():
-            raise RuntimeError("capture arena exhausted")
-        host = ar[o:o + max(total, 16)]
-        _CAPTURE["used"] = o + max(total, 16)
-    else:
-        host = torch.empty(max(total, 16), dtype=torch.uint8, pin_memory=True)
-    hn = host.numpy()
+    total = max(total, 16)
+    hn = np.empty(total, np.uint8)
     for k, a, o in items:
         hn[o:o + a.nbytes] = a.view(np.uint8).reshape(-1)
-    d = host.to(dev, non_blocking=True)
+    d = torch.empty(total, dtype=torch.uint8, device=dev)
+    call("skb_h2d", hn, total, d, _stream())
     IO["h2d"] += total
     out = {}
     for k, a, o in items:
         tdt = {np.dtype(np.int64): torch.int64, np.dtype(np.float64): torch.float64,
                np.dtype(np.int32): torch.int32, np.dtype(np.uint64): torch.int64}[a.dtype]
         out[k] = d[o:o + a.nbytes].view(tdt)
-    out["_keep"] = (host, d)
+    out["_keep"] = (None, d)
     return out
 
 
@@ -352,10 +394,19 @@ class BoxBatch:
         pend = getattr(self, "_pending", None)
         if pend is not None:
             info_h, ratio_h, ev = pend
+            t0 = time.perf_counter()
             ev.synchronize()
+            IO["wait_s"] += time.perf_counter() - t0
+            IO["waits"] += 1
             self.info[:] = info_h.numpy()
             self.ratio[:] = ratio_h.numpy()
             self._pending = None
+        dfr = getattr(self, "_deferred", None)
+        if dfr:
+            self._deferred = []
+            for sel, other, osel in dfr:
+                other.resolve()
+                self.info[sel], self.ratio[sel] = other.info[osel], other.ratio[osel]
 
     def skel_csr(self):
         off, pos = _seg_gather(self.perm.astype(np.int64), self.act_off[:-1], self.k)
@@ -381,9 +432,10 @@ class BoxBatch:
         for f in self.FIELDS:
             self.ptr[f][sel] = other.ptr[f][osel]
         self.ipiv[sel] = other.ipiv[osel]
-        other.resolve()
-        self.resolve()
-        self.info[sel], self.ratio[sel] = other.info[osel], other.ratio[osel]
+        # pivot info may still be in flight: copy it when this batch is resolved
+        if getattr(self, "_deferred", None) is None:
+            self._deferred = []
+        self._deferred.append((sel, other, osel))
         have = {id(x) for x in self.slabs}
         self.slabs.extend(x for x in other.slabs if id(x) not in have)
 
@@ -427,6 +479,10 @@ class _Ctx:
         th = 2 * np.pi * np.arange(self.P) / self.P
         self.cs = np.stack([np.cos(th), np.sin(th)], axis=1)
         self.stats = {"kernel_s": {}}
+
+    @property
+    def sstream(self) -> torch.cuda.Stream:
+        return _level_stream()
 
     @property
     def g(self) -> DeviceBoundary:
@@ -497,8 +553,10 @@ class _Ctx:
         return co, cx
 
     # -- device pipeline ----------------------------------------------------
-    def compress(self, idx, store: "ActStore", kmin=None) -> BoxBatch:
-        """Compress a batch of same-level boxes (reference compress_box, skel.py:293-338)."""
+    def launch(self, idx, store: "ActStore", kmin=None) -> dict:
+        """(a)+(b) of compress_box (reference skel.py:293-316) for a batch of
+        same-level boxes: ID stacks, Householder pre-reduction and QRCP are
+        enqueued on the current stream; nothing waits."""
         t, P = self.t, self.P
         _Prof.start()
         idx = np.asarray(idx, np.int64)
@@ -535,41 +593,64 @@ class _Ctx:
         _Prof.tick("b_geqrf")
         m_q = np.where(pre, nB, rows).astype(np.int64)
         kmin_a = np.zeros(B, np.int64) if kmin is None else np.asarray(kmin, np.int64)
-        perm_d = torch.empty(max(len(act), 1), dtype=torch.int32, device=dev)
-        diag_d = torch.empty(max(len(act), 1), dtype=torch.float64, device=dev)
-        out_i = torch.empty(2 * B, dtype=torch.int32, device=dev)
-        gap_d = torch.empty(B, dtype=torch.float64, device=dev)
+        na = len(act)
+        ints = torch.empty(na + 2 * B + 1, dtype=torch.int32, device=dev)   # perm | k | steps
+        diag_d = torch.empty(max(na, 1), dtype=torch.float64, device=dev)
+        gap_d = torch.empty(max(B, 1), dtype=torch.float64, device=dev)
         lda = rows.astype(np.int64)
         call("skb_qrcp_id_batched", B, m_q, nB, lda,
-             A, kmin_a, self.tol, act_off, ptr(perm_d),
-             ptr(diag_d), ptr(out_i), ptr(out_i) + 4 * B, ptr(gap_d), s)
+             A, kmin_a, self.tol, act_off, ptr(ints),
+             ptr(diag_d), ptr(ints) + 4 * na, ptr(ints) + 4 * (na + B), ptr(gap_d), s)
         _Prof.tick("b_qrcp")
-        bt = BoxBatch(idx, act_off, act)
-        bt.perm[:] = _d2h(perm_d[:len(act)])      # sync point 1 (sizes for (c))
-        oi = _d2h(out_i)
-        bt.k[:] = oi[:B]
-        bt.steps[:] = oi[B:]
-        bt.gap[:] = _d2h(gap_d)
+        ints_h = torch.empty(ints.numel(), dtype=torch.int32, pin_memory=True)
+        gap_h = torch.empty(gap_d.numel(), dtype=torch.float64, pin_memory=True)
+        ints_h.copy_(ints, non_blocking=True)
+        gap_h.copy_(gap_d, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        IO["d2h"] += 4 * ints.numel() + 8 * gap_d.numel()
+        return dict(idx=idx, act_off=act_off, act=act, nB=nB, rows=rows, pre=pre, m_q=m_q,
+                    stack=stack, up=up, A=A, lda=lda, perm_d=ints, ints_h=ints_h, gap_h=gap_h,
+                    ev=ev)
+
+    def finish(self, h: dict) -> BoxBatch:
+        """Wait for a launched batch's QRCP (the one host sync per level) and
+        lay out its factor storage; no kernels are launched."""
+        idx, act_off, nB = h["idx"], h["act_off"], h["nB"]
+        B, na = len(idx), len(h["act"])
+        t0 = time.perf_counter()
+        h["ev"].synchronize()                     # sync point (sizes for (c))
+        IO["wait_s"] += time.perf_counter() - t0
+        IO["waits"] += 1
+        ih = h["ints_h"].numpy()
+        bt = BoxBatch(idx, act_off, h["act"])
+        bt.perm[:] = ih[:na]
+        bt.k[:] = ih[na:na + B]
+        bt.steps[:] = ih[na + B:na + 2 * B]
+        bt.gap[:] = h["gap_h"].numpy()[:B]
         k = bt.k
         r = nB - k
         if _lib.PROF_ON:
             # algorithmic work (SURVEY.md §8(d)): stack + self-block bytes written,
             # Householder 2 m n^2 - 2/3 n^3, QRCP 2mn + sum_i 4 (m-i)(n-i-1)
+            rows, pre = h["rows"], h["pre"]
             _lib.prof_add("assemble", 0.0, 8.0 * float((rows * nB).sum() + (nB * nB).sum()))
             mr, nr_ = rows[pre].astype(float), nB[pre].astype(float)
             _lib.prof_add("geqrf", float((2 * mr * nr_ ** 2 - 2.0 / 3.0 * nr_ ** 3).sum()))
             fq = 0.0
-            for mm, nn, st in zip(m_q, nB, bt.steps):
+            for mm, nn, st in zip(h["m_q"], nB, bt.steps):
                 i_ = np.arange(st, dtype=float)
                 fq += 2.0 * mm * nn + float((4.0 * (mm - i_) * (nn - i_ - 1)).sum())
             _lib.prof_add("qrcp", fq)
-        # ---- factor storage (one slab) and scratch
-        sz = np.stack([k * r, r * r, r * r, k * r, r * k, k * k], axis=1)
-        tot = sz.sum(axis=1)
-        boff = np.zeros(B + 1, np.int64)
-        np.cumsum(tot, out=boff[1:])
-        slab = torch.empty(max(int(boff[-1]), 1), dtype=torch.float64, device=dev)
-        ipiv = torch.empty(max(int(r.sum()), 1), dtype=torch.int32, device=dev)
+        # factor storage (one slab), allocated for the level stream that fills it
+        dev = _dev()
+        with torch.cuda.stream(self.sstream):
+            sz = np.stack([k * r, r * r, r * r, k * r, r * k, k * k], axis=1)
+            tot = sz.sum(axis=1)
+            boff = np.zeros(B + 1, np.int64)
+            np.cumsum(tot, out=boff[1:])
+            slab = torch.empty(max(int(boff[-1]), 1), dtype=torch.float64, device=dev)
+            ipiv = torch.empty(max(int(r.sum()), 1), dtype=torch.int32, device=dev)
         bt.slabs.append(slab)
         bt.slabs.append(ipiv)
         sb = _addr(slab)
@@ -580,6 +661,29 @@ class _Ctx:
         ioff = np.zeros(B + 1, np.int64)
         np.cumsum(r, out=ioff[1:])
         bt.ipiv[:] = (_addr(ipiv) + 4 * ioff[:-1]).astype(np.uint64)
+        bt._launch = h
+        return bt
+
+    def schur(self, bt: BoxBatch, store: "ActStore"):
+        """(c) of compress_box (reference skel.py:317-338) on the level stream:
+        it depends on this batch's QRCP and on the children's Xss (previous
+        level, same stream), not on the next level's compression."""
+        h = bt.__dict__.pop("_launch")
+        S = self.sstream
+        S.wait_event(h["ev"])
+        for tns in (h["stack"], h["perm_d"], h["up"]["_keep"][1]):
+            tns.record_stream(S)
+        with torch.cuda.stream(S):
+            self._schur(bt, store, h)
+
+    def _schur(self, bt, store, h):
+        idx, act_off, nB, up, A, lda, perm_d = (h["idx"], h["act_off"], h["nB"], h["up"], h["A"],
+                                                h["lda"], h["perm_d"])
+        k = bt.k
+        r = nB - k
+        B = len(idx)
+        dev = _dev()
+        s = _stream()
         E_off = np.zeros(B + 1, np.int64)
         np.cumsum(nB * nB, out=E_off[1:])
         Ebuf = torch.empty(max(int(E_off[-1]), 1), dtype=torch.float64, device=dev)
@@ -646,11 +750,13 @@ class _Ctx:
         ev.record()
         IO["d2h"] += 12 * B
         bt._pending = (info_h, ratio_h, ev)
-        del stack, Ebuf, Xrs
-        return bt
+        del Ebuf, Xrs
 
-    def compress_level(self, idx, store) -> BoxBatch:
-        return self.compress(idx, store)
+    def compress(self, idx, store: "ActStore", kmin=None) -> BoxBatch:
+        """Compress a batch of same-level boxes (reference compress_box, skel.py:293-338)."""
+        bt = self.finish(self.launch(idx, store, kmin))
+        self.schur(bt, store)
+        return bt
 
     def migrate(self, bt: "BoxBatch", store) -> bool:
         """R -> S migration while the X_RR pivot ratio is below the floor
@@ -929,22 +1035,32 @@ class Factorization:
             self._solve_dev(x.clone())           # warm-up outside capture
             torch.cuda.synchronize()
             g = torch.cuda.CUDAGraph()
-            arena = torch.empty(32 << 20, dtype=torch.uint8, pin_memory=True)
-            call("skb_capture_begin", 16 << 20)
-            _CAPTURE["arena"], _CAPTURE["used"] = arena, 0
+            # destructors of unreachable objects holding graphs / device memory
+            # must not run inside the capture (graph teardown and frees are
+            # illegal there): collect now and keep the collector off meanwhile
+            gc.collect()
+            _CaptureArena.flush()
+            call("skb_capture_begin", 48 << 20)
+            gc_was = gc.isenabled()
+            gc.disable()
             try:
                 with torch.cuda.graph(g):
                     self._solve_dev(xs)
             except Exception:
-                _CAPTURE["arena"] = None
+                if gc_was:
+                    gc.enable()
+                if os.environ.get("SKB_DEBUG_CAPTURE"):
+                    import traceback
+                    traceback.print_exc()
                 call("skb_capture_end")
                 self._graphs[nr] = False
                 torch.cuda.synchronize()
                 self._solve_dev(x)
                 return x
-            _CAPTURE["arena"] = None
+            if gc_was:
+                gc.enable()
             sess = call("skb_capture_end")
-            ent = (g, xs, sess, (self._keep, arena))
+            ent = (g, xs, _CaptureArena(sess), self._keep)
             if len(self._graphs) >= 4:
                 self._graphs.clear()
             self._graphs[nr] = ent
@@ -1137,14 +1253,18 @@ class _AugPipe:
         self._hc = torch.from_numpy(np.ascontiguousarray(b.hole_centers, np.float64)).to(dev)
         call("skb_assemble_aug", ptr(ctx.g.pos), ptr(ctx.g.w), b.n_nodes, ptr(self._hc), b.n_holes,
              np.ascontiguousarray(b.offsets, np.int64), ptr(self.UH), ptr(self.PsiV), _stream())
-        self.stream = torch.cuda.Stream()
+        self.stream = _aug_stream()
+        self.src = ctx.sstream
 
     def submit(self, L: "LevelFactors"):
         if not self.q:
             return
-        ev = torch.cuda.Event()
-        ev.record()
-        self.stream.wait_event(ev)
+        # the level's Schur work (level stream) and its descriptor uploads /
+        # H, Psi assembly (current stream) must both precede the sweep
+        for st in (self.src, torch.cuda.current_stream()):
+            ev = torch.cuda.Event()
+            ev.record(st)
+            self.stream.wait_event(ev)
         with torch.cuda.stream(self.stream):
             _aug_level(L, self.UH, self.PsiV, self.UH_div, self.schur, self.q)
 
@@ -1291,7 +1411,13 @@ def _aug_level(L: LevelFactors, UH, PsiV, UH_div, schur, q):
 
 
 def _run_levels(ctx: _Ctx, reuse=None, dirty=None):
-    """Bottom-up level loop (reference factor skel.py:443-449 / update skel.py:502-509)."""
+    """Bottom-up level loop (reference factor skel.py:443-449 / update skel.py:502-509).
+
+    Software-pipelined: as soon as a level's QRCP results reach the host, the
+    next level's ID stacks / QR / QRCP are launched (they need only the new
+    skeleton lists), then this level's Schur complements go to the level
+    stream, so the host bookkeeping and the Schur work overlap the critical
+    QRCP -> host -> QRCP chain."""
     t = ctx.t
     store = ActStore(t)
     ctx.store = store
@@ -1301,45 +1427,20 @@ def _run_levels(ctx: _Ctx, reuse=None, dirty=None):
     levels = []
     n_recomp = 0
     prev = None          # (level, batch, fresh boxes) whose migration check is pending
-    lev = t.depth
     if _Prof.enabled:
         torch.cuda.synchronize()
         _Prof._lt = time.perf_counter()
-    while lev >= 1:
+
+    def start(lev):
         idx = t.level_indices(lev)
         store.set_internal(t, idx)            # assign_internal_actives, skel.py:251-256
         if reuse is None:
             todo = idx
         else:
             todo = idx[np.fromiter((t.key(i) in dirty for i in idx), bool, len(idx))]
-        bt_new = ctx.compress_level(todo, store) if len(todo) else None
-        # the previous level's X_RR pivot ratios are available now (its kernels ran
-        # before this level's QRCP sync); a migration there invalidates this level
-        if prev is not None and prev[2] is not None and ctx.migrate(prev[2], store):
-            pl, pbt, pnew = prev
-            if pbt is not pnew:
-                pos = np.searchsorted(pbt.idx, pnew.idx)
-                pbt.take(pos, pnew, np.arange(len(pnew.idx)))
-            store.set_skel(pbt.idx, pbt.act_off, pbt.act, pbt.perm, pbt.k)
-            store.xss[pbt.idx] = pbt.ptr["Xss"]
-            levels[-1] = LevelFactors(pl, t, pbt, *_hole_columns(t, ctx.b, pbt.idx, pairs))
-            prev = (pl, pbt, None)
-            continue                          # redo this level on the corrected skeletons
-        if prev is not None:
-            pipe.submit(levels[-1])           # previous level final: start its aug sweep
-        n_recomp += len(todo)
-        if _Prof.enabled:
-            torch.cuda.synchronize()
-            _Prof.acc[f"level{lev}"] = time.perf_counter() - _Prof._lt
-            _Prof._lt = time.perf_counter()
-        bt = bt_new if reuse is None else _merge_level(ctx, idx, store, todo, bt_new, reuse)
-        store.set_skel(bt.idx, bt.act_off, bt.act, bt.perm, bt.k)
-        store.xss[bt.idx] = bt.ptr["Xss"]
-        cols_off, cols = _hole_columns(t, ctx.b, bt.idx, pairs)
-        levels.append(LevelFactors(lev, t, bt, cols_off, cols))
-        prev = (lev, bt, bt_new)
-        lev -= 1
-    if prev is not None and prev[2] is not None and ctx.migrate(prev[2], store):
+        return idx, todo, (ctx.launch(todo, store) if len(todo) else None)
+
+    def fix_prev():
         pl, pbt, pnew = prev
         if pbt is not pnew:
             pos = np.searchsorted(pbt.idx, pnew.idx)
@@ -1347,8 +1448,42 @@ def _run_levels(ctx: _Ctx, reuse=None, dirty=None):
         store.set_skel(pbt.idx, pbt.act_off, pbt.act, pbt.perm, pbt.k)
         store.xss[pbt.idx] = pbt.ptr["Xss"]
         levels[-1] = LevelFactors(pl, t, pbt, *_hole_columns(t, ctx.b, pbt.idx, pairs))
+        return (pl, pbt, None)
+
+    lev = t.depth
+    cur = start(lev) if lev >= 1 else None
+    while lev >= 1:
+        idx, todo, h = cur
+        bt_new = ctx.finish(h) if h is not None else None
+        # the previous level's X_RR pivot ratios are available now (its kernels
+        # ran before this sync); a migration there invalidates this level
+        if prev is not None and prev[2] is not None and ctx.migrate(prev[2], store):
+            prev = fix_prev()
+            cur = start(lev)                  # redo this level on the corrected skeletons
+            continue
+        if prev is not None:
+            pipe.submit(levels[-1])           # previous level final: start its aug sweep
+        n_recomp += len(todo)
+        bt = bt_new if reuse is None else _merge_level(ctx, idx, store, todo, bt_new, reuse)
+        store.set_skel(bt.idx, bt.act_off, bt.act, bt.perm, bt.k)
+        store.xss[bt.idx] = bt.ptr["Xss"]
+        nxt = start(lev - 1) if lev > 1 else None     # critical path first
+        if bt_new is not None:
+            ctx.schur(bt_new, store)
+        if _Prof.enabled:
+            torch.cuda.synchronize()
+            _Prof.acc[f"level{lev}"] = time.perf_counter() - _Prof._lt
+            _Prof._lt = time.perf_counter()
+        cols_off, cols = _hole_columns(t, ctx.b, bt.idx, pairs)
+        levels.append(LevelFactors(lev, t, bt, cols_off, cols))
+        prev = (lev, bt, bt_new)
+        lev -= 1
+        cur = nxt
+    if prev is not None and prev[2] is not None and ctx.migrate(prev[2], store):
+        prev = fix_prev()
     if levels:
         pipe.submit(levels[-1])
+    torch.cuda.current_stream().wait_stream(ctx.sstream)
     return levels, store, n_recomp
 
 
@@ -1398,8 +1533,9 @@ def factor(spec, b, t: Tree, tol: float, workers: int = 1,
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     ctx = _Ctx(spec, b, t, tol, proxy_count, proxy_factor)
-    levels, store, _ = _run_levels(ctx)
-    rd, E_root, top, ipiv, UH, PsiV, UH_div, q, ratio = _finish_top(ctx, levels, store, ctx.pipe)
+    with torch.cuda.stream(_compress_stream()):
+        levels, store, _ = _run_levels(ctx)
+        rd, E_root, top, ipiv, UH, PsiV, UH_div, q, ratio = _finish_top(ctx, levels, store, ctx.pipe)
     torch.cuda.synchronize()
     stats = {"k_per_level": {L.lev: int(L.k.max(initial=0)) for L in levels},
              "root_size": len(rd), "top_pivot_ratio": ratio}
@@ -1423,8 +1559,10 @@ def update(fct: Factorization, b_new, report, workers: int = 1) -> Factorization
         raise NotImplementedError("only DOF-preserving edits (hole moves) are supported")
     old = {L.lev: L for L in fct.levels}
     ctx = _Ctx(fct.spec, b_new, t_new, fct.tol, fct.proxy_count, fct.proxy_factor)
-    levels, store, n_recomp = _run_levels(ctx, reuse=old, dirty=dirty)
-    rd, E_root, top, ipiv, UH, PsiV, UH_div, q, ratio = _finish_top(ctx, levels, store, ctx.pipe)
+    torch.cuda.current_stream().synchronize()
+    with torch.cuda.stream(_compress_stream()):
+        levels, store, n_recomp = _run_levels(ctx, reuse=old, dirty=dirty)
+        rd, E_root, top, ipiv, UH, PsiV, UH_div, q, ratio = _finish_top(ctx, levels, store, ctx.pipe)
     torch.cuda.synchronize()
     stats = {"k_per_level": {L.lev: int(L.k.max(initial=0)) for L in levels},
              "root_size": len(rd), "top_pivot_ratio": ratio}
