@@ -106,6 +106,38 @@ def _compress_stream() -> torch.cuda.Stream:
     return _LEVEL_STREAM[1]
 
 
+class _HostTimer:
+    """Host-only time per section (SKB_HOST_PROF=1; no device syncs)."""
+
+    enabled = bool(os.environ.get("SKB_HOST_PROF"))
+    acc: dict = {}
+
+    def __init__(self, name):
+        self.name = name
+
+    def __enter__(self):
+        self.t0 = time.perf_counter()
+
+    def __exit__(self, *a):
+        a_ = _HostTimer.acc
+        a_[self.name] = a_.get(self.name, 0.0) + time.perf_counter() - self.t0
+
+
+class _Null:
+    def __enter__(self):
+        pass
+
+    def __exit__(self, *a):
+        pass
+
+
+_NULL = _Null()
+
+
+def _ht(name):
+    return _HostTimer(name) if _HostTimer.enabled else _NULL
+
+
 class _Prof:
     """Optional per-stage wall-clock breakdown (SKB_PROFILE=1 synchronises
     after every stage; off by default so the pipeline stays asynchronous)."""
@@ -492,10 +524,10 @@ class _Ctx:
         return self._g
 
     # -- host bookkeeping ---------------------------------------------------
-    def far_lists(self, idx, store: "ActStore"):
-        """F_int per box (reference _Compressor.far_dofs, skel.py:258-280):
-        colleagues (sorted keys) then coarser leaves meeting the proxy disc
-        (sorted keys), filtered by strict distance < r_p from the box centre."""
+    def far_pairs(self, idx):
+        """Skeleton-independent half of far_dofs (reference skel.py:258-280):
+        the (box, source box) candidate pairs -- colleagues (sorted keys) then
+        coarser leaves meeting the proxy disc (sorted keys) -- and the radii."""
         t = self.t
         rp = proxy_radius(t.hw[idx], self.factor)
         nbr = t.neighbors[idx]
@@ -505,7 +537,14 @@ class _Ctx:
         pb = np.concatenate([bl_n, bl_c]).astype(np.int64)
         ps = np.concatenate([src_n, src_c]).astype(np.int64)
         order = np.argsort(pb, kind="stable")
-        pb, ps = pb[order], ps[order]
+        return rp, pb[order], ps[order]
+
+    def far_lists(self, idx, store: "ActStore", pairs=None):
+        """F_int per box (reference _Compressor.far_dofs, skel.py:258-280):
+        active DOFs of the candidate sources, filtered by strict distance < r_p
+        from the box centre."""
+        t = self.t
+        rp, pb, ps = self.far_pairs(idx) if pairs is None else pairs
         B = len(idx)
         if len(ps) == 0:
             return np.zeros(B + 1, np.int64), np.zeros(0, np.int64)
@@ -528,14 +567,18 @@ class _Ctx:
         """Proxy rings + radial normals + weights (kernels.py:263-273, 340-342)."""
         rp = proxy_radius(self.t.hw[idx], self.factor)
         pts = self.t.center[idx][:, None, :] + rp[:, None, None] * self.cs[None]
-        acc = pts[:, 0, :].copy()
-        for p in range(1, self.P):
-            acc = acc + pts[:, p, :]
-        ctr = acc / self.P
+        # ring centre: sequential left-to-right sum (cumsum keeps that order)
+        ctr = np.cumsum(pts, axis=1)[:, -1, :] / self.P
         pn = pts - ctr[:, None, :]
         pn = pn / np.sqrt((pn * pn).sum(axis=2))[:, :, None]
         pw = 2 * np.pi * rp / self.P
         return pts, pn, pw
+
+    def prep(self, idx) -> dict:
+        """Skeleton-independent inputs of launch() for a batch (candidate far
+        pairs, proxy rings); computed while the previous level is on the GPU."""
+        idx = np.asarray(idx, np.int64)
+        return dict(pairs=self.far_pairs(idx), proxies=self.proxies(idx))
 
     def child_desc(self, idx, store: "ActStore"):
         """Children's skeleton offsets (active order) and Xss addresses."""
@@ -553,7 +596,7 @@ class _Ctx:
         return co, cx
 
     # -- device pipeline ----------------------------------------------------
-    def launch(self, idx, store: "ActStore", kmin=None) -> dict:
+    def launch(self, idx, store: "ActStore", kmin=None, prep=None) -> dict:
         """(a)+(b) of compress_box (reference skel.py:293-316) for a batch of
         same-level boxes: ID stacks, Householder pre-reduction and QRCP are
         enqueued on the current stream; nothing waits."""
@@ -561,11 +604,15 @@ class _Ctx:
         _Prof.start()
         idx = np.asarray(idx, np.int64)
         B = len(idx)
-        act_off, act = store.acts(idx)
+        with _ht("L.acts"):
+            act_off, act = store.acts(idx)
         nB = np.diff(act_off)
-        far_off, far = self.far_lists(idx, store)
+        if prep is None:
+            prep = self.prep(idx)
+        with _ht("L.far_lists"):
+            far_off, far = self.far_lists(idx, store, prep["pairs"])
         nF = np.diff(far_off)
-        pts, pn, pw = self.proxies(idx)
+        pts, pn, pw = prep["proxies"]
         rows = 2 * nF + 6 * P + 2
         sizes = rows * nB
         stack_off = np.zeros(B + 1, np.int64)
@@ -619,7 +666,8 @@ class _Ctx:
         idx, act_off, nB = h["idx"], h["act_off"], h["nB"]
         B, na = len(idx), len(h["act"])
         t0 = time.perf_counter()
-        h["ev"].synchronize()                     # sync point (sizes for (c))
+        with _ht("F.wait"):
+            h["ev"].synchronize()                 # sync point (sizes for (c))
         IO["wait_s"] += time.perf_counter() - t0
         IO["waits"] += 1
         ih = h["ints_h"].numpy()
@@ -1431,14 +1479,22 @@ def _run_levels(ctx: _Ctx, reuse=None, dirty=None):
         torch.cuda.synchronize()
         _Prof._lt = time.perf_counter()
 
-    def start(lev):
+    def pre(lev):
+        """Level lev's batch and its skeleton-independent launch inputs."""
         idx = t.level_indices(lev)
-        store.set_internal(t, idx)            # assign_internal_actives, skel.py:251-256
         if reuse is None:
             todo = idx
         else:
             todo = idx[np.fromiter((t.key(i) in dirty for i in idx), bool, len(idx))]
-        return idx, todo, (ctx.launch(todo, store) if len(todo) else None)
+        with _ht("prep"):
+            return idx, todo, (ctx.prep(todo) if len(todo) else None)
+
+    def go(p):
+        idx, todo, pr = p
+        with _ht("set_internal"):
+            store.set_internal(t, idx)        # assign_internal_actives, skel.py:251-256
+        with _ht("launch"):
+            return idx, todo, (ctx.launch(todo, store, prep=pr) if len(todo) else None)
 
     def fix_prev():
         pl, pbt, pnew = prev
@@ -1451,32 +1507,39 @@ def _run_levels(ctx: _Ctx, reuse=None, dirty=None):
         return (pl, pbt, None)
 
     lev = t.depth
-    cur = start(lev) if lev >= 1 else None
+    p_cur = pre(lev) if lev >= 1 else None
+    cur = go(p_cur) if lev >= 1 else None
+    p_nxt = pre(lev - 1) if lev > 1 else None
     while lev >= 1:
         idx, todo, h = cur
-        bt_new = ctx.finish(h) if h is not None else None
+        with _ht("finish"):
+            bt_new = ctx.finish(h) if h is not None else None
         # the previous level's X_RR pivot ratios are available now (its kernels
         # ran before this sync); a migration there invalidates this level
         if prev is not None and prev[2] is not None and ctx.migrate(prev[2], store):
             prev = fix_prev()
-            cur = start(lev)                  # redo this level on the corrected skeletons
+            cur = go(p_cur)                   # redo this level on the corrected skeletons
             continue
         if prev is not None:
-            pipe.submit(levels[-1])           # previous level final: start its aug sweep
+            with _ht("aug_submit"):
+                pipe.submit(levels[-1])       # previous level final: start its aug sweep
         n_recomp += len(todo)
         bt = bt_new if reuse is None else _merge_level(ctx, idx, store, todo, bt_new, reuse)
         store.set_skel(bt.idx, bt.act_off, bt.act, bt.perm, bt.k)
         store.xss[bt.idx] = bt.ptr["Xss"]
-        nxt = start(lev - 1) if lev > 1 else None     # critical path first
+        nxt = go(p_nxt) if lev > 1 else None          # critical path first
         if bt_new is not None:
-            ctx.schur(bt_new, store)
+            with _ht("schur"):
+                ctx.schur(bt_new, store)
         if _Prof.enabled:
             torch.cuda.synchronize()
             _Prof.acc[f"level{lev}"] = time.perf_counter() - _Prof._lt
             _Prof._lt = time.perf_counter()
-        cols_off, cols = _hole_columns(t, ctx.b, bt.idx, pairs)
-        levels.append(LevelFactors(lev, t, bt, cols_off, cols))
+        with _ht("levelfactors"):
+            cols_off, cols = _hole_columns(t, ctx.b, bt.idx, pairs)
+            levels.append(LevelFactors(lev, t, bt, cols_off, cols))
         prev = (lev, bt, bt_new)
+        p_cur, p_nxt = p_nxt, (pre(lev - 2) if lev > 2 else None)   # while the GPU compresses
         lev -= 1
         cur = nxt
     if prev is not None and prev[2] is not None and ctx.migrate(prev[2], store):
@@ -1534,9 +1597,12 @@ def factor(spec, b, t: Tree, tol: float, workers: int = 1,
     t0 = time.perf_counter()
     ctx = _Ctx(spec, b, t, tol, proxy_count, proxy_factor)
     with torch.cuda.stream(_compress_stream()):
-        levels, store, _ = _run_levels(ctx)
-        rd, E_root, top, ipiv, UH, PsiV, UH_div, q, ratio = _finish_top(ctx, levels, store, ctx.pipe)
-    torch.cuda.synchronize()
+        with _ht("run_levels"):
+            levels, store, _ = _run_levels(ctx)
+        with _ht("finish_top"):
+            rd, E_root, top, ipiv, UH, PsiV, UH_div, q, ratio = _finish_top(ctx, levels, store, ctx.pipe)
+    with _ht("final_sync"):
+        torch.cuda.synchronize()
     stats = {"k_per_level": {L.lev: int(L.k.max(initial=0)) for L in levels},
              "root_size": len(rd), "top_pivot_ratio": ratio}
     fct = Factorization(spec, b, t, tol, proxy_count, proxy_factor, levels, rd, E_root, top, ipiv,

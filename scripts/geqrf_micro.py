@@ -21,9 +21,12 @@ def run(m, n, B, reps=5):
         if r: ts.append(e0.elapsed_time(e1))
     return min(ts)
 
-shapes = [(512, 32), (512, 64), (512, 96), (512, 128), (512, 160), (512, 192),
+if __name__ != "__main__":
+    shapes = []
+else:
+    shapes = [(512, 32), (512, 64), (512, 96), (512, 128), (512, 160), (512, 192),
           (256, 96), (384, 96), (1024, 96), (1024, 192), (2048, 96)]
-for m, n in shapes:
+for m, n in shapes:  # noqa
     t1 = run(m, n, 1)
     t148 = run(m, n, 148)
     t296 = run(m, n, 296)

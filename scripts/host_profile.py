@@ -22,4 +22,4 @@ torch.cuda.synchronize()
 pr.disable()
 print("factor_time", f.stats["factor_time"])
 st = pstats.Stats(pr)
-st.sort_stats("tottime").print_stats(30)
+st.sort_stats(sys.argv[2] if len(sys.argv) > 2 else "tottime").print_stats(45)
