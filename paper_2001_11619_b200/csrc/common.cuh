@@ -133,6 +133,24 @@ inline int ring_stage(const void* host, size_t bytes, cudaStream_t s, void* dev)
   return 0;
 }
 
+// Opt a kernel into the largest dynamic shared memory once (changing the
+// attribute between launches can serialise the device).
+inline cudaError_t smem_optin(const void* fn) {
+  static std::vector<const void*> done;
+  for (const void* f : done)
+    if (f == fn) return cudaSuccess;
+  int dev = 0, mx = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&mx, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaFuncAttributes fa;
+  if (e == cudaSuccess) e = cudaFuncGetAttributes(&fa, fn);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             mx - (int)fa.sharedSizeBytes);
+  if (e == cudaSuccess) done.push_back(fn);
+  return e;
+}
+
 // Copy host descriptors to a stream-ordered device buffer (freed async by caller).
 template <typename T>
 inline int upload(const T* host, int64_t n, cudaStream_t s, T** dev) {

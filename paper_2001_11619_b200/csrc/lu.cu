@@ -340,8 +340,7 @@ int getrf_batched(int64_t nbox, const SkbMat* a, const int64_t* ipiv, int32_t* i
     SmallLU* ds = nullptr;
     if ((rc = upload(sl.data(), (int64_t)sl.size(), s, &ds))) return rc;
     const size_t smem = sizeof(double) * (size_t)max_small * (max_small + 1);
-    SKB_RET(cudaFuncSetAttribute(k_getrf_small<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
+    SKB_RET(smem_optin((const void*)k_getrf_small<256>));
     {
       ProfScope ps(F_GETRF, s);
       k_getrf_small<256><<<(unsigned)sl.size(), 256, smem, s>>>(ds);
@@ -364,8 +363,7 @@ int getrf_batched(int64_t nbox, const SkbMat* a, const int64_t* ipiv, int32_t* i
   for (int64_t b = 0; b < nbox; ++b)
     if (a[b].rows > kSmallLU) rounds = std::max(rounds, (a[b].rows + pbw(a[b].rows) - 1) / pbw(a[b].rows));
   if (rounds > 0) {
-    SKB_RET(cudaFuncSetAttribute(k_getf2_panel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)kPanelSmem));
+    SKB_RET(smem_optin((const void*)k_getf2_panel<512>));
   }
   for (int64_t rd_ = 0; rd_ < rounds; ++rd_) {
     pd.clear(); td.clear(); gd.clear();
