@@ -239,6 +239,68 @@ int skb_system_matvec(const double* pos, const double* nrm, const double* w, con
 int skb_fill_rows(int64_t nidx, const int64_t* idx, double* dst, int64_t ld, const void* unused,
                   int64_t ncols, double value, void* stream);
 
+/* ---- level-granular entry points (csrc/level.cu) ---------------------------
+ * One call per quadtree level; descriptor arrays are HOST memory, matrices
+ * device.  Per-box factor addresses (uint64) as laid out by the caller.      */
+
+/* (c) of compress_box for a level batch (skel.py:316-338): T = R11^-1 R12 from
+ * the QRCP'd stacks A (lda), permuted self blocks E with the children's Xss
+ * (child_off/child_xss: nbox x 5, as skb_assemble_self), X_sr, X_rs, X_rr
+ * (grouped DMMA GEMMs), LU(X_rr) with pivot ratio (info_dev/ratio_dev, as
+ * skb_getrf_batched), X_rs_div = X_rr^-1 X_rs and Xss_mod = E_SS - X_sr X_rs_div.
+ * nB, k, act_off: host; act_off_dev/act_dev/perm_dev: the level's device CSR
+ * active lists and QRCP permutations.                                         */
+int skb_level_schur(int64_t nbox, const int64_t* nB, const int64_t* k,
+                    const int64_t* act_off, const double* pos, const double* nrm,
+                    const double* w, const double* kappa, const int64_t* act_off_dev,
+                    const int64_t* act_dev, const int32_t* perm_dev, const int64_t* A,
+                    const int64_t* lda, const int64_t* child_off,
+                    const uint64_t* child_xss, const uint64_t* T, const uint64_t* Xrr,
+                    const uint64_t* LU, const uint64_t* Xsr, const uint64_t* Xrsdiv,
+                    const uint64_t* Xss, const uint64_t* ipiv, int32_t* info_dev,
+                    double* ratio_dev, void* stream);
+
+/* (d) augmentation sweep of one level (_finish_top, skel.py:384-396): on the
+ * (2N x q) UH / PsiV / UH_div, UH_R -= T^T UH_S; w = X_rr^-1 UH_R;
+ * UH_S -= X_sr w; UH_div_R = w; PsiV_R -= T^T PsiV_S; PsiV_S -= X_rs_div^T PsiV_R
+ * (PsiV restricted to the box's hole columns cols, host CSR cols_off/cols and
+ * the same lists on the device c_off/c) and the deterministic (box order)
+ * accumulation schur += PsiV_R^T w.  sd/rd: device CSR skeleton/redundant DOFs. */
+int skb_level_aug(int64_t nbox, const int64_t* k, const int64_t* r, int64_t q,
+                  const int64_t* cols_off, const int64_t* cols, const int64_t* sd_off,
+                  const int64_t* sd, const int64_t* rd_off, const int64_t* rd,
+                  const int64_t* c_off, const int64_t* c, const uint64_t* T,
+                  const uint64_t* LU, const uint64_t* Xsr, const uint64_t* Xrsdiv,
+                  const uint64_t* ipiv, double* UH, double* PsiV, double* UH_div,
+                  double* schur, void* stream);
+
+/* ---- native host runtime (host arrays, no device; csrc/host.cpp) ---------
+ * Per-level bookkeeping the reference does per box in Python.  Tree arrays as
+ * in tree.py: center (nbox x 2), hw, neighbours (nbox x 8, -1 = none, sorted
+ * keys), lev/ix/iy, is_leaf (uint8), level_start (depth + 2);
+ * root = {cx, cy, half width}.                                               */
+
+/* F_int of each box idx[b] (reference _Compressor.far_dofs, skel.py:258-280 with
+ * Tree.colleagues tree.py:70-81, Tree.shallow_leaves_near tree.py:83-99 and
+ * proxy_radius tree.py:158-160): active DOFs (segments big[a_start[j]..+a_len[j]])
+ * of the colleagues then the coarser leaves meeting the proxy disc, kept where
+ * the node lies strictly inside the disc.  far_off: nb + 1.  Returns 1 with
+ * *need = required length when cap is too small.                            */
+int skb_host_far_lists(int64_t nb, const int64_t* idx, const double* center, const double* hw,
+                       const int64_t* nbr, const int64_t* lev, const int64_t* ix,
+                       const int64_t* iy, const uint8_t* is_leaf, const int64_t* level_start,
+                       int64_t depth, const double* root, double factor, const int64_t* big,
+                       const int64_t* a_start, const int64_t* a_len, const double* px,
+                       const double* py, int64_t* far_off, int64_t* far, int64_t cap,
+                       int64_t* need);
+
+/* Proxy rings (kernels.py:263-273): pts = centre + r_p (cos, sin)(2 pi j / P),
+ * radial normals about the ring centroid (kernels.py:340-342), weights
+ * 2 pi r_p / P.  cs: P x 2 (cos, sin); pts, pn: nb x P x 2; pw: nb.          */
+int skb_host_proxies(int64_t nb, const int64_t* idx, const double* center, const double* hw,
+                     double factor, int64_t P, const double* cs, double* pts, double* pn,
+                     double* pw);
+
 #ifdef __cplusplus
 }
 #endif

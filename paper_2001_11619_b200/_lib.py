@@ -59,6 +59,14 @@ SIGNATURES = {
     "skb_psi_dot": [_i64, _vp, _vp, _vp, _i64, _vp, _i64, _i64, _vp, _i64, _f64, _vp, _i64, _vp],
     "skb_sum_partials": [_i64, _i32, _vp, _i64, _vp, _f64, _vp, _vp],
     "skb_system_matvec": [_vp, _vp, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _i64, _vp, _vp],
+    "skb_level_schur": [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                        _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "skb_level_aug": [_i64, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                      _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    # native host runtime (host arrays only, no device)
+    "skb_host_far_lists": [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _f64,
+                           _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp],
+    "skb_host_proxies": [_i64, _vp, _vp, _vp, _f64, _i64, _vp, _vp, _vp, _vp],
 }
 
 _LIB = None

@@ -207,16 +207,17 @@ struct ProfScope {
 // Side streams for running independent size classes of a batch concurrently
 // (different dynamic shared memory footprints -> different CTAs per SM).
 struct SideStreams {
+  static constexpr int kN = 8;
   bool init = false;
-  cudaStream_t st[3];
-  cudaEvent_t fork_ev, join_ev[3];
+  cudaStream_t st[kN];
+  cudaEvent_t fork_ev, join_ev[kN];
 };
 SideStreams& side();
 
 inline int side_init() {
   SideStreams& S = side();
   if (!S.init) {
-    for (int i = 0; i < 3; ++i) {
+    for (int i = 0; i < SideStreams::kN; ++i) {
       SKB_RET(cudaStreamCreateWithFlags(&S.st[i], cudaStreamNonBlocking));
       SKB_RET(cudaEventCreateWithFlags(&S.join_ev[i], cudaEventDisableTiming));
     }
@@ -226,45 +227,28 @@ inline int side_init() {
   return 0;
 }
 
-inline int fork3(cudaStream_t s) {
+// side streams 0..n-1 wait for everything enqueued on s so far
+inline int fork_n(cudaStream_t s, int n) {
   SKB_RET((cudaError_t)(-side_init()));
   SideStreams& S = side();
   SKB_RET(cudaEventRecord(S.fork_ev, s));
-  for (int i = 0; i < 3; ++i) SKB_RET(cudaStreamWaitEvent(S.st[i], S.fork_ev, 0));
+  for (int i = 0; i < n; ++i) SKB_RET(cudaStreamWaitEvent(S.st[i], S.fork_ev, 0));
   return 0;
 }
 
-inline int join3(cudaStream_t s) {
+// s waits for everything enqueued on side streams 0..n-1
+inline int join_n(cudaStream_t s, int n) {
   SideStreams& S = side();
-  for (int i = 0; i < 3; ++i) {
+  for (int i = 0; i < n; ++i) {
     SKB_RET(cudaEventRecord(S.join_ev[i], S.st[i]));
     SKB_RET(cudaStreamWaitEvent(s, S.join_ev[i], 0));
   }
   return 0;
 }
 
-inline int fork2(cudaStream_t s) {
-  SideStreams& S = side();
-  if (!S.init) {
-    for (int i = 0; i < 3; ++i) {
-      SKB_RET(cudaStreamCreateWithFlags(&S.st[i], cudaStreamNonBlocking));
-      SKB_RET(cudaEventCreateWithFlags(&S.join_ev[i], cudaEventDisableTiming));
-    }
-    SKB_RET(cudaEventCreateWithFlags(&S.fork_ev, cudaEventDisableTiming));
-    S.init = true;
-  }
-  SKB_RET(cudaEventRecord(S.fork_ev, s));
-  for (int i = 0; i < 2; ++i) SKB_RET(cudaStreamWaitEvent(S.st[i], S.fork_ev, 0));
-  return 0;
-}
-
-inline int join2(cudaStream_t s) {
-  SideStreams& S = side();
-  for (int i = 0; i < 2; ++i) {
-    SKB_RET(cudaEventRecord(S.join_ev[i], S.st[i]));
-    SKB_RET(cudaStreamWaitEvent(s, S.join_ev[i], 0));
-  }
-  return 0;
-}
+inline int fork3(cudaStream_t s) { return fork_n(s, 3); }
+inline int join3(cudaStream_t s) { return join_n(s, 3); }
+inline int fork2(cudaStream_t s) { return fork_n(s, 2); }
+inline int join2(cudaStream_t s) { return join_n(s, 2); }
 
 }  // namespace skb

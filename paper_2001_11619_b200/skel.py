@@ -110,6 +110,7 @@ class _HostTimer:
     """Host-only time per section (SKB_HOST_PROF=1; no device syncs)."""
 
     enabled = bool(os.environ.get("SKB_HOST_PROF"))
+    trace = os.environ.get("SKB_HOST_PROF") == "trace"     # record_function ranges (timeline.py)
     acc: dict = {}
 
     def __init__(self, name):
@@ -135,6 +136,8 @@ _NULL = _Null()
 
 
 def _ht(name):
+    if _HostTimer.trace:
+        return torch.profiler.record_function(name)
     return _HostTimer(name) if _HostTimer.enabled else _NULL
 
 
@@ -287,6 +290,45 @@ class ActStore:
         self.s_len[idx] = k
 
 
+
+
+def _tree_native(t: Tree) -> dict:
+    """Contiguous copies of the tree arrays the native host runtime reads
+    (built once per tree)."""
+    nv = getattr(t, "_native", None)
+    if nv is None:
+        nv = dict(center=np.ascontiguousarray(t.center, np.float64),
+                  hw=np.ascontiguousarray(t.hw, np.float64),
+                  nbr=np.ascontiguousarray(t.neighbors, np.int64),
+                  lev=np.ascontiguousarray(t.lev, np.int64),
+                  ix=np.ascontiguousarray(t.ix, np.int64),
+                  iy=np.ascontiguousarray(t.iy, np.int64),
+                  leaf=np.ascontiguousarray(t.is_leaf, np.uint8),
+                  ls=np.ascontiguousarray(t.level_start, np.int64),
+                  root=np.array([t.root_center[0], t.root_center[1], t.root_half_width]))
+        t._native = nv
+    return nv
+
+
+def _native_far_lists(ctx, idx, store):
+    nv = _tree_native(ctx.t)
+    B = len(idx)
+    off = np.zeros(B + 1, np.int64)
+    need = np.zeros(1, np.int64)
+    cap = max(getattr(ctx, "_far_cap", 0), 4096)
+    while True:
+        far = np.empty(cap, np.int64)
+        rc = _lib.load().skb_host_far_lists(
+            B, idx.ctypes.data, nv["center"].ctypes.data, nv["hw"].ctypes.data,
+            nv["nbr"].ctypes.data, nv["lev"].ctypes.data, nv["ix"].ctypes.data,
+            nv["iy"].ctypes.data, nv["leaf"].ctypes.data, nv["ls"].ctypes.data, ctx.t.depth,
+            nv["root"].ctypes.data, ctx.factor, store.big.ctypes.data, store.a_start.ctypes.data,
+            store.a_len.ctypes.data, ctx.px.ctypes.data, ctx.py.ctypes.data, off.ctypes.data,
+            far.ctypes.data, cap, need.ctypes.data)
+        if rc == 0:
+            ctx._far_cap = cap
+            return off, far[:int(need[0])]
+        cap = int(need[0]) + 1024
 
 
 class _CaptureArena:
@@ -542,7 +584,13 @@ class _Ctx:
     def far_lists(self, idx, store: "ActStore", pairs=None):
         """F_int per box (reference _Compressor.far_dofs, skel.py:258-280):
         active DOFs of the candidate sources, filtered by strict distance < r_p
-        from the box centre."""
+        from the box centre.  Native (csrc/host.cpp) unless candidate pairs are
+        given (the NumPy restatement below, kept for the host tests)."""
+        if pairs is None:
+            return _native_far_lists(self, np.asarray(idx, np.int64), store)
+        return self.far_lists_np(idx, store, pairs)
+
+    def far_lists_np(self, idx, store: "ActStore", pairs=None):
         t = self.t
         rp, pb, ps = self.far_pairs(idx) if pairs is None else pairs
         B = len(idx)
@@ -564,7 +612,18 @@ class _Ctx:
         return off, F
 
     def proxies(self, idx):
-        """Proxy rings + radial normals + weights (kernels.py:263-273, 340-342)."""
+        """Proxy rings + radial normals + weights (kernels.py:263-273, 340-342), native."""
+        idx = np.asarray(idx, np.int64)
+        nv = _tree_native(self.t)
+        B = len(idx)
+        pts = np.empty((B, self.P, 2))
+        pn = np.empty((B, self.P, 2))
+        pw = np.empty(B)
+        call("skb_host_proxies", B, idx, nv["center"], nv["hw"], self.factor, self.P,
+             np.ascontiguousarray(self.cs), pts, pn, pw)
+        return pts, pn, pw
+
+    def proxies_np(self, idx):
         rp = proxy_radius(self.t.hw[idx], self.factor)
         pts = self.t.center[idx][:, None, :] + rp[:, None, None] * self.cs[None]
         # ring centre: sequential left-to-right sum (cumsum keeps that order)
@@ -575,10 +634,9 @@ class _Ctx:
         return pts, pn, pw
 
     def prep(self, idx) -> dict:
-        """Skeleton-independent inputs of launch() for a batch (candidate far
-        pairs, proxy rings); computed while the previous level is on the GPU."""
+        """Skeleton-independent inputs of launch() for a batch (proxy rings)."""
         idx = np.asarray(idx, np.int64)
-        return dict(pairs=self.far_pairs(idx), proxies=self.proxies(idx))
+        return dict(pairs=None, proxies=self.proxies(idx))
 
     def child_desc(self, idx, store: "ActStore"):
         """Children's skeleton offsets (active order) and Xss addresses."""
@@ -619,8 +677,9 @@ class _Ctx:
         np.cumsum(sizes, out=stack_off[1:])
         dev = _dev()
         _Prof.tick("host_far_proxy")
-        stack = torch.empty(max(int(stack_off[-1]), 1), dtype=torch.float64, device=dev)
-        up = _upload(act_off=act_off, act=act if len(act) else np.zeros(1, np.int64),
+        with _ht("L.upload"):
+          stack = torch.empty(max(int(stack_off[-1]), 1), dtype=torch.float64, device=dev)
+          up = _upload(act_off=act_off, act=act if len(act) else np.zeros(1, np.int64),
                      far_off=far_off, far=far if len(far) else np.zeros(1, np.int64),
                      pts=pts.reshape(-1), pn=pn.reshape(-1), pw=pw, stack_off=stack_off[:-1])
         s = _stream()
@@ -633,6 +692,7 @@ class _Ctx:
         A = (base + 8 * stack_off[:-1]).astype(np.int64)
         pre = rows > nB
         if pre.any():
+          with _ht("L.geqrf"):
             call("skb_geqrf_batched", int(pre.sum()), np.ascontiguousarray(rows[pre]),
                  np.ascontiguousarray(nB[pre]),
                  np.ascontiguousarray(rows[pre]),
@@ -645,7 +705,8 @@ class _Ctx:
         diag_d = torch.empty(max(na, 1), dtype=torch.float64, device=dev)
         gap_d = torch.empty(max(B, 1), dtype=torch.float64, device=dev)
         lda = rows.astype(np.int64)
-        call("skb_qrcp_id_batched", B, m_q, nB, lda,
+        with _ht("L.qrcp"):
+          call("skb_qrcp_id_batched", B, m_q, nB, lda,
              A, kmin_a, self.tol, act_off, ptr(ints),
              ptr(diag_d), ptr(ints) + 4 * na, ptr(ints) + 4 * (na + B), ptr(gap_d), s)
         _Prof.tick("b_qrcp")
@@ -676,6 +737,14 @@ class _Ctx:
         bt.k[:] = ih[na:na + B]
         bt.steps[:] = ih[na + B:na + 2 * B]
         bt.gap[:] = h["gap_h"].numpy()[:B]
+        bt._launch = h
+        return bt
+
+    def layout(self, bt: BoxBatch):
+        """Factor storage of a finished batch (one slab per level); off the
+        critical path: runs after the next level's compression is launched."""
+        h = bt._launch
+        nB, B = bt.nB, len(bt.idx)
         k = bt.k
         r = nB - k
         if _lib.PROF_ON:
@@ -709,13 +778,13 @@ class _Ctx:
         ioff = np.zeros(B + 1, np.int64)
         np.cumsum(r, out=ioff[1:])
         bt.ipiv[:] = (_addr(ipiv) + 4 * ioff[:-1]).astype(np.uint64)
-        bt._launch = h
-        return bt
 
     def schur(self, bt: BoxBatch, store: "ActStore"):
         """(c) of compress_box (reference skel.py:317-338) on the level stream:
         it depends on this batch's QRCP and on the children's Xss (previous
         level, same stream), not on the next level's compression."""
+        if not bt.slabs:
+            self.layout(bt)
         h = bt.__dict__.pop("_launch")
         S = self.sstream
         S.wait_event(h["ev"])
@@ -727,67 +796,19 @@ class _Ctx:
     def _schur(self, bt, store, h):
         idx, act_off, nB, up, A, lda, perm_d = (h["idx"], h["act_off"], h["nB"], h["up"], h["A"],
                                                 h["lda"], h["perm_d"])
-        k = bt.k
-        r = nB - k
         B = len(idx)
         dev = _dev()
-        s = _stream()
-        E_off = np.zeros(B + 1, np.int64)
-        np.cumsum(nB * nB, out=E_off[1:])
-        Ebuf = torch.empty(max(int(E_off[-1]), 1), dtype=torch.float64, device=dev)
-        Xrs = torch.empty(max(int((r * k).sum()), 1), dtype=torch.float64, device=dev)
-        # ---- T: column-major in place over R12 -> row-major k x r
-        perm_ptrs = (_addr(perm_d) + 4 * act_off[:-1]).astype(np.int64)
-        call("skb_id_T_batched", B, A, lda, k.astype(np.int64), nB.astype(np.int64), perm_ptrs,
-             bt.ptr["T"].astype(np.int64), s)
-        # ---- permuted self blocks with children's Xss
         co, cx = self.child_desc(idx, store)
-        up2 = _upload(co=co.reshape(-1), cx=cx.reshape(-1), E_off=E_off[:-1], E_ld=nB.astype(np.int64))
-        call("skb_assemble_self", ptr(self.g.pos), ptr(self.g.nrm), ptr(self.g.w), ptr(self.g.kap),
-             B, ptr(up["act_off"]), ptr(up["act"]), ptr(up["act_off"]), ptr(perm_d),
-             ptr(up2["co"]), ptr(up2["cx"]), ptr(Ebuf), ptr(up2["E_off"]), ptr(up2["E_ld"]),
-             int(nB.max(initial=0)), s)
-        _Prof.tick("a_self_T")
-        E = (_addr(Ebuf) + 8 * E_off[:-1]).astype(np.uint64)
-        xoff = np.zeros(B + 1, np.int64)
-        np.cumsum(r * k, out=xoff[1:])
-        Xrs_p = (_addr(Xrs) + 8 * xoff[:-1]).astype(np.uint64)
-        Ess, Esr = E, E + (8 * k).astype(np.uint64)
-        Ers = E + (8 * k * nB).astype(np.uint64)
-        Err = Ers + (8 * k).astype(np.uint64)
-        T, Xsr, Xrr = bt.ptr["T"], bt.ptr["Xsr"], bt.ptr["Xrr"]
-        one, mone = np.ones(B), -np.ones(B)
-        # X_sr = E_SR - E_SS T ; X_rs = E_RS - T^T E_SS ; X_rr = E_RR - E_RS T   (skel.py:321-332)
-        _gemm([
-            dict(A=Ess, B=T, C=Esr, D=Xsr, m=k, n=r, k=k, lda=nB, ldb=r, ldc=nB, ldd=r,
-                 alpha=mone, beta=one),
-            dict(A=T, B=Ess, C=Ers, D=Xrs_p, m=r, n=k, k=k, lda=r, ldb=nB, ldc=nB, ldd=k,
-                 alpha=mone, beta=one, transA=1),
-            dict(A=Ers, B=T, C=Err, D=Xrr, m=r, n=r, k=k, lda=nB, ldb=r, ldc=nB, ldd=r,
-                 alpha=mone, beta=one),
-        ])
-        # X_rr -= T^T X_sr
-        _gemm([dict(A=T, B=Xsr, C=Xrr, D=Xrr, m=r, n=r, k=k, lda=r, ldb=r, ldc=r, ldd=r,
-                    alpha=mone, beta=one, transA=1)])
-        _Prof.tick("c_schur_gemm")
-        LU = bt.ptr["LU"]
-        call("skb_copy2d_batched", B, _mats(LU, r, r, r),
-             _mats(Xrr, r, r, r), 0, s)
         info_d = torch.empty(B, dtype=torch.int32, device=dev)
         ratio_d = torch.empty(B, dtype=torch.float64, device=dev)
-        call("skb_getrf_batched", B, _mats(LU, r, r, r), bt.ipiv,
-             ptr(info_d), ptr(ratio_d), s)
-        _Prof.tick("c_getrf")
-        # X_rs_div = X_rr^-1 X_rs (skel.py:333)
-        Xrsdiv = bt.ptr["Xrsdiv"]
-        call("skb_copy2d_batched", B, _mats(Xrsdiv, r, k, k),
-             _mats(Xrs_p, r, k, k), 0, s)
-        call("skb_getrs_batched", B, _mats(LU, r, r, r), bt.ipiv,
-             _mats(Xrsdiv, r, k, k), s)
-        # Xss_mod = E_SS - X_sr X_rs_div (skel.py:334)
-        _gemm([dict(A=Xsr, B=Xrsdiv, C=Ess, D=bt.ptr["Xss"], m=k, n=k, k=r, lda=r, ldb=k,
-                    ldc=nB, ldd=k, alpha=mone, beta=one)])
-        _Prof.tick("c_getrs_xss")
+        # T, self blocks, Schur GEMMs, LU(X_rr), X_rs_div, Xss_mod: one native call
+        call("skb_level_schur", B, np.ascontiguousarray(nB, np.int64), bt.k, act_off,
+             ptr(self.g.pos), ptr(self.g.nrm), ptr(self.g.w), ptr(self.g.kap), ptr(up["act_off"]),
+             ptr(up["act"]), ptr(perm_d), A, lda, np.ascontiguousarray(co.reshape(-1)),
+             np.ascontiguousarray(cx.reshape(-1)), bt.ptr["T"], bt.ptr["Xrr"], bt.ptr["LU"],
+             bt.ptr["Xsr"], bt.ptr["Xrsdiv"], bt.ptr["Xss"], bt.ipiv, ptr(info_d), ptr(ratio_d),
+             _stream())
+        _Prof.tick("c_schur")
         # X_RR pivot info for the migration rule: copied asynchronously, checked
         # after the next level's QRCP sync (no extra host sync per level)
         info_h = torch.empty(B, dtype=torch.int32, pin_memory=True)
@@ -798,7 +819,6 @@ class _Ctx:
         ev.record()
         IO["d2h"] += 12 * B
         bt._pending = (info_h, ratio_h, ev)
-        del Ebuf, Xrs
 
     def compress(self, idx, store: "ActStore", kmin=None) -> BoxBatch:
         """Compress a batch of same-level boxes (reference compress_box, skel.py:293-338)."""
@@ -1382,80 +1402,12 @@ def _finish_top(ctx: _Ctx, levels, store, pipe: "_AugPipe"):
 
 
 def _aug_level(L: LevelFactors, UH, PsiV, UH_div, schur, q):
-    """U sweep on H and V^T sweep on Psi for one level (skel.py:384-396)."""
-    B = len(L.k)
-    k, r, c = L.k, L.r, L.ncols
-    dev = UH.device
-    s = _stream()
-
-    def offs(sz):
-        o = np.zeros(B + 1, np.int64)
-        np.cumsum(sz, out=o[1:])
-        return o
-
-    oS, oR, oPS, oPR, oSp = offs(k * q), offs(r * q), offs(k * c), offs(r * c), offs(c * q)
-    buf = torch.empty(max(int(oS[-1] + 2 * oR[-1] + oPS[-1] + oPR[-1] + oSp[-1]), 1),
-                      dtype=torch.float64, device=dev)
-    base = _addr(buf)
-    b0 = 0
-    addr = {}
-    for name, o in (("Us", oS), ("Ur", oR), ("w", oR), ("Ps", oPS), ("Pr", oPR), ("Sp", oSp)):
-        addr[name] = (base + 8 * (b0 + o[:-1])).astype(np.uint64)
-        addr[name + "_off"] = b0 + o[:-1]
-        b0 += int(o[-1])
-    up = _upload(Us=addr["Us_off"], Ur=addr["Ur_off"], w=addr["w_off"], Ps=addr["Ps_off"],
-                 Pr=addr["Pr_off"], ldq=np.full(B, q, np.int64), ldc=c.astype(np.int64))
+    """U sweep on H and V^T sweep on Psi for one level (skel.py:384-396), one native call."""
     d = L.d
-    mk, mr, mc = int(k.max(initial=0)), int(r.max(initial=0)), int(c.max(initial=0))
-    call("skb_gather_rows", B, ptr(d["sd_off"]), ptr(d["sd"]), None, None, q, ptr(UH), q,
-         base, ptr(up["Us"]), ptr(up["ldq"]), mk, q, s)
-    call("skb_gather_rows", B, ptr(d["rd_off"]), ptr(d["rd"]), None, None, q, ptr(UH), q,
-         base, ptr(up["Ur"]), ptr(up["ldq"]), mr, q, s)
-    if mc:
-        call("skb_gather_rows", B, ptr(d["sd_off"]), ptr(d["sd"]), ptr(d["c_off"]), ptr(d["c"]), 0,
-             ptr(PsiV), q, base, ptr(up["Ps"]), ptr(up["ldc"]), mk, mc, s)
-        call("skb_gather_rows", B, ptr(d["rd_off"]), ptr(d["rd"]), ptr(d["c_off"]), ptr(d["c"]), 0,
-             ptr(PsiV), q, base, ptr(up["Pr"]), ptr(up["ldc"]), mr, mc, s)
-    one, mone, zero = np.ones(B), -np.ones(B), np.zeros(B)
-    qq = np.full(B, q)
-    T = L.P["T"]
-    _gemm([dict(A=T, B=addr["Us"], C=addr["Ur"], D=addr["Ur"], m=r, n=qq, k=k, lda=r, ldb=qq,
-                ldc=qq, ldd=qq, alpha=mone, beta=one, transA=1),
-           dict(A=T, B=addr["Ps"], C=addr["Pr"], D=addr["Pr"], m=r, n=c, k=k, lda=r, ldb=c,
-                ldc=c, ldd=c, alpha=mone, beta=one, transA=1)])
-    call("skb_copy2d_batched", B, _mats(addr["w"], r, qq, qq),
-         _mats(addr["Ur"], r, qq, qq), 0, s)
-    call("skb_getrs_batched", B, _mats(L.P["LU"], r, r, r), L.ipiv,
-         _mats(addr["w"], r, qq, qq), s)
-    _gemm([dict(A=L.P["Xsr"], B=addr["w"], C=addr["Us"], D=addr["Us"], m=k, n=qq, k=r, lda=r,
-                ldb=qq, ldc=qq, ldd=qq, alpha=mone, beta=one),
-           dict(A=L.P["Xrsdiv"], B=addr["Pr"], C=addr["Ps"], D=addr["Ps"], m=k, n=c, k=r, lda=k,
-                ldb=c, ldc=c, ldd=c, alpha=mone, beta=one, transA=1),
-           dict(A=addr["Pr"], B=addr["w"], D=addr["Sp"], m=c, n=qq, k=r, lda=c, ldb=qq, ldd=qq,
-                alpha=one, beta=zero, transA=1)])
-    call("skb_scatter_rows", B, ptr(d["rd_off"]), ptr(d["rd"]), None, None, q, base, ptr(up["Ur"]),
-         ptr(up["ldq"]), ptr(UH), q, 0, 1.0, mr, q, s)
-    call("skb_scatter_rows", B, ptr(d["sd_off"]), ptr(d["sd"]), None, None, q, base, ptr(up["Us"]),
-         ptr(up["ldq"]), ptr(UH), q, 0, 1.0, mk, q, s)
-    call("skb_scatter_rows", B, ptr(d["rd_off"]), ptr(d["rd"]), None, None, q, base, ptr(up["w"]),
-         ptr(up["ldq"]), ptr(UH_div), q, 0, 1.0, mr, q, s)
-    if mc:
-        call("skb_scatter_rows", B, ptr(d["rd_off"]), ptr(d["rd"]), ptr(d["c_off"]), ptr(d["c"]), 0,
-             base, ptr(up["Pr"]), ptr(up["ldc"]), ptr(PsiV), q, 0, 1.0, mr, mc, s)
-        call("skb_scatter_rows", B, ptr(d["sd_off"]), ptr(d["sd"]), ptr(d["c_off"]), ptr(d["c"]), 0,
-             base, ptr(up["Ps"]), ptr(up["ldc"]), ptr(PsiV), q, 0, 1.0, mk, mc, s)
-        # deterministic schur accumulation in box order
-        rows = L.cols
-        owner = np.repeat(np.arange(B), c)
-        local = np.arange(len(rows)) - np.repeat(L.cols_off[:-1], c)
-        contrib = addr["Sp_off"][owner] + local * q
-        order = np.argsort(rows, kind="stable")
-        row_off = np.zeros(q + 1, np.int64)
-        np.cumsum(np.bincount(rows, minlength=q), out=row_off[1:])
-        up3 = _upload(ro=row_off, ct=contrib[order].astype(np.int64))
-        call("skb_schur_accumulate", q, ptr(up3["ro"]), ptr(up3["ct"]), base, ptr(schur), s)
-    # buf/up are released here: the caching allocator is stream-ordered, so the
-    # memory is reused only after the kernels above have run
+    call("skb_level_aug", len(L.k), L.k, L.r, q, L.cols_off,
+         L.cols if len(L.cols) else np.zeros(1, np.int64), ptr(d["sd_off"]), ptr(d["sd"]),
+         ptr(d["rd_off"]), ptr(d["rd"]), ptr(d["c_off"]), ptr(d["c"]), L.P["T"], L.P["LU"],
+         L.P["Xsr"], L.P["Xrsdiv"], L.ipiv, ptr(UH), ptr(PsiV), ptr(UH_div), ptr(schur), _stream())
 
 
 def _run_levels(ctx: _Ctx, reuse=None, dirty=None):
@@ -1516,21 +1468,25 @@ def _run_levels(ctx: _Ctx, reuse=None, dirty=None):
             bt_new = ctx.finish(h) if h is not None else None
         # the previous level's X_RR pivot ratios are available now (its kernels
         # ran before this sync); a migration there invalidates this level
-        if prev is not None and prev[2] is not None and ctx.migrate(prev[2], store):
+        with _ht("migrate"):
+            mig = prev is not None and prev[2] is not None and ctx.migrate(prev[2], store)
+        if mig:
             prev = fix_prev()
             cur = go(p_cur)                   # redo this level on the corrected skeletons
             continue
-        if prev is not None:
-            with _ht("aug_submit"):
-                pipe.submit(levels[-1])       # previous level final: start its aug sweep
         n_recomp += len(todo)
+        if reuse is not None and bt_new is not None:
+            ctx.layout(bt_new)                # merge copies the factor pointers
         bt = bt_new if reuse is None else _merge_level(ctx, idx, store, todo, bt_new, reuse)
         store.set_skel(bt.idx, bt.act_off, bt.act, bt.perm, bt.k)
-        store.xss[bt.idx] = bt.ptr["Xss"]
         nxt = go(p_nxt) if lev > 1 else None          # critical path first
         if bt_new is not None:
             with _ht("schur"):
                 ctx.schur(bt_new, store)
+        store.xss[bt.idx] = bt.ptr["Xss"]             # laid out by schur()
+        if prev is not None:
+            with _ht("aug_submit"):
+                pipe.submit(levels[-1])       # previous level final: start its aug sweep
         if _Prof.enabled:
             torch.cuda.synchronize()
             _Prof.acc[f"level{lev}"] = time.perf_counter() - _Prof._lt

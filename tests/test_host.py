@@ -82,3 +82,28 @@ def test_cfg4_dirty_sets_match_oracle():
         ref = O.dirty_set(ot, ot2, nb, rep, wl.proxy_factor)
         assert mine == ref
         t, ot = t2, ot2
+
+
+def test_native_far_lists_and_proxies_match_numpy():
+    """Native host runtime (csrc/host.cpp) == the NumPy restatement, bitwise,
+    on every level of cfg2 with synthetic (seeded random) skeletons."""
+    wl = configs.cfg2()
+    b = wl.boundary
+    t = build_tree(b.positions, wl.leaf_cap)
+    rng = np.random.default_rng(7)
+    store = skel.ActStore(t)
+    for lev in range(t.depth, 0, -1):
+        idx = t.level_indices(lev)
+        store.set_internal(t, idx)
+        act_off, act = store.acts(idx)
+        k = np.array([rng.integers(0, n + 1) for n in np.diff(act_off)], np.int64)
+        perm = np.concatenate([rng.permutation(n) for n in np.diff(act_off)]).astype(np.int32)
+        store.set_skel(idx, act_off, act, perm, k)
+    ctx = skel._Ctx(skel.SystemSpec(), b, t, wl.tol, wl.proxy_count, wl.proxy_factor)
+    for lev in range(t.depth, 0, -1):
+        idx = t.level_indices(lev)
+        off, F = ctx.far_lists(idx, store)
+        off2, F2 = ctx.far_lists_np(idx, store)
+        assert np.array_equal(off, off2) and np.array_equal(F, F2)
+        for a, a2 in zip(ctx.proxies(idx), ctx.proxies_np(idx)):
+            assert np.array_equal(a, a2)
