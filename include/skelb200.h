@@ -280,6 +280,10 @@ int skb_level_aug(int64_t nbox, const int64_t* k, const int64_t* r, int64_t q,
  * keys), lev/ix/iy, is_leaf (uint8), level_start (depth + 2);
  * root = {cx, cy, half width}.                                               */
 
+/* Host allocator tuning (called once at load): large freed blocks stay in the
+ * heap instead of being unmapped, so per-level host arrays do not page-fault. */
+int skb_host_init(void);
+
 /* F_int of each box idx[b] (reference _Compressor.far_dofs, skel.py:258-280 with
  * Tree.colleagues tree.py:70-81, Tree.shallow_leaves_near tree.py:83-99 and
  * proxy_radius tree.py:158-160): active DOFs (segments big[a_start[j]..+a_len[j]])
@@ -300,6 +304,34 @@ int skb_host_far_lists(int64_t nb, const int64_t* idx, const double* center, con
 int skb_host_proxies(int64_t nb, const int64_t* idx, const double* center, const double* hw,
                      double factor, int64_t P, const double* cs, double* pts, double* pn,
                      double* pw);
+
+/* Adaptive quadtree (reference build_tree, tree.py:110-155): root {cx, cy,
+ * half width}; split while a box holds more than leaf_cap nodes (depth <
+ * max_depth), east = x >= cx, north = y >= cy, empty children pruned, boxes of
+ * a level sorted by key.  Returns an opaque handle; skb_tree_sizes gives
+ * {nbox, depth, level-node entries}; skb_tree_export copies the flat arrays
+ * (tree.py layout: children nbox x 4 compacted in SW, SE, NW, NE order,
+ * neighbours nbox x 8, level_nodes concatenated with level_nodes_off,
+ * node_leaf N); skb_tree_free releases the handle.                          */
+int skb_tree_build(const double* pos, int64_t N, int64_t leaf_cap, int64_t max_depth,
+                   const double* root, int64_t* handle);
+int skb_tree_sizes(int64_t handle, int64_t* sizes);
+int skb_tree_export(int64_t handle, int64_t* level_start, int64_t* lev, int64_t* ix, int64_t* iy,
+                    int64_t* parent, double* center, double* hw, int64_t* children,
+                    int64_t* nchild, int64_t* node_start, int64_t* node_cnt, int64_t* level_nodes,
+                    int64_t* level_nodes_off, int64_t* nbr, int64_t* node_leaf);
+int skb_tree_free(int64_t handle);
+
+/* Dirty boxes of a local update (reference update skel.py:476-491 with
+ * ownership_changed tree.py:251-270, _mark_disc_hits tree.py:215-236 and
+ * _dirty_closure skel.py:517-534).  Trees passed as 11 flat arrays {level_start,
+ * lev, ix, iy, parent, node_start, node_cnt, level_nodes, level_nodes_off,
+ * neighbours, node_leaf}; pts: moved positions (old and new, npts x 2);
+ * mod_new: moved nodes (new numbering).  out_mask: new-tree boxes.          */
+int skb_dirty_set(const int64_t* const* new_arrays, const double* new_center, int64_t new_depth,
+                  const int64_t* const* old_arrays, int64_t old_depth, const double* root,
+                  const int64_t* old_to_new, const double* pts, int64_t npts,
+                  const int64_t* mod_new, int64_t nmod, double proxy_factor, uint8_t* out_mask);
 
 #ifdef __cplusplus
 }

@@ -67,6 +67,12 @@ SIGNATURES = {
     "skb_host_far_lists": [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _f64,
                            _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp],
     "skb_host_proxies": [_i64, _vp, _vp, _vp, _f64, _i64, _vp, _vp, _vp, _vp],
+    "skb_host_init": [],
+    "skb_tree_build": [_vp, _i64, _i64, _i64, _vp, _vp],
+    "skb_tree_sizes": [_i64, _vp],
+    "skb_tree_export": [_i64] + [_vp] * 15,
+    "skb_tree_free": [_i64],
+    "skb_dirty_set": [_vp, _vp, _i64, _vp, _i64, _vp, _vp, _vp, _i64, _vp, _i64, _f64, _vp],
 }
 
 _LIB = None
@@ -88,6 +94,7 @@ def load(path: str = LIB_PATH):
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = ctypes.c_int
+    lib.skb_host_init()
     _LIB = lib
     return lib
 

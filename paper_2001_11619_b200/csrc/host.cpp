@@ -8,6 +8,7 @@
 // level by level, keys (lev, ix, iy) sorted within a level, children in
 // SW, SE, NW, NE order, neighbours (nbox x 8) in sorted key order.
 
+#include <malloc.h>
 #include <math.h>
 #include <stdint.h>
 #include <string.h>
@@ -80,6 +81,20 @@ void coarse_leaves(const TreeView& t, int64_t L, double cx, double cy, double r,
 
 extern "C" {
 
+// Host allocator tuning for the level pipeline: per-level descriptor arrays
+// (host vectors, NumPy buffers) of 0.1-10 MB are allocated and freed at every
+// level; keeping freed blocks in the heap avoids an mmap/munmap + page-fault
+// cycle per allocation (the dominant host cost of a native tree build).
+int skb_host_init(void) {
+  static bool done = false;
+  if (!done) {
+    mallopt(M_MMAP_THRESHOLD, 256 << 20);
+    mallopt(M_TRIM_THRESHOLD, 512 << 20);
+    done = true;
+  }
+  return 0;
+}
+
 int skb_host_far_lists(int64_t nb, const int64_t* idx, const double* center, const double* hw,
                        const int64_t* nbr, const int64_t* lev, const int64_t* ix,
                        const int64_t* iy, const uint8_t* is_leaf, const int64_t* level_start,
@@ -147,6 +162,314 @@ int skb_host_proxies(int64_t nb, const int64_t* idx, const double* center, const
     }
     pw[b] = two_pi * rp / (double)P;
   }
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Quadtree build (reference build_tree, tree.py:110-155; same rules as the
+// NumPy restatement tree.build_tree): split while a box holds more than
+// leaf_cap nodes, east = x >= cx, north = y >= cy, empty children pruned,
+// boxes of a level sorted by key, nodes of a child in their parent order.
+// ---------------------------------------------------------------------------
+struct NativeTree {
+  int64_t n_nodes = 0, nbox = 0, depth = 0;
+  std::vector<int64_t> level_start, lev, ix, iy, parent, children, nchild, node_start, node_cnt;
+  std::vector<int64_t> level_nodes, level_nodes_off, nbr, node_leaf;
+  std::vector<double> center, hw;
+};
+
+int skb_tree_build(const double* pos, int64_t N, int64_t leaf_cap, int64_t max_depth,
+                   const double* root, int64_t* handle) {
+  NativeTree* T = new NativeTree();
+  T->n_nodes = N;
+  // level 0
+  std::vector<int64_t> nxt_ix{0}, nxt_iy{0}, nxt_par{-1}, nxt_cnt{N}, nxt_nodes(N);
+  std::vector<double> nxt_cx{root[0]}, nxt_cy{root[1]}, nxt_half{root[2]};
+  for (int64_t i = 0; i < N; ++i) nxt_nodes[i] = i;
+  int64_t l = 0;
+  std::vector<std::vector<int64_t>> L_children;   // per level, nb x 4 (local child idx, by quadrant)
+  struct Lv { std::vector<int64_t> ix, iy, par, cnt, nodes; std::vector<double> cx, cy, half; };
+  std::vector<Lv> levels;
+  levels.reserve(64);
+  while (true) {
+    const int64_t nb = (int64_t)nxt_ix.size();
+    levels.push_back(Lv{std::move(nxt_ix), std::move(nxt_iy), std::move(nxt_par),
+                        std::move(nxt_cnt), std::move(nxt_nodes), std::move(nxt_cx),
+                        std::move(nxt_cy), std::move(nxt_half)});
+    const Lv& cur = levels.back();
+    const auto& ix = cur.ix; const auto& iy = cur.iy; const auto& cnt = cur.cnt;
+    const auto& nodes = cur.nodes; const auto& cx = cur.cx; const auto& cy = cur.cy;
+    const auto& half = cur.half;
+    std::vector<int64_t> ch(4 * nb, -1);
+    std::vector<int64_t> start(nb + 1, 0);
+    for (int64_t b = 0; b < nb; ++b) start[b + 1] = start[b] + cnt[b];
+    bool any = false;
+    for (int64_t b = 0; b < nb; ++b) any |= (cnt[b] > leaf_cap) && (l < max_depth);
+    if (!any) { L_children.push_back(ch); break; }
+    // children of all split boxes, keyed by code = cix * side + ciy; nodes of
+    // a child keep their order in the parent (counting sort per quadrant)
+    const int64_t side = (int64_t)1 << (l + 1);
+    std::vector<int64_t> quad(nodes.size());
+    std::vector<int64_t> qcnt(4 * nb, 0);
+    for (int64_t b = 0; b < nb; ++b) {
+      if (!((cnt[b] > leaf_cap) && (l < max_depth))) continue;
+      for (int64_t t = start[b]; t < start[b + 1]; ++t) {
+        const int64_t nd = nodes[t];
+        const int64_t dx = pos[2 * nd] >= cx[b] ? 1 : 0;
+        const int64_t dy = pos[2 * nd + 1] >= cy[b] ? 1 : 0;
+        quad[t] = dx + 2 * dy;
+        qcnt[4 * b + quad[t]]++;
+      }
+    }
+    struct Kid { int64_t code, b, q; };
+    std::vector<Kid> kids;
+    for (int64_t b = 0; b < nb; ++b)
+      for (int64_t q = 0; q < 4; ++q)
+        if (qcnt[4 * b + q] > 0)
+          kids.push_back(Kid{(2 * ix[b] + (q & 1)) * side + (2 * iy[b] + (q >> 1)), b, q});
+    std::sort(kids.begin(), kids.end(), [](const Kid& a, const Kid& b) { return a.code < b.code; });
+    const size_t nk = kids.size();
+    std::vector<int64_t> nix(nk), niy(nk), npar(nk), ncnt(nk), kstart(nk + 1, 0);
+    std::vector<double> ncx(nk), ncy(nk), nhalf(nk);
+    std::vector<int64_t> slot(4 * nb, -1);
+    for (size_t c = 0; c < nk; ++c) {
+      const int64_t b = kids[c].b, q = kids[c].q, dx = q & 1, dy = q >> 1;
+      ch[4 * b + q] = (int64_t)c;
+      slot[4 * b + q] = (int64_t)c;
+      nix[c] = 2 * ix[b] + dx;
+      niy[c] = 2 * iy[b] + dy;
+      npar[c] = b;
+      ncnt[c] = qcnt[4 * b + q];
+      kstart[c + 1] = kstart[c] + ncnt[c];
+      ncx[c] = cx[b] + ((double)dx - 0.5) * half[b];
+      ncy[c] = cy[b] + ((double)dy - 0.5) * half[b];
+      nhalf[c] = half[b] / 2;
+    }
+    std::vector<int64_t> nnodes(kstart[nk]);
+    std::vector<int64_t> fillp(kstart.begin(), kstart.end() - 1);
+    for (int64_t b = 0; b < nb; ++b) {
+      if (!((cnt[b] > leaf_cap) && (l < max_depth))) continue;
+      for (int64_t t = start[b]; t < start[b + 1]; ++t) nnodes[fillp[slot[4 * b + quad[t]]]++] = nodes[t];
+    }
+    L_children.push_back(ch);
+    nxt_ix.swap(nix); nxt_iy.swap(niy); nxt_par.swap(npar); nxt_cnt.swap(ncnt);
+    nxt_nodes.swap(nnodes); nxt_cx.swap(ncx); nxt_cy.swap(ncy); nxt_half.swap(nhalf);
+    ++l;
+  }
+  T->depth = l;
+  const int64_t nlev = l + 1;
+  T->level_start.assign(nlev + 1, 0);
+  for (int64_t q = 0; q < nlev; ++q) T->level_start[q + 1] = T->level_start[q] + (int64_t)levels[q].ix.size();
+  const int64_t nbox = T->level_start[nlev];
+  T->nbox = nbox;
+  T->lev.resize(nbox); T->ix.resize(nbox); T->iy.resize(nbox); T->parent.resize(nbox);
+  T->center.resize(2 * nbox); T->hw.resize(nbox); T->children.assign(4 * nbox, -1);
+  T->nchild.assign(nbox, 0); T->node_start.resize(nbox); T->node_cnt.resize(nbox);
+  T->level_nodes_off.assign(nlev + 1, 0);
+  for (int64_t q = 0; q < nlev; ++q) {
+    const Lv& L = levels[q];
+    const int64_t base = T->level_start[q];
+    int64_t st = 0;
+    for (size_t b = 0; b < L.ix.size(); ++b) {
+      const int64_t g = base + (int64_t)b;
+      T->lev[g] = q; T->ix[g] = L.ix[b]; T->iy[g] = L.iy[b];
+      T->parent[g] = L.par[b] >= 0 ? L.par[b] + T->level_start[q > 0 ? q - 1 : 0] : -1;
+      T->center[2 * g] = L.cx[b]; T->center[2 * g + 1] = L.cy[b]; T->hw[g] = L.half[b];
+      T->node_start[g] = st; T->node_cnt[g] = L.cnt[b]; st += L.cnt[b];
+      int nc = 0;
+      for (int qd = 0; qd < 4; ++qd) {
+        const int64_t c = L_children[q][4 * b + qd];
+        if (c >= 0) T->children[4 * g + nc++] = c + T->level_start[q + 1];
+      }
+      T->nchild[g] = nc;
+    }
+    T->level_nodes_off[q + 1] = T->level_nodes_off[q] + (int64_t)L.nodes.size();
+    T->level_nodes.insert(T->level_nodes.end(), L.nodes.begin(), L.nodes.end());
+  }
+  // same-level neighbours in sorted key order (tree.py:70-81)
+  T->nbr.assign(8 * nbox, -1);
+  TreeView tv{T->center.data(), T->hw.data(), nullptr, T->lev.data(), T->ix.data(), T->iy.data(),
+              nullptr, T->level_start.data(), T->depth, root[0], root[1], root[2]};
+  for (int64_t g = 0; g < nbox; ++g) {
+    const int64_t q = T->lev[g], side = (int64_t)1 << q;
+    int s = 0;
+    for (int dx = -1; dx <= 1; ++dx)
+      for (int dy = -1; dy <= 1; ++dy) {
+        if (!dx && !dy) continue;
+        const int64_t nx = T->ix[g] + dx, ny = T->iy[g] + dy;
+        if (nx >= 0 && ny >= 0 && nx < side && ny < side) T->nbr[8 * g + s] = find_code(tv, q, nx * side + ny);
+        ++s;
+      }
+  }
+  T->node_leaf.assign(N, -1);
+  for (int64_t g = 0; g < nbox; ++g)
+    if (T->nchild[g] == 0) {
+      const int64_t* nd = T->level_nodes.data() + T->level_nodes_off[T->lev[g]] + T->node_start[g];
+      for (int64_t t = 0; t < T->node_cnt[g]; ++t) T->node_leaf[nd[t]] = g;
+    }
+  *handle = (int64_t)T;
+  return 0;
+}
+
+// sizes: {nbox, depth, total level-node entries}
+int skb_tree_sizes(int64_t handle, int64_t* sizes) {
+  const NativeTree* T = (const NativeTree*)handle;
+  sizes[0] = T->nbox; sizes[1] = T->depth; sizes[2] = (int64_t)T->level_nodes.size();
+  return 0;
+}
+
+int skb_tree_export(int64_t handle, int64_t* level_start, int64_t* lev, int64_t* ix, int64_t* iy,
+                    int64_t* parent, double* center, double* hw, int64_t* children,
+                    int64_t* nchild, int64_t* node_start, int64_t* node_cnt, int64_t* level_nodes,
+                    int64_t* level_nodes_off, int64_t* nbr, int64_t* node_leaf) {
+  const NativeTree* T = (const NativeTree*)handle;
+  auto cp = [](int64_t* d, const std::vector<int64_t>& v) { memcpy(d, v.data(), v.size() * 8); };
+  cp(level_start, T->level_start); cp(lev, T->lev); cp(ix, T->ix); cp(iy, T->iy);
+  cp(parent, T->parent); cp(children, T->children); cp(nchild, T->nchild);
+  cp(node_start, T->node_start); cp(node_cnt, T->node_cnt); cp(level_nodes, T->level_nodes);
+  cp(level_nodes_off, T->level_nodes_off); cp(nbr, T->nbr); cp(node_leaf, T->node_leaf);
+  memcpy(center, T->center.data(), T->center.size() * 8);
+  memcpy(hw, T->hw.data(), T->hw.size() * 8);
+  return 0;
+}
+
+int skb_tree_free(int64_t handle) {
+  delete (NativeTree*)handle;
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Dirty set of an update (reference skel.py:476-491, 517-534; tree.py:215-270;
+// same rules as tree.dirty_set): ownership changes, proxy discs holding an
+// old/new moved position, ancestors of the moved nodes' new leaves, closed
+// under parents + colleagues.  Trees as flat arrays (tree.py layout);
+// out_mask: new-tree boxes (uint8).
+// ---------------------------------------------------------------------------
+struct FlatTree {
+  const int64_t *level_start, *lev, *ix, *iy, *parent, *node_start, *node_cnt, *level_nodes,
+      *level_nodes_off, *nbr, *node_leaf;
+  const double* center;
+  int64_t depth;
+  double root_cx, root_cy, root_hw;
+};
+
+static int64_t flat_find(const FlatTree& t, int64_t lp, int64_t code) {
+  if (lp > t.depth) return -1;
+  int64_t lo = t.level_start[lp], hi = t.level_start[lp + 1];
+  const int64_t side = (int64_t)1 << lp;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    const int64_t c = t.ix[mid] * side + t.iy[mid];
+    if (c < code) lo = mid + 1;
+    else hi = mid;
+  }
+  if (lo < t.level_start[lp + 1] && t.ix[lo] * side + t.iy[lo] == code) return lo;
+  return -1;
+}
+
+static FlatTree flat(const int64_t* const* a, const double* center, int64_t depth, const double* root) {
+  return FlatTree{a[0], a[1], a[2], a[3], a[4], a[5], a[6], a[7], a[8], a[9], a[10],
+                  center, depth, root[0], root[1], root[2]};
+}
+
+// arrays: {level_start, lev, ix, iy, parent, node_start, node_cnt, level_nodes,
+//          level_nodes_off, nbr, node_leaf}
+int skb_dirty_set(const int64_t* const* new_arrays, const double* new_center, int64_t new_depth,
+                  const int64_t* const* old_arrays, int64_t old_depth, const double* root,
+                  const int64_t* old_to_new, const double* pts, int64_t npts,
+                  const int64_t* mod_new, int64_t nmod, double proxy_factor, uint8_t* out_mask) {
+  const FlatTree tn = flat(new_arrays, new_center, new_depth, root);
+  const FlatTree to = flat(old_arrays, nullptr, old_depth, root);
+  const int64_t nbn = tn.level_start[new_depth + 1];
+  std::vector<uint8_t> content(nbn, 0);
+  // ownership changes (tree.py:251-270)
+  for (int64_t l = 0; l <= std::max(new_depth, old_depth); ++l) {
+    const int64_t side = (int64_t)1 << l;
+    if (l <= new_depth)
+      for (int64_t g = tn.level_start[l]; g < tn.level_start[l + 1]; ++g) {
+        const int64_t o = flat_find(to, l, tn.ix[g] * side + tn.iy[g]);
+        if (o < 0 || tn.node_cnt[g] != to.node_cnt[o]) { content[g] = 1; continue; }
+        const int64_t* nn = tn.level_nodes + tn.level_nodes_off[l] + tn.node_start[g];
+        const int64_t* oo = to.level_nodes + to.level_nodes_off[l] + to.node_start[o];
+        for (int64_t t = 0; t < tn.node_cnt[g]; ++t)
+          if (nn[t] != old_to_new[oo[t]]) { content[g] = 1; break; }
+      }
+    if (l <= old_depth)
+      for (int64_t o = to.level_start[l]; o < to.level_start[l + 1]; ++o) {
+        if (flat_find(tn, l, to.ix[o] * side + to.iy[o]) >= 0) continue;
+        int64_t p = o;                 // vanished: nearest surviving ancestor changed
+        while (p >= 0) {
+          const int64_t lp = to.lev[p], sp = (int64_t)1 << lp;
+          const int64_t g = flat_find(tn, lp, to.ix[p] * sp + to.iy[p]);
+          if (g >= 0) { content[g] = 1; break; }
+          p = to.parent[p];
+        }
+      }
+  }
+  // proxy discs holding a moved position (tree.py:215-236)
+  if (npts > 0) {
+    const double ox = tn.root_cx - tn.root_hw, oy = tn.root_cy - tn.root_hw;
+    std::vector<int64_t> cand;
+    for (int64_t l = 0; l <= new_depth; ++l) {
+      if (tn.level_start[l + 1] == tn.level_start[l]) continue;
+      const double hw = tn.root_hw / (double)((int64_t)1 << l);
+      const double rad = proxy_factor * hw * sqrt(2.0);
+      const double step = 2 * hw;
+      const int64_t reach = (int64_t)ceil(rad / step) + 1, side = (int64_t)1 << l;
+      std::vector<int64_t> cells(npts);
+      const int64_t W = side + 2 * reach + 2;
+      for (int64_t i = 0; i < npts; ++i)
+        cells[i] = (int64_t)floor((pts[2 * i] - ox) / step) * W + (int64_t)floor((pts[2 * i + 1] - oy) / step);
+      std::sort(cells.begin(), cells.end());
+      cells.erase(std::unique(cells.begin(), cells.end()), cells.end());
+      cand.clear();
+      for (int64_t uc : cells) {
+        // floor division matching numpy's // for negative codes
+        int64_t cxl = uc / W, cyl = uc - cxl * W;
+        if (cyl < 0) { cxl -= 1; cyl += W; }
+        for (int64_t dx = -reach; dx <= reach; ++dx)
+          for (int64_t dy = -reach; dy <= reach; ++dy) {
+            const int64_t nx = cxl + dx, ny = cyl + dy;
+            if (nx < 0 || ny < 0 || nx >= side || ny >= side) continue;
+            const int64_t g = flat_find(tn, l, nx * side + ny);
+            if (g >= 0) cand.push_back(g);
+          }
+      }
+      std::sort(cand.begin(), cand.end());
+      cand.erase(std::unique(cand.begin(), cand.end()), cand.end());
+      const double r2 = rad * rad;
+      for (int64_t g : cand) {
+        if (content[g]) continue;
+        const double bx = tn.center[2 * g], by = tn.center[2 * g + 1];
+        for (int64_t i = 0; i < npts; ++i) {
+          const double dx = pts[2 * i] - bx, dy = pts[2 * i + 1] - by;
+          if (dx * dx + dy * dy <= r2) { content[g] = 1; break; }
+        }
+      }
+    }
+  }
+  // ancestors of the moved nodes' new leaves (skel.py:486-490)
+  for (int64_t t = 0; t < nmod; ++t) {
+    int64_t i = tn.node_leaf[mod_new[t]];
+    while (i >= 0 && !content[i]) { content[i] = 1; i = tn.parent[i]; }
+  }
+  // closure under parents + colleagues, bottom-up (skel.py:517-534)
+  std::vector<uint8_t> marked(content);
+  for (int64_t l = new_depth; l >= 0; --l) {
+    std::vector<int64_t> grew;
+    for (int64_t g = tn.level_start[l]; g < tn.level_start[l + 1]; ++g)
+      if (marked[g]) grew.push_back(g);
+    if (l + 1 <= new_depth)
+      for (int64_t g = tn.level_start[l + 1]; g < tn.level_start[l + 2]; ++g)
+        if (marked[g] && tn.parent[g] >= 0 && !marked[tn.parent[g]]) {
+          marked[tn.parent[g]] = 1;
+          grew.push_back(tn.parent[g]);
+        }
+    for (int64_t g : grew)
+      for (int s = 0; s < 8; ++s)
+        if (tn.nbr[8 * g + s] >= 0) marked[tn.nbr[8 * g + s]] = 1;
+  }
+  memcpy(out_mask, marked.data(), nbn);
   return 0;
 }
 

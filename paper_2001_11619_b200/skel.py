@@ -33,7 +33,7 @@ import torch
 
 from . import _lib
 from ._lib import GEMM_DT, MAT_DT, call, ptr
-from .tree import Tree, build_tree, dirty_set, proxy_radius, refit_tree
+from .tree import Tree, build_tree, dirty_mask, proxy_radius, refit_tree
 
 PIVOT_RATIO_FLOOR = 1e-12          # skel.py:46
 DEFAULT_PROXY_COUNT = 64           # skel.py:47
@@ -518,12 +518,18 @@ class LevelFactors:
     """All boxes of one tree level (sorted keys) with device CSR lists of
     skeleton/redundant DOFs for the gathers of the sweeps."""
 
+    @property
+    def keys(self):
+        ks = self.__dict__.get("_keys")
+        if ks is None:
+            ks = self.__dict__["_keys"] = [self.tree.key(i) for i in self.idx]
+        return ks
+
     def __init__(self, lev, tree, batch: BoxBatch, cols_off, cols):
         self.lev = lev
         self.tree = tree
         self.batch = batch
         self.idx = batch.idx
-        self.keys = [tree.key(i) for i in self.idx]
         self.k = batch.k.copy()
         self.r = batch.r.copy()
         self.sd_off, self.sd = batch.skel_csr()
@@ -1437,7 +1443,7 @@ def _run_levels(ctx: _Ctx, reuse=None, dirty=None):
         if reuse is None:
             todo = idx
         else:
-            todo = idx[np.fromiter((t.key(i) in dirty for i in idx), bool, len(idx))]
+            todo = idx[dirty[idx]]                 # dirty: mask over the tree's boxes
         with _ht("prep"):
             return idx, todo, (ctx.prep(todo) if len(todo) else None)
 
@@ -1576,14 +1582,14 @@ def update(fct: Factorization, b_new, report, workers: int = 1) -> Factorization
         t_new = refit_tree(fct.tree, b_new.positions)
     except ValueError as e:
         raise RootBoxExceededError("perturbed node escaped the root box; refactor with a fresh tree") from e
-    dirty = dirty_set(fct.tree, t_new, b_new, report, fct.proxy_factor)
+    dmask = dirty_mask(fct.tree, t_new, b_new, report, fct.proxy_factor)
     if not np.array_equal(report.old_to_new, np.arange(len(report.old_to_new))):
         raise NotImplementedError("only DOF-preserving edits (hole moves) are supported")
     old = {L.lev: L for L in fct.levels}
     ctx = _Ctx(fct.spec, b_new, t_new, fct.tol, fct.proxy_count, fct.proxy_factor)
     torch.cuda.current_stream().synchronize()
     with torch.cuda.stream(_compress_stream()):
-        levels, store, n_recomp = _run_levels(ctx, reuse=old, dirty=dirty)
+        levels, store, n_recomp = _run_levels(ctx, reuse=old, dirty=dmask)
         rd, E_root, top, ipiv, UH, PsiV, UH_div, q, ratio = _finish_top(ctx, levels, store, ctx.pipe)
     torch.cuda.synchronize()
     stats = {"k_per_level": {L.lev: int(L.k.max(initial=0)) for L in levels},
@@ -1591,9 +1597,9 @@ def update(fct: Factorization, b_new, report, workers: int = 1) -> Factorization
     nf = Factorization(fct.spec, b_new, t_new, fct.tol, fct.proxy_count, fct.proxy_factor, levels,
                        rd, E_root, top, ipiv, UH, PsiV, UH_div, q, ctx, stats)
     nf.stats["update_time"] = time.perf_counter() - t0
-    nf.stats["n_dirty"] = len(dirty)
+    nf.stats["n_dirty"] = int(dmask.sum())
     nf.stats["n_boxes"] = len(t_new.lev)
-    nf.stats["dirty"] = dirty
+    nf.stats["dirty"] = {t_new.key(i) for i in np.flatnonzero(dmask)}
     return nf
 
 

@@ -63,6 +63,14 @@ class Tree:
     def key(self, i) -> tuple:
         return (int(self.lev[i]), int(self.ix[i]), int(self.iy[i]))
 
+    @property
+    def _index(self) -> dict:
+        idx = self.__dict__.get("_index_d")
+        if idx is None:
+            idx = {self.key(i): i for i in range(len(self.lev))}
+            self.__dict__["_index_d"] = idx
+        return idx
+
     def index(self, key) -> int:
         return self._index[tuple(int(v) for v in key)]
 
@@ -87,7 +95,6 @@ class Tree:
     # -- vectorised queries ---------------------------------------------------
     def _finish(self):
         n = len(self.lev)
-        self._index = {self.key(i): i for i in range(n)}
         self.is_leaf = self.nchild == 0
         # same-level neighbours in sorted key order (tree.py:70-81)
         self.neighbors = np.full((n, 8), -1, dtype=np.int64)
@@ -222,7 +229,59 @@ class Tree:
 
 
 def build_tree(positions, leaf_cap: int = 64, root_box=None, max_depth: int = 40) -> Tree:
-    """Reference build_tree (tree.py:110-155), vectorised per level."""
+    """Reference build_tree (tree.py:110-155) in the native host runtime
+    (csrc/host.cpp skb_tree_build); same tree as ``build_tree_np``."""
+    from . import _lib
+    pos = np.ascontiguousarray(positions, np.float64)
+    N = len(pos)
+    if root_box is None:
+        center, hw = default_root_box(pos)
+    else:
+        center, hw = np.asarray(root_box[0], float), float(root_box[1])
+        if np.any(np.abs(pos - center[None, :]) > hw * (1 + 1e-12)):
+            raise TreeError("node outside the fixed root box")
+    max_depth_eff = min(max_depth, 30)   # keys are int64 codes; deeper trees never occur here
+    lib = _lib.load()
+    root = np.array([center[0], center[1], hw], np.float64)
+    h = np.zeros(1, np.int64)
+    lib.skb_tree_build(pos.ctypes.data, N, leaf_cap, max_depth_eff, root.ctypes.data, h.ctypes.data)
+    try:
+        sz = np.zeros(3, np.int64)
+        lib.skb_tree_sizes(int(h[0]), sz.ctypes.data)
+        nbox, depth, nln = (int(v) for v in sz)
+        t = Tree(center, hw, leaf_cap, max_depth)
+        t.n_nodes = N
+        a = {k: np.empty(n, np.int64) for k, n in (
+            ("level_start", depth + 2), ("lev", nbox), ("ix", nbox), ("iy", nbox), ("parent", nbox),
+            ("children", 4 * nbox), ("nchild", nbox), ("node_start", nbox), ("node_cnt", nbox),
+            ("level_nodes", nln), ("level_nodes_off", depth + 2), ("nbr", 8 * nbox),
+            ("node_leaf", N))}
+        cen = np.empty((nbox, 2))
+        hws = np.empty(nbox)
+        lib.skb_tree_export(int(h[0]), *(a[k].ctypes.data for k in (
+            "level_start", "lev", "ix", "iy", "parent")), cen.ctypes.data, hws.ctypes.data,
+            *(a[k].ctypes.data for k in ("children", "nchild", "node_start", "node_cnt",
+                                        "level_nodes", "level_nodes_off", "nbr", "node_leaf")))
+    finally:
+        lib.skb_tree_free(int(h[0]))
+    t.level_start, t.lev, t.ix, t.iy, t.parent = (a["level_start"], a["lev"], a["ix"], a["iy"],
+                                                  a["parent"])
+    t.center, t.hw = cen, hws
+    t.children = a["children"].reshape(nbox, 4)
+    t.nchild = a["nchild"]
+    t.node_start, t.node_cnt = a["node_start"], a["node_cnt"]
+    lo = a["level_nodes_off"]
+    t.level_nodes = [a["level_nodes"][lo[l]:lo[l + 1]] for l in range(depth + 1)]
+    t._level_nodes_flat, t._level_nodes_off = a["level_nodes"], lo
+    t.is_leaf = t.nchild == 0
+    t.neighbors = a["nbr"].reshape(nbox, 8)
+    t.node_leaf = a["node_leaf"]
+    return t
+
+
+def build_tree_np(positions, leaf_cap: int = 64, root_box=None, max_depth: int = 40) -> Tree:
+    """Reference build_tree (tree.py:110-155), vectorised per level (NumPy
+    restatement of the native build, kept as its test oracle)."""
     pos = np.asarray(positions, float)
     N = len(pos)
     if root_box is None:
@@ -426,8 +485,49 @@ def dirty_closure(t: Tree, content: set) -> set:
     return out
 
 
+def _flat_arrays(t: Tree):
+    if not hasattr(t, "_level_nodes_flat"):
+        t._level_nodes_off = np.zeros(t.depth + 2, np.int64)
+        np.cumsum([len(x) for x in t.level_nodes], out=t._level_nodes_off[1:])
+        t._level_nodes_flat = np.concatenate(t.level_nodes).astype(np.int64)
+    arrs = [np.ascontiguousarray(x, np.int64) for x in (
+        t.level_start, t.lev, t.ix, t.iy, t.parent, t.node_start, t.node_cnt,
+        t._level_nodes_flat, t._level_nodes_off, t.neighbors, t.node_leaf)]
+    return arrs, (np.ctypeslib.as_ctypes_type(np.uint64) * len(arrs))(*[x.ctypes.data for x in arrs])
+
+
+def dirty_mask(t_old: Tree, t_new: Tree, b_new, report, proxy_factor) -> np.ndarray:
+    """Dirty boxes of an update (reference skel.py:476-491) as a mask over the
+    new tree, from the native host runtime (csrc/host.cpp skb_dirty_set)."""
+    from . import _lib
+    pts = []
+    if len(report.modified_nodes_old):
+        pts.append(report.old_positions[report.modified_nodes_old])
+    if len(report.modified_nodes_new):
+        pts.append(b_new.positions[report.modified_nodes_new])
+    pts = np.ascontiguousarray(np.concatenate(pts) if pts else np.zeros((0, 2)), np.float64)
+    an, pn = _flat_arrays(t_new)
+    ao, po = _flat_arrays(t_old)
+    root = np.array([t_new.root_center[0], t_new.root_center[1], t_new.root_half_width])
+    o2n = np.ascontiguousarray(report.old_to_new, np.int64)
+    mod = np.ascontiguousarray(report.modified_nodes_new, np.int64)
+    cen = np.ascontiguousarray(t_new.center, np.float64)
+    out = np.zeros(len(t_new.lev), np.uint8)
+    _lib.load().skb_dirty_set(pn, cen.ctypes.data, t_new.depth, po, t_old.depth, root.ctypes.data,
+                              o2n.ctypes.data, pts.ctypes.data, len(pts), mod.ctypes.data, len(mod),
+                              float(proxy_factor), out.ctypes.data)
+    del an, ao
+    return out.astype(bool)
+
+
 def dirty_set(t_old: Tree, t_new: Tree, b_new, report, proxy_factor) -> set:
-    """Dirty boxes of an update (reference skel.py:476-491)."""
+    """Dirty boxes of an update (reference skel.py:476-491), as keys."""
+    m = dirty_mask(t_old, t_new, b_new, report, proxy_factor)
+    return {t_new.key(i) for i in np.flatnonzero(m)}
+
+
+def dirty_set_np(t_old: Tree, t_new: Tree, b_new, report, proxy_factor) -> set:
+    """NumPy restatement of ``dirty_set`` (reference skel.py:476-491)."""
     content = set(ownership_changed(t_new, t_old, report.old_to_new))
     pts = []
     if len(report.modified_nodes_old):

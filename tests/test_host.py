@@ -107,3 +107,27 @@ def test_native_far_lists_and_proxies_match_numpy():
         assert np.array_equal(off, off2) and np.array_equal(F, F2)
         for a, a2 in zip(ctx.proxies(idx), ctx.proxies_np(idx)):
             assert np.array_equal(a, a2)
+
+
+@pytest.mark.parametrize("name", ["cfg1", "mini", "cfg2"])
+def test_native_tree_matches_numpy(name):
+    """Native quadtree build (csrc/host.cpp) == the NumPy restatement."""
+    from paper_2001_11619_b200.tree import build_tree_np
+    wl = configs.by_name(name)
+    a = build_tree(wl.boundary.positions, wl.leaf_cap)
+    b = build_tree_np(wl.boundary.positions, wl.leaf_cap)
+    for f in ("level_start", "lev", "ix", "iy", "parent", "children", "nchild", "node_start",
+              "node_cnt", "neighbors", "node_leaf", "is_leaf", "center", "hw"):
+        assert np.array_equal(getattr(a, f), getattr(b, f)), f
+    assert all(np.array_equal(x, y) for x, y in zip(a.level_nodes, b.level_nodes))
+
+
+def test_native_dirty_sets_match_numpy():
+    from paper_2001_11619_b200.tree import dirty_set_np
+    wl = configs.cfg2()
+    b = wl.boundary
+    t = build_tree(b.positions, wl.leaf_cap)
+    for h, d, nb, rep in configs.hole_move_sequence(b, 6):
+        tn = refit_tree(t, nb.positions)
+        assert dirty_set(t, tn, nb, rep, wl.proxy_factor) == dirty_set_np(t, tn, nb, rep, wl.proxy_factor)
+        t = tn
