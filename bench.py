@@ -286,6 +286,7 @@ def main():
                 "warmup": max(3, args.warmup), "ms_per_step": total_ms / args.steps,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic", "config": {**cfg, "l2": "flushed (256 MB write) before every timed step"},
+                "step_ms": [round(x, 3) for x in times], "e2e_step_ms": [round(x, 3) for x in e2e_times],
                 "roofline": roof, "kernel_families": fam_summary,
                 "kernel_families_note": f"CUDA-event timers on {prof_steps} extra steps after the timed region", "fp64_dgemm_tflops": fp64,
                 "gpu_launches": int(launches),

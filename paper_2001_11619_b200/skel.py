@@ -683,8 +683,9 @@ class _Ctx:
         np.cumsum(sizes, out=stack_off[1:])
         dev = _dev()
         _Prof.tick("host_far_proxy")
-        with _ht("L.upload"):
+        with _ht("L.stack_alloc"):
           stack = torch.empty(max(int(stack_off[-1]), 1), dtype=torch.float64, device=dev)
+        with _ht("L.upload"):
           up = _upload(act_off=act_off, act=act if len(act) else np.zeros(1, np.int64),
                      far_off=far_off, far=far if len(far) else np.zeros(1, np.int64),
                      pts=pts.reshape(-1), pn=pn.reshape(-1), pw=pw, stack_off=stack_off[:-1])
@@ -888,12 +889,18 @@ def _fetch(addr, rows, cols):
 class _FactorsView:
     """Lazy mapping key -> BoxFactors (reference Factorization.factors)."""
 
-    def __init__(self, fct):
-        self._f = fct
-        self._where = {}
-        for li, L in enumerate(fct.levels):
-            for bi, key in enumerate(L.keys):
-                self._where[key] = (li, bi)
+    def __init__(self, levels):
+        # holds the level list only (no reference back to the Factorization:
+        # a cycle would keep its device memory alive until the cyclic GC runs)
+        self._levels = levels
+        self._w = None
+
+    @property
+    def _where(self) -> dict:
+        if self._w is None:
+            self._w = {key: (li, bi) for li, L in enumerate(self._levels)
+                       for bi, key in enumerate(L.keys)}
+        return self._w
 
     def __len__(self):
         return len(self._where)
@@ -909,7 +916,7 @@ class _FactorsView:
 
     def __getitem__(self, key):
         li, bi = self._where[tuple(key)]
-        L = self._f.levels[li]
+        L = self._levels[li]
         bt = L.batch
         a0, a1 = bt.act_off[bi], bt.act_off[bi + 1]
         dofs = bt.act[a0:a1]
@@ -942,7 +949,7 @@ class Factorization:
         self.stats = stats
         rd = root_dofs if len(root_dofs) else np.zeros(1, np.int64)
         self._root_d = _upload(r=rd)
-        self.factors = _FactorsView(self)
+        self.factors = _FactorsView(levels)
 
     @property
     def n_dofs(self) -> int:

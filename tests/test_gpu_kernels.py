@@ -78,6 +78,33 @@ def test_getrf_getrs_batched():
         assert abs(r - d.min() / d.max()) <= 1e-10 * (d.min() / d.max())
 
 
+@pytest.mark.parametrize("n", [513, 849, 1100, 1600, 2532, 3100])
+def test_getrf_blocked_panel_classes(n):
+    """Blocked LU (shared-memory panels of 64/32/16/8 columns by order):
+    backward error of the solve, pivot ratio and interchanges against LAPACK."""
+    rng = np.random.default_rng(n)
+    A = rng.standard_normal((n, n))
+    Bm = rng.standard_normal((n, 2))
+    dA, dB = _dev(A), _dev(Bm)
+    ip = torch.empty(n, dtype=torch.int32, device="cuda")
+    info = torch.empty(1, dtype=torch.int32, device="cuda")
+    ratio = torch.empty(1, dtype=torch.float64, device="cuda")
+    m = skel._mats(np.array([dA.data_ptr()], np.uint64), [n], [n], [n])
+    call("skb_getrf_batched", 1, m, np.array([ip.data_ptr()], np.uint64), info, ratio, skel._stream())
+    call("skb_getrs_batched", 1, m, np.array([ip.data_ptr()], np.uint64),
+         skel._mats(np.array([dB.data_ptr()], np.uint64), [n], [2], [2]), skel._stream())
+    torch.cuda.synchronize()
+    assert int(info.cpu()[0]) == -1
+    x = dB.cpu().numpy()
+    berr = np.linalg.norm(A @ x - Bm) / (np.linalg.norm(A) * np.linalg.norm(x))
+    assert berr < 1e-14, berr
+    lu, piv = sla.lu_factor(A)
+    d = np.abs(np.diag(lu))
+    assert abs(float(ratio.cpu()[0]) - d.min() / d.max()) <= 1e-6 * (d.min() / d.max())
+    # partial pivoting on a random matrix: same interchanges as LAPACK
+    assert np.array_equal(ip.cpu().numpy(), piv.astype(np.int32))
+
+
 def test_getrf_singular_reports_index():
     A = np.array([[1.0, 2.0], [2.0, 4.0]])
     dA = _dev(A)
