@@ -263,20 +263,29 @@ def main():
         peaks = _peaks()
         fp64 = measure_fp64_peak(torch)
         hbm = float(peaks.get("hbm_gbs", 6650.0))
-        # dominant kernel family by device time
+        # dominant kernel family by device time; DRAM traffic per launch from the
+        # committed ncu capture of one factorization (profiles/, scripts/ncu_traffic.py)
         dom = max(fam, key=lambda k: fam[k]["ms"])
+        traffic = None
+        try:
+            tr = json.load(open(os.path.join(ROOT, "profiles", "r01_cfg2_traffic.json")))["families"]
+            # per launch of the family's timed scopes (bench launch count per step)
+            per_step = fam[dom]["launches"] / prof_steps
+            traffic = tr[dom]["dram_bytes"] / per_step if dom in tr and per_step else None
+        except Exception:
+            traffic = None
         d = fam[dom]
         per = max(d["launches"], 1)
         if d["flops"] > 0:
             ach = d["flops"] / (d["ms"] * 1e-3) / 1e12
             roof = {"bound": "tensor", "achieved": ach, "peak": fp64, "unit": "TFLOP/s",
-                    "frac": ach / fp64, "traffic": None, "kernel": dom,
+                    "frac": ach / fp64, "traffic": traffic, "kernel": dom,
                     "peak_source": "measured cuBLAS DGEMM 8192^3 (torch.matmul float64) in this run",
                     "avg_launch_ms": d["ms"] / per}
         else:
             ach = d["bytes"] / (d["ms"] * 1e-3) / 1e9
             roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
-                    "frac": ach / hbm, "traffic": None, "kernel": dom,
+                    "frac": ach / hbm, "traffic": traffic, "kernel": dom,
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs", "avg_launch_ms": d["ms"] / per}
         fam_summary = {k: {"ms_per_step": v["ms"] / prof_steps, "launches_per_step": v["launches"] / prof_steps,
                            **({"tflops": v["flops"] / (v["ms"] * 1e-3) / 1e12} if v["flops"] and v["ms"] else {}),
