@@ -274,6 +274,36 @@ int skb_level_aug(int64_t nbox, const int64_t* k, const int64_t* r, int64_t q,
                   const uint64_t* ipiv, double* UH, double* PsiV, double* UH_div,
                   double* schur, void* stream);
 
+/* ---- native level engine (csrc/engine.cu) ----------------------------------
+ * The compression chain of factor() (skel.py:443-449 over compress_box
+ * skel.py:293-316: assign_internal_actives, far_dofs, proxy rings, ID stack,
+ * Householder pre-reduction, QRCP, skeletons) runs level by level on a host
+ * thread of the library; the caller consumes finished levels.
+ * tree = {center, hw, neighbours, lev, ix, iy, children (nbox x 4), level_start,
+ * is_leaf (uint8)}; store = {big, a_start, a_len, s_start, s_len, fill} (int64,
+ * big of capacity cap; leaf actives pre-filled, the engine appends);
+ * geo = {px, py (host), pos, nrm, w (device), cs (P x 2 host)}.  Levels depth
+ * down to lev_lo; max_level_ints bounds one level's (perm, k, steps, gap).   */
+int skb_engine_start(const void* const* tree, int64_t depth, const double* root, double factor,
+                     int64_t* const* store, int64_t cap, const double* const* geo, int64_t P,
+                     double tol, void* stream, int64_t lev_lo, int64_t max_level_ints,
+                     int64_t* handle);
+/* Block until level L is done: sizes = {rc, B, na, box0, o_int, o_act}; ptrs =
+ * {act_off, act, rows, A, m_q, perm, k, steps, gap (host), stack, dbuf, dup
+ * (device), event}.  Host arrays stay valid until skb_engine_free.          */
+int skb_engine_wait(int64_t handle, int64_t L, int64_t* sizes, int64_t* ptrs);
+/* stream waits for level L's compression */
+int skb_engine_stream_wait(int64_t handle, int64_t L, void* stream);
+/* free level L's device buffers, stream-ordered on stream */
+int skb_engine_release(int64_t handle, int64_t L, void* stream);
+/* the caller has enqueued level L's Schur stage; lead >= 0 limits how many
+ * levels the engine may run ahead of the acknowledged level               */
+int skb_engine_ack(int64_t handle, int64_t L);
+int skb_engine_set_lead(int64_t handle, int64_t lead);
+/* stop after the current level and join the engine thread */
+int skb_engine_stop(int64_t handle);
+int skb_engine_free(int64_t handle, void* stream);
+
 /* ---- native host runtime (host arrays, no device; csrc/host.cpp) ---------
  * Per-level bookkeeping the reference does per box in Python.  Tree arrays as
  * in tree.py: center (nbox x 2), hw, neighbours (nbox x 8, -1 = none, sorted

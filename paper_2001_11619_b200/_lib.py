@@ -63,6 +63,14 @@ SIGNATURES = {
                         _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "skb_level_aug": [_i64, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                       _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "skb_engine_start": [_vp, _i64, _vp, _f64, _vp, _i64, _vp, _i64, _f64, _vp, _i64, _i64, _vp],
+    "skb_engine_wait": [_i64, _i64, _vp, _vp],
+    "skb_engine_stream_wait": [_i64, _i64, _vp],
+    "skb_engine_release": [_i64, _i64, _vp],
+    "skb_engine_stop": [_i64],
+    "skb_engine_ack": [_i64, _i64],
+    "skb_engine_set_lead": [_i64, _i64],
+    "skb_engine_free": [_i64, _vp],
     # native host runtime (host arrays only, no device)
     "skb_host_far_lists": [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _f64,
                            _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp],

@@ -24,6 +24,7 @@ SOURCES = {
     "misc.cu": [],
     "matvec.cu": [],
     "level.cu": [],
+    "engine.cu": [],
 }
 # native host runtime (no CUDA): plain g++, no FP contraction (NumPy rounding)
 HOST_SOURCES = {"host.cpp": []}

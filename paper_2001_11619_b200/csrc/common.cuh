@@ -5,6 +5,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <mutex>
 #include <utility>
 #include <vector>
 
@@ -70,8 +71,12 @@ struct PinnedRing {
   std::vector<cudaEvent_t> pool;
 };
 PinnedRing& ring();
+// host-side state shared by the Python thread and the native level engine
+// thread (pinned ring, shared-memory opt-in table, profiling timers)
+std::recursive_mutex& host_mutex();
 
 inline int ring_stage(const void* host, size_t bytes, cudaStream_t s, void* dev) {
+  std::lock_guard<std::recursive_mutex> lk(host_mutex());
   PinnedRing& R = ring();
   if (!R.base) {
     // keep stream-ordered allocations cached in the pool across synchronisations
@@ -81,6 +86,11 @@ inline int ring_stage(const void* host, size_t bytes, cudaStream_t s, void* dev)
     SKB_RET(cudaDeviceGetDefaultMemPool(&pool, dev));
     uint64_t thr = ~0ull;
     SKB_RET(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    if (getenv("SKB_POOL_STRICT")) {
+      int zero = 0;
+      SKB_RET(cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowOpportunistic, &zero));
+      SKB_RET(cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &zero));
+    }
     SKB_RET(cudaHostAlloc((void**)&R.base, PinnedRing::kSize, cudaHostAllocDefault));
   }
   if (bytes > PinnedRing::kSize / 2) {      // oversized: plain (pageable) copy
@@ -136,6 +146,7 @@ inline int ring_stage(const void* host, size_t bytes, cudaStream_t s, void* dev)
 // Opt a kernel into the largest dynamic shared memory once (changing the
 // attribute between launches can serialise the device).
 inline cudaError_t smem_optin(const void* fn) {
+  std::lock_guard<std::recursive_mutex> lk(host_mutex());
   static std::vector<const void*> done;
   for (const void* f : done)
     if (f == fn) return cudaSuccess;
@@ -151,12 +162,21 @@ inline cudaError_t smem_optin(const void* fn) {
   return e;
 }
 
+// Stream-ordered allocation from the calling thread's pool: the native level
+// engine thread allocates from a pool of its own, so its allocations never
+// share a pool with the Python thread's (cross-stream reuse stays per thread).
+cudaMemPool_t& tl_pool();
+inline cudaError_t malloc_async(void** p, size_t n, cudaStream_t s) {
+  cudaMemPool_t pl = tl_pool();
+  return pl ? cudaMallocFromPoolAsync(p, n, pl, s) : cudaMallocAsync(p, n, s);
+}
+
 // Copy host descriptors to a stream-ordered device buffer (freed async by caller).
 template <typename T>
 inline int upload(const T* host, int64_t n, cudaStream_t s, T** dev) {
   *dev = nullptr;
   if (n <= 0) return 0;
-  SKB_RET(cudaMallocAsync((void**)dev, sizeof(T) * n, s));
+  SKB_RET(malloc_async((void**)dev, sizeof(T) * n, s));
   if (capture().on) {
     CaptureSession& C = capture();
     const size_t off = (C.used + 255) & ~(size_t)255;
@@ -197,10 +217,16 @@ struct ProfScope {
   cudaStream_t s;
   cudaEvent_t a{}, b{};
   ProfScope(int f, cudaStream_t st) : fam(f), s(st) {
-    if (prof().on) { a = prof().get(); b = prof().get(); cudaEventRecord(a, s); }
+    if (prof().on) {
+      std::lock_guard<std::recursive_mutex> lk(host_mutex());
+      a = prof().get(); b = prof().get(); cudaEventRecord(a, s);
+    }
   }
   ~ProfScope() {
-    if (prof().on) { cudaEventRecord(b, s); prof().ev[fam].push_back({a, b}); }
+    if (prof().on) {
+      std::lock_guard<std::recursive_mutex> lk(host_mutex());
+      cudaEventRecord(b, s); prof().ev[fam].push_back({a, b});
+    }
   }
 };
 

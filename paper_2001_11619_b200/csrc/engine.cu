@@ -1,0 +1,425 @@
+// Native level engine: the critical-path compression chain of factor()
+// (reference skel.py:443-449 driving compress_box skel.py:293-316) runs on a
+// host thread of its own, level by level from the leaves up:
+//
+//   assign_internal_actives (skel.py:251-256) -> far_dofs (skel.py:258-280)
+//   -> proxy rings (kernels.py:263-273) -> ID stacks (skb_assemble_stack)
+//   -> Householder pre-reduction -> QRCP -> ONE device->host copy of
+//   (perm, k, steps, gap) -> skeletons (skel = act[perm[:k]]) -> next level.
+//
+// The Python side consumes finished levels (skb_engine_wait) and enqueues the
+// Schur stage and the augmentation sweep on its own streams while the engine
+// already compresses the next level, so Python bookkeeping is off the
+// critical path.  Same host functions and kernels as the Python launch path:
+// identical results.  The active/skeleton store arrays are the caller's
+// (ActStore numpy buffers); the engine appends to them.
+
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <atomic>
+#include <condition_variable>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include "common.cuh"
+
+namespace skb {
+void use_engine_ring(bool on);
+int geqrf_batched(int64_t nbox, const int64_t* m, const int64_t* n, const int64_t* lda,
+                  const int64_t* A, cudaStream_t s);
+int qrcp_batched(int64_t nbox, const int64_t* m, const int64_t* n, const int64_t* lda,
+                 const int64_t* A, const int64_t* kmin, double tol, const int64_t* perm_off,
+                 int32_t* perm, double* diag, int32_t* k_out, int32_t* steps_out,
+                 double* min_gap, cudaStream_t s);
+}  // namespace skb
+
+using namespace skb;
+
+namespace {
+
+struct LevelOut {
+  int rc = 0;
+  bool ready = false;
+  int64_t B = 0, na = 0, box0 = 0;
+  std::vector<int64_t> act_off, act, rows, A, mq;
+  std::vector<int32_t> perm, k, steps;
+  std::vector<double> gap;
+  double* stack = nullptr;
+  char* dbuf = nullptr;          // diag | gap | perm, k, steps (device)
+  int64_t* dup = nullptr;        // uploaded descriptors (device): act_off | act | ...
+  int64_t o_int = 0;             // byte offset of perm in dbuf
+  int64_t o_act = 0;             // element offset of act in dup
+  cudaEvent_t ev = nullptr;
+};
+
+struct Engine {
+  // tree (tree.py layout)
+  const double *center, *hw;
+  const int64_t *nbr, *lev, *ix, *iy, *children, *level_start;
+  const uint8_t* leaf;
+  int64_t depth;
+  double root[3], factor;
+  // store (ActStore buffers)
+  int64_t *big, *a_start, *a_len, *s_start, *s_len, *fill;
+  int64_t cap;
+  // geometry
+  const double *px, *py, *pos, *nrm, *w, *cs;
+  int64_t P;
+  double tol;
+  cudaStream_t s;
+  int dev;
+  int64_t lev_lo;
+  std::vector<LevelOut> out;     // indexed by level
+  std::mutex m;
+  std::condition_variable cv;
+  std::atomic<bool> stop{false};
+  int64_t acked = 1 << 30;       // lowest level whose Schur stage the caller has enqueued
+  int64_t lead = -1;             // >= 0: run at most `lead` levels ahead of the caller
+  std::thread th;
+  char* pinned = nullptr;
+  size_t pinned_size = 0;
+  bool* shared_pinned = nullptr;   // set: the pinned buffer is the shared one
+};
+
+int64_t append(Engine& E, const int64_t* a, int64_t n) {
+  const int64_t o = *E.fill;
+  if (o + n > E.cap) return -1;
+  if (n) memcpy(E.big + o, a, sizeof(int64_t) * n);
+  *E.fill = o + n;
+  return o;
+}
+
+int run_level(Engine& E, int64_t L, LevelOut& R) {
+  const int64_t b0 = E.level_start[L], B = E.level_start[L + 1] - b0;
+  R.B = B;
+  R.box0 = b0;
+  if (B == 0) return 0;
+  std::vector<int64_t> idx(B);
+  for (int64_t b = 0; b < B; ++b) idx[b] = b0 + b;
+  // assign_internal_actives: active = concat of the children's skeletons in child order
+  {
+    std::vector<int64_t> tmp;
+    for (int64_t i : idx) {
+      if (E.leaf[i]) continue;
+      tmp.clear();
+      for (int q = 0; q < 4; ++q) {
+        const int64_t c = E.children[4 * i + q];
+        if (c < 0) continue;
+        tmp.insert(tmp.end(), E.big + E.s_start[c], E.big + E.s_start[c] + E.s_len[c]);
+      }
+      const int64_t o = append(E, tmp.data(), (int64_t)tmp.size());
+      if (o < 0) return 7;
+      E.a_start[i] = o;
+      E.a_len[i] = (int64_t)tmp.size();
+    }
+  }
+  R.act_off.assign(B + 1, 0);
+  for (int64_t b = 0; b < B; ++b) R.act_off[b + 1] = R.act_off[b] + E.a_len[idx[b]];
+  R.na = R.act_off[B];
+  R.act.resize(std::max<int64_t>(R.na, 1));
+  for (int64_t b = 0; b < B; ++b)
+    memcpy(R.act.data() + R.act_off[b], E.big + E.a_start[idx[b]], sizeof(int64_t) * E.a_len[idx[b]]);
+  // far-field DOF lists and proxy rings (native host runtime)
+  std::vector<int64_t> far_off(B + 1), far(4096);
+  int64_t need = 0;
+  int rc = skb_host_far_lists(B, idx.data(), E.center, E.hw, E.nbr, E.lev, E.ix, E.iy, E.leaf,
+                              E.level_start, E.depth, E.root, E.factor, E.big, E.a_start, E.a_len,
+                              E.px, E.py, far_off.data(), far.data(), (int64_t)far.size(), &need);
+  if (rc == 1) {
+    far.resize(need + 1);
+    rc = skb_host_far_lists(B, idx.data(), E.center, E.hw, E.nbr, E.lev, E.ix, E.iy, E.leaf,
+                            E.level_start, E.depth, E.root, E.factor, E.big, E.a_start, E.a_len,
+                            E.px, E.py, far_off.data(), far.data(), (int64_t)far.size(), &need);
+  }
+  if (rc) return 8;
+  const int64_t P = E.P;
+  std::vector<double> pts(B * P * 2), pn(B * P * 2), pw(B);
+  skb_host_proxies(B, idx.data(), E.center, E.hw, E.factor, P, E.cs, pts.data(), pn.data(), pw.data());
+  // stack layout (column-major per box, ld = rows)
+  R.rows.resize(B);
+  std::vector<int64_t> nB(B), stack_off(B + 1, 0);
+  int64_t maxnB = 0, maxitems = 0;
+  for (int64_t b = 0; b < B; ++b) {
+    nB[b] = R.act_off[b + 1] - R.act_off[b];
+    const int64_t nF = far_off[b + 1] - far_off[b];
+    R.rows[b] = 2 * nF + 6 * P + 2;
+    stack_off[b + 1] = stack_off[b] + R.rows[b] * nB[b];
+    maxnB = std::max(maxnB, nB[b]);
+    maxitems = std::max(maxitems, nF + P + 1);
+  }
+  cudaStream_t s = E.s;
+  SKB_RET(malloc_async((void**)&R.stack, sizeof(double) * std::max<int64_t>(stack_off[B], 1), s));
+  // one upload: act_off | act | far_off | far | pts | pn | pw | stack_off
+  std::vector<int64_t> pk;
+  const int64_t nfar = std::max<int64_t>(far_off[B], 1);
+  pk.reserve(2 * (B + 1) + R.act.size() + nfar + 4 * B * P + 2 * B);
+  auto add = [&](const void* p, int64_t n) {
+    const int64_t o = ((int64_t)pk.size() + 1) & ~(int64_t)1;   // 16-byte aligned (double2 loads)
+    pk.resize(o + n);
+    memcpy(pk.data() + o, p, sizeof(int64_t) * n);
+    return o;
+  };
+  const int64_t o_ao = add(R.act_off.data(), B + 1);
+  R.o_act = add(R.act.data(), (int64_t)R.act.size());
+  const int64_t o_fo = add(far_off.data(), B + 1);
+  const int64_t o_f = add(far.data(), nfar);
+  const int64_t o_pt = add(pts.data(), B * P * 2);
+  const int64_t o_pn = add(pn.data(), B * P * 2);
+  const int64_t o_pw = add(pw.data(), B);
+  const int64_t o_so = add(stack_off.data(), B);
+  if ((rc = upload(pk.data(), (int64_t)pk.size(), s, &R.dup))) return rc;
+  if ((rc = skb_assemble_stack(E.pos, E.nrm, E.w, B, R.dup + o_ao, R.dup + R.o_act, R.dup + o_fo,
+                               R.dup + o_f, (const double*)(R.dup + o_pt),
+                               (const double*)(R.dup + o_pn), (const double*)(R.dup + o_pw),
+                               (int32_t)P, R.dup + o_so, R.stack, maxnB, maxitems, s)))
+    return rc;
+  // Householder pre-reduction of the tall stacks (dense.py:56-59)
+  R.A.resize(B);
+  R.mq.resize(B);
+  std::vector<int64_t> pm, pn_, pA;
+  for (int64_t b = 0; b < B; ++b) {
+    R.A[b] = (int64_t)(R.stack + stack_off[b]);
+    const bool pre = R.rows[b] > nB[b];
+    R.mq[b] = pre ? nB[b] : R.rows[b];
+    if (pre) { pm.push_back(R.rows[b]); pn_.push_back(nB[b]); pA.push_back(R.A[b]); }
+  }
+  if (!pm.empty() && (rc = geqrf_batched((int64_t)pm.size(), pm.data(), pn_.data(), pm.data(),
+                                         pA.data(), s)))
+    return rc;
+  // QRCP with rank at tol (dense.py:60-68)
+  const int64_t na = R.na;
+  const int64_t o_gap = 8 * std::max<int64_t>(na, 1);
+  R.o_int = o_gap + 8 * std::max<int64_t>(B, 1);
+  const int64_t nint = na + 2 * B + 1;
+  const int64_t dbytes = R.o_int + 4 * nint;
+  SKB_RET(malloc_async((void**)&R.dbuf, dbytes, s));
+  std::vector<int64_t> kmin(B, 0);
+  int32_t* ints = (int32_t*)(R.dbuf + R.o_int);
+  if ((rc = qrcp_batched(B, R.mq.data(), nB.data(), R.rows.data(), R.A.data(), kmin.data(), E.tol,
+                         R.act_off.data(), ints, (double*)R.dbuf, ints + na, ints + na + B,
+                         (double*)(R.dbuf + o_gap), s)))
+    return rc;
+  // one device->host copy: gap | perm | k | steps
+  const size_t hb = (size_t)(dbytes - o_gap);
+  if (hb > E.pinned_size) return 9;
+  SKB_RET(cudaMemcpyAsync(E.pinned, R.dbuf + o_gap, hb, cudaMemcpyDeviceToHost, s));
+  SKB_RET(cudaEventRecord(R.ev, s));
+  SKB_RET(cudaEventSynchronize(R.ev));
+  const double* gap = (const double*)E.pinned;
+  const int32_t* ih = (const int32_t*)(E.pinned + (R.o_int - o_gap));
+  R.gap.assign(gap, gap + B);
+  R.perm.assign(ih, ih + na);
+  R.k.assign(ih + na, ih + na + B);
+  R.steps.assign(ih + na + B, ih + na + 2 * B);
+  // skeletons: skel = act[perm[:k]] (assign_internal_actives of the next level reads them)
+  for (int64_t b = 0; b < B; ++b) {
+    const int64_t i = idx[b], a0 = R.act_off[b], kk = R.k[b];
+    std::vector<int64_t> sk(kk);
+    for (int64_t j = 0; j < kk; ++j) sk[j] = R.act[a0 + R.perm[a0 + j]];
+    const int64_t o = append(E, sk.data(), kk);
+    if (o < 0) return 7;
+    E.s_start[i] = o;
+    E.s_len[i] = kk;
+  }
+  return 0;
+}
+
+void engine_main(Engine* E) {
+  cudaSetDevice(E->dev);
+  if (!getenv("SKB_ENGINE_SHARED_POOL")) {
+    static cudaMemPool_t pool = nullptr;
+    static std::mutex pm;
+    std::lock_guard<std::mutex> lk(pm);
+    if (!pool) {
+      cudaMemPoolProps props = {};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.handleTypes = cudaMemHandleTypeNone;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = E->dev;
+      if (cudaMemPoolCreate(&pool, &props) == cudaSuccess) {
+        uint64_t thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      } else {
+        pool = nullptr;
+      }
+    }
+    skb::tl_pool() = pool;
+  }
+  for (int64_t L = E->depth; L >= E->lev_lo; --L) {
+    LevelOut& R = E->out[L];
+    if (E->lead >= 0) {
+      std::unique_lock<std::mutex> lk(E->m);
+      E->cv.wait(lk, [&] { return E->stop.load() || E->acked <= L + 1 + E->lead || L + 1 + E->lead > E->depth; });
+    }
+    int rc = 0;
+    if (E->stop.load()) rc = -1000;
+    else rc = run_level(*E, L, R);
+    {
+      std::lock_guard<std::mutex> lk(E->m);
+      R.rc = rc;
+      R.ready = true;
+    }
+    E->cv.notify_all();
+    if (rc) {
+      // later levels cannot run: mark them failed
+      std::lock_guard<std::mutex> lk(E->m);
+      for (int64_t L2 = L - 1; L2 >= E->lev_lo; --L2) {
+        E->out[L2].rc = -1000;
+        E->out[L2].ready = true;
+      }
+      E->cv.notify_all();
+      return;
+    }
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+// arrays: {center, hw, nbr, lev, ix, iy, children, level_start, leaf(uint8)} (tree.py layout);
+// store: {big, a_start, a_len, s_start, s_len, fill}; geo: {px, py, pos, nrm, w, cs} (pos/nrm/w device)
+int skb_engine_start(const void* const* tree, int64_t depth, const double* root, double factor,
+                     int64_t* const* store, int64_t cap, const double* const* geo, int64_t P,
+                     double tol, void* stream, int64_t lev_lo, int64_t max_level_ints,
+                     int64_t* handle) {
+  Engine* E = new Engine();
+  E->center = (const double*)tree[0];
+  E->hw = (const double*)tree[1];
+  E->nbr = (const int64_t*)tree[2];
+  E->lev = (const int64_t*)tree[3];
+  E->ix = (const int64_t*)tree[4];
+  E->iy = (const int64_t*)tree[5];
+  E->children = (const int64_t*)tree[6];
+  E->level_start = (const int64_t*)tree[7];
+  E->leaf = (const uint8_t*)tree[8];
+  E->depth = depth;
+  memcpy(E->root, root, sizeof(E->root));
+  E->factor = factor;
+  E->big = store[0]; E->a_start = store[1]; E->a_len = store[2];
+  E->s_start = store[3]; E->s_len = store[4]; E->fill = store[5];
+  E->cap = cap;
+  E->px = geo[0]; E->py = geo[1]; E->pos = geo[2]; E->nrm = geo[3]; E->w = geo[4]; E->cs = geo[5];
+  E->P = P;
+  E->tol = tol;
+  E->s = (cudaStream_t)stream;
+  E->lev_lo = lev_lo;
+  cudaGetDevice(&E->dev);
+  E->out.resize(depth + 1);
+  for (int64_t L = lev_lo; L <= depth; ++L)
+    SKB_RET(cudaEventCreateWithFlags(&E->out[L].ev, cudaEventDisableTiming));
+  // pinned landing buffer for the per-level device->host copy: kept across
+  // factorizations (cudaHostAlloc / cudaFreeHost would synchronise the device)
+  {
+    static char* g_pinned = nullptr;
+    static size_t g_size = 0;
+    static bool g_busy = false;
+    std::lock_guard<std::recursive_mutex> lk(host_mutex());
+    const size_t want = (size_t)(8 * max_level_ints + 1024);
+    if (!g_busy) {
+      if (g_size < want) {
+        if (g_pinned) cudaFreeHost(g_pinned);
+        SKB_RET(cudaHostAlloc((void**)&g_pinned, want, cudaHostAllocDefault));
+        g_size = want;
+      }
+      g_busy = true;
+      E->pinned = g_pinned;
+      E->pinned_size = g_size;
+      E->shared_pinned = &g_busy;
+    } else {
+      SKB_RET(cudaHostAlloc((void**)&E->pinned, want, cudaHostAllocDefault));
+      E->pinned_size = want;
+    }
+  }
+  E->th = std::thread(engine_main, E);
+  *handle = (int64_t)E;
+  return 0;
+}
+
+// Block until level L is compressed; sizes = {rc, B, na, box0, o_int, o_act}; ptrs =
+// {act_off, act, rows, A, mq, perm(i32), k(i32), steps(i32), gap(f64), stack, dbuf, dup, event}
+int skb_engine_wait(int64_t handle, int64_t L, int64_t* sizes, int64_t* ptrs) {
+  Engine* E = (Engine*)handle;
+  LevelOut& R = E->out[L];
+  {
+    std::unique_lock<std::mutex> lk(E->m);
+    E->cv.wait(lk, [&] { return R.ready; });
+  }
+  sizes[0] = R.rc; sizes[1] = R.B; sizes[2] = R.na; sizes[3] = R.box0; sizes[4] = R.o_int;
+  sizes[5] = R.o_act;
+  ptrs[0] = (int64_t)R.act_off.data(); ptrs[1] = (int64_t)R.act.data(); ptrs[2] = (int64_t)R.rows.data();
+  ptrs[3] = (int64_t)R.A.data(); ptrs[4] = (int64_t)R.mq.data(); ptrs[5] = (int64_t)R.perm.data();
+  ptrs[6] = (int64_t)R.k.data(); ptrs[7] = (int64_t)R.steps.data(); ptrs[8] = (int64_t)R.gap.data();
+  ptrs[9] = (int64_t)R.stack; ptrs[10] = (int64_t)R.dbuf; ptrs[11] = (int64_t)R.dup;
+  ptrs[12] = (int64_t)R.ev;
+  return 0;
+}
+
+// The caller has enqueued level L's Schur stage (engine lead control).
+int skb_engine_ack(int64_t handle, int64_t L) {
+  Engine* E = (Engine*)handle;
+  {
+    std::lock_guard<std::mutex> lk(E->m);
+    if (L < E->acked) E->acked = L;
+  }
+  E->cv.notify_all();
+  return 0;
+}
+
+int skb_engine_set_lead(int64_t handle, int64_t lead) {
+  ((Engine*)handle)->lead = lead;
+  return 0;
+}
+
+// Make `stream` wait for level L's compression (the Schur stage reads its stacks).
+int skb_engine_stream_wait(int64_t handle, int64_t L, void* stream) {
+  Engine* E = (Engine*)handle;
+  SKB_RET(cudaStreamWaitEvent((cudaStream_t)stream, E->out[L].ev, 0));
+  return 0;
+}
+
+// Release level L's device buffers, stream-ordered on `stream` (after the
+// Schur stage that reads them has been enqueued there).
+int skb_engine_release(int64_t handle, int64_t L, void* stream) {
+  Engine* E = (Engine*)handle;
+  LevelOut& R = E->out[L];
+  cudaStream_t s = (cudaStream_t)stream;
+  if (R.stack) { cudaFreeAsync(R.stack, s); R.stack = nullptr; }
+  if (R.dbuf) { cudaFreeAsync(R.dbuf, s); R.dbuf = nullptr; }
+  if (R.dup) { cudaFreeAsync(R.dup, s); R.dup = nullptr; }
+  return 0;
+}
+
+// Ask the engine to stop after its current level and wait for the thread.
+int skb_engine_stop(int64_t handle) {
+  Engine* E = (Engine*)handle;
+  {
+    std::lock_guard<std::mutex> lk(E->m);
+    E->stop.store(true);
+  }
+  E->cv.notify_all();
+  if (E->th.joinable()) E->th.join();
+  return 0;
+}
+
+int skb_engine_free(int64_t handle, void* stream) {
+  Engine* E = (Engine*)handle;
+  if (E->th.joinable()) E->th.join();
+  for (int64_t L = E->lev_lo; L <= E->depth; ++L) {
+    skb_engine_release(handle, L, stream);
+    if (E->out[L].ev) cudaEventDestroy(E->out[L].ev);
+  }
+  if (E->shared_pinned) {
+    std::lock_guard<std::recursive_mutex> lk(host_mutex());
+    *E->shared_pinned = false;       // the engine thread has joined: no copy in flight
+  } else if (E->pinned) {
+    cudaFreeHost(E->pinned);
+  }
+  delete E;
+  return 0;
+}
+
+}  // extern "C"

@@ -76,8 +76,8 @@ extern "C" int skb_level_schur(int64_t nbox, const int64_t* nB, const int64_t* k
   }
   double* Ebuf = nullptr;
   double* Xrs = nullptr;
-  SKB_RET(cudaMallocAsync((void**)&Ebuf, sizeof(double) * std::max<int64_t>(E_off[B], 1), s));
-  SKB_RET(cudaMallocAsync((void**)&Xrs, sizeof(double) * std::max<int64_t>(X_off[B], 1), s));
+  SKB_RET(malloc_async((void**)&Ebuf, sizeof(double) * std::max<int64_t>(E_off[B], 1), s));
+  SKB_RET(malloc_async((void**)&Xrs, sizeof(double) * std::max<int64_t>(X_off[B], 1), s));
   int rc;
   // T = R11^-1 R12 (dense.py:77)
   if ((rc = skb_id_T_batched(B, A, lda, k, nB, perm_ptr.data(), (const int64_t*)T, s))) return rc;
@@ -161,7 +161,7 @@ extern "C" int skb_level_aug(int64_t nbox, const int64_t* k, const int64_t* r, i
     oSp[b] += bSp;
   }
   double* buf = nullptr;
-  SKB_RET(cudaMallocAsync((void**)&buf, sizeof(double) * std::max<int64_t>(total, 1), s));
+  SKB_RET(malloc_async((void**)&buf, sizeof(double) * std::max<int64_t>(total, 1), s));
   // deterministic schur accumulation order: contributions grouped by corner
   // row, box order kept (stable), skel.py:396
   const int64_t ncol = cols_off[B];

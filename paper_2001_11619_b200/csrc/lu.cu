@@ -558,8 +558,8 @@ int getrs_batched(int64_t nbox, const SkbMat* lu, const int64_t* ipiv, const Skb
     if ((rc = upload(sd.data(), (int64_t)sd.size(), s, &d))) return rc;
     if ((rc = upload(poff.data(), (int64_t)poff.size(), s, &dpo))) return rc;
     if ((rc = upload(toff.data(), (int64_t)toff.size(), s, &dto))) return rc;
-    SKB_RET(cudaMallocAsync((void**)&perm, sizeof(int32_t) * std::max<int64_t>(pt, 1), s));
-    SKB_RET(cudaMallocAsync((void**)&tmp, sizeof(double) * std::max<int64_t>(tt, 1), s));
+    SKB_RET(malloc_async((void**)&perm, sizeof(int32_t) * std::max<int64_t>(pt, 1), s));
+    SKB_RET(malloc_async((void**)&tmp, sizeof(double) * std::max<int64_t>(tt, 1), s));
     {
       ProfScope ps(F_TRSM, s);
       const int64_t nbx = (int64_t)sd.size();

@@ -168,7 +168,7 @@ extern "C" int skb_system_matvec(const double* pos, const double* nrm, const dou
   cudaStream_t s = (cudaStream_t)stream;
   const int nparts = 148;
   double* parts = nullptr;
-  SKB_RET(cudaMallocAsync((void**)&parts, sizeof(double) * nparts * MV_R, s));
+  SKB_RET(malloc_async((void**)&parts, sizeof(double) * nparts * MV_R, s));
   for (int64_t r0 = 0; r0 < nrhs; r0 += MV_R) {
     const int rc = (int)((nrhs - r0) < MV_R ? (nrhs - r0) : MV_R);
     k_mv_ndot<<<nparts, MV_T, 0, s>>>((const double2*)nrm, w, n_nodes, x, nrhs, r0, rc, parts);

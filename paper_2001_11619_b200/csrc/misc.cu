@@ -263,9 +263,20 @@ CaptureSession& capture() {
   static CaptureSession c;
   return c;
 }
+thread_local bool t_engine_ring = false;
 PinnedRing& ring() {
   static PinnedRing r;
-  return r;
+  static PinnedRing re;        // the native level engine thread's own ring
+  return t_engine_ring ? re : r;
+}
+void use_engine_ring(bool on) { t_engine_ring = on; }
+cudaMemPool_t& tl_pool() {
+  thread_local cudaMemPool_t p = nullptr;
+  return p;
+}
+std::recursive_mutex& host_mutex() {
+  static std::recursive_mutex m;
+  return m;
 }
 static std::vector<std::vector<void*>> g_sessions;
 }  // namespace skb
