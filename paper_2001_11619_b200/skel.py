@@ -1084,12 +1084,9 @@ class Factorization:
             call("skb_scatter_rows", 1, ptr(up["ro"]), ptr(rd["r"]), None, None, nr,
                  _addr(top_rhs), ptr(up["o"]), ptr(up["ld"]), ptr(x), nr, 0, 1.0, ns, nr, s)
             x[nd:].copy_(top_rhs[ns:])
-            # x[:nd] -= UH_div lam (UH_div rows of root DOFs are exactly zero)
-            _gemm([dict(A=np.array([_addr(self.UH_div)], np.uint64),
-                        B=np.array([_addr(top_rhs) + 8 * ns * nr], np.uint64),
-                        C=np.array([_addr(x)], np.uint64), D=np.array([_addr(x)], np.uint64),
-                        m=[nd], n=[nr], k=[q], lda=[q], ldb=[nr], ldc=[nr], ldd=[nr],
-                        alpha=[-1.0], beta=[1.0])])
+            # x[:nd] -= UH_div lam (UH_div rows of root DOFs are exactly zero): one
+            # plain (2N x q) x (q x nrhs) product, the largest GEMM of the solve -> cuBLAS
+            x[:nd].addmm_(self.UH_div, top_rhs[ns:], alpha=-1.0)
             keep += [top_rhs]
         else:
             top_rhs = torch.empty((ns, nr), dtype=torch.float64, device=dev)

@@ -39,3 +39,5 @@ run(1000, 768, 200, batch=64)
 run(100, 768, 100, ta=1, batch=1000)
 run(500, 91, 32, batch=300)
 run(768, 256, 300000, ta=1)
+run(294912, 256, 768)
+run(2532, 256, 2532)

@@ -24,12 +24,18 @@ t = build_tree(b.positions, wl.leaf_cap)
 fa = lambda: factor(SystemSpec(), b, t, wl.tol, proxy_count=wl.proxy_count, proxy_factor=wl.proxy_factor)
 for _ in range(3):
     f = fa()
-if mode == "update":
+if mode == "solve":
+    import numpy as np
+    X = torch.from_numpy(np.random.default_rng(5).standard_normal((f.dim, 256))).cuda()
+    f.solve(X)
+    f.solve(X)
+    run = lambda: f.solve(X)
+elif mode == "update":
     seq = configs.hole_move_sequence(b, 3)
     f = update(f, seq[0][2], seq[0][3])
     run = lambda: update(f, seq[1][2], seq[1][3])
     run()
-else:
+elif mode != "solve":
     run = fa
 torch.cuda.synchronize()
 with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
