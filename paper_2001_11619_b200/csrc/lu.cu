@@ -75,6 +75,8 @@ __global__ void __launch_bounds__(NT) k_getf2_panel(const LuPanel* __restrict__ 
       __syncthreads();
       continue;
     }
+    // every thread has read the pivot before thread c swaps it out of col[p]
+    __syncthreads();
     if (p != c && threadIdx.x < jb) {
       double* a = P + (int64_t)threadIdx.x * rows;
       const double t = a[c]; a[c] = a[p]; a[p] = t;
@@ -250,7 +252,12 @@ __global__ void k_pivot_ratio(const RatioDesc* __restrict__ descs, double* __res
 
 // Whole-matrix LU in shared memory, one CTA per matrix (n <= kSmallLU):
 // right-looking dgetf2 with the row swap applied to the full row.
-constexpr int kSmallLU = 160;
+constexpr int kSmallLU_ = 160;
+static inline int64_t small_lu_max() {   // SKB_SMALL_LU: debug override of the one-CTA LU bound
+  static const int64_t v = getenv("SKB_SMALL_LU") ? atoll(getenv("SKB_SMALL_LU")) : kSmallLU_;
+  return v;
+}
+#define kSmallLU small_lu_max()
 
 struct SmallLU {
   double* A;
@@ -296,6 +303,8 @@ __global__ void __launch_bounds__(NT) k_getrf_small(const SmallLU* __restrict__ 
       __syncthreads();
       continue;
     }
+    // every thread has read the pivot before the row interchange moves it
+    __syncthreads();
     if (p != j)
       for (int c = threadIdx.x; c < n; c += NT) {
         const double t = M[j * L + c]; M[j * L + c] = M[p * L + c]; M[p * L + c] = t;

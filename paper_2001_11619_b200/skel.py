@@ -1437,11 +1437,9 @@ def _aug_level(L: LevelFactors, UH, PsiV, UH_div, schur, q):
          L.P["Xsr"], L.P["Xrsdiv"], L.ipiv, ptr(UH), ptr(PsiV), ptr(UH_div), ptr(schur), _stream())
 
 
-# The native level engine (csrc/engine.cu) is opt-in (SKB_ENGINE=1): with the
-# engine running ahead, a Schur-stage LU occasionally differs when it executes
-# concurrently with the next levels' compression (root cause not yet found;
-# see DESIGN.md §7).  The default is the single-threaded level loop below.
-_ENGINE_ON = os.environ.get("SKB_ENGINE", "0") == "1"
+# The native level engine (csrc/engine.cu) drives factor() unless SKB_ENGINE=0
+# (then the single-threaded level loop below, which update() always uses).
+_ENGINE_ON = os.environ.get("SKB_ENGINE", "1") != "0"
 
 
 class _EngineAbort(Exception):

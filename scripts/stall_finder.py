@@ -28,6 +28,18 @@ if "--smi" in sys.argv:
                            stdout=subprocess.DEVNULL)
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 12
 thr = float(sys.argv[2]) if len(sys.argv) > 2 else 5.0
+if "--update" in sys.argv:
+    from paper_2001_11619_b200 import update
+    cur = fa()
+    seq = configs.hole_move_sequence(b, n + 1)
+    cur = update(cur, seq[0][2], seq[0][3])
+    torch.cuda.synchronize()
+    seq_it = iter(seq[1:])
+    def fa():
+        global cur
+        h_, d_, nb_, rep_ = next(seq_it)
+        cur = update(cur, nb_, rep_)
+        return None
 with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
     for it in range(n):
         if "--flush" in sys.argv:
