@@ -288,7 +288,8 @@ int skb_engine_start(const void* const* tree, int64_t depth, const double* root,
                      int64_t* const* store, int64_t cap, const double* const* geo, int64_t P,
                      double tol, void* stream, int64_t lev_lo, int64_t max_level_ints,
                      int64_t* handle);
-/* Block until level L is done: sizes = {rc, B, na, box0, o_int, o_act}; ptrs =
+/* Block until level L is done: sizes = {rc, B, na, box0, o_int, o_act, h2d bytes,
+ * d2h bytes}; ptrs =
  * {act_off, act, rows, A, m_q, perm, k, steps, gap (host), stack, dbuf, dup
  * (device), event}.  Host arrays stay valid until skb_engine_free.          */
 int skb_engine_wait(int64_t handle, int64_t L, int64_t* sizes, int64_t* ptrs);

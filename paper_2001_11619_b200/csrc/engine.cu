@@ -52,6 +52,7 @@ struct LevelOut {
   int64_t* dup = nullptr;        // uploaded descriptors (device): act_off | act | ...
   int64_t o_int = 0;             // byte offset of perm in dbuf
   int64_t o_act = 0;             // element offset of act in dup
+  int64_t h2d = 0, d2h = 0;      // bytes moved host<->device for this level
   cudaEvent_t ev = nullptr;
 };
 
@@ -171,6 +172,7 @@ int run_level(Engine& E, int64_t L, LevelOut& R) {
   const int64_t o_pw = add(pw.data(), B);
   const int64_t o_so = add(stack_off.data(), B);
   if ((rc = upload(pk.data(), (int64_t)pk.size(), s, &R.dup))) return rc;
+  R.h2d += 8 * (int64_t)pk.size();
   if ((rc = skb_assemble_stack(E.pos, E.nrm, E.w, B, R.dup + o_ao, R.dup + R.o_act, R.dup + o_fo,
                                R.dup + o_f, (const double*)(R.dup + o_pt),
                                (const double*)(R.dup + o_pn), (const double*)(R.dup + o_pw),
@@ -206,6 +208,7 @@ int run_level(Engine& E, int64_t L, LevelOut& R) {
   const size_t hb = (size_t)(dbytes - o_gap);
   if (hb > E.pinned_size) return 9;
   SKB_RET(cudaMemcpyAsync(E.pinned, R.dbuf + o_gap, hb, cudaMemcpyDeviceToHost, s));
+  R.d2h += (int64_t)hb;
   SKB_RET(cudaEventRecord(R.ev, s));
   SKB_RET(cudaEventSynchronize(R.ev));
   const double* gap = (const double*)E.pinned;
@@ -339,7 +342,7 @@ int skb_engine_start(const void* const* tree, int64_t depth, const double* root,
   return 0;
 }
 
-// Block until level L is compressed; sizes = {rc, B, na, box0, o_int, o_act}; ptrs =
+// Block until level L is compressed; sizes = {rc, B, na, box0, o_int, o_act, h2d, d2h}; ptrs =
 // {act_off, act, rows, A, mq, perm(i32), k(i32), steps(i32), gap(f64), stack, dbuf, dup, event}
 int skb_engine_wait(int64_t handle, int64_t L, int64_t* sizes, int64_t* ptrs) {
   Engine* E = (Engine*)handle;
@@ -350,6 +353,8 @@ int skb_engine_wait(int64_t handle, int64_t L, int64_t* sizes, int64_t* ptrs) {
   }
   sizes[0] = R.rc; sizes[1] = R.B; sizes[2] = R.na; sizes[3] = R.box0; sizes[4] = R.o_int;
   sizes[5] = R.o_act;
+  sizes[6] = R.h2d;
+  sizes[7] = R.d2h;
   ptrs[0] = (int64_t)R.act_off.data(); ptrs[1] = (int64_t)R.act.data(); ptrs[2] = (int64_t)R.rows.data();
   ptrs[3] = (int64_t)R.A.data(); ptrs[4] = (int64_t)R.mq.data(); ptrs[5] = (int64_t)R.perm.data();
   ptrs[6] = (int64_t)R.k.data(); ptrs[7] = (int64_t)R.steps.data(); ptrs[8] = (int64_t)R.gap.data();

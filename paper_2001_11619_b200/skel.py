@@ -1481,7 +1481,7 @@ class _Engine:
         lead = os.environ.get("SKB_ENGINE_LEAD")
         if lead is not None:
             self.lib.skb_engine_set_lead(self.h, int(lead))
-        self.sizes = np.zeros(6, np.int64)
+        self.sizes = np.zeros(8, np.int64)
         self.ptrs = np.zeros(13, np.int64)
 
     @staticmethod
@@ -1492,7 +1492,9 @@ class _Engine:
     def wait(self, L) -> dict:
         with _ht("E.wait"):
             self.lib.skb_engine_wait(self.h, L, self.sizes.ctypes.data, self.ptrs.ctypes.data)
-        rc, B, na, box0, o_int, o_act = (int(v) for v in self.sizes)
+        rc, B, na, box0, o_int, o_act, h2d, d2h = (int(v) for v in self.sizes)
+        IO["h2d"] += h2d
+        IO["d2h"] += d2h
         if rc:
             raise _lib.SkbError(f"native level engine failed at level {L} (rc {rc})")
         p = self.ptrs
