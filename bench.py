@@ -259,9 +259,12 @@ def main():
     e2e_value, _ = aggregate(e2e_times, world, n_unk, reduce_max)
 
     line = None
+    fp64 = None
     if rank == 0:
         peaks = _peaks()
-        fp64 = measure_fp64_peak(torch)
+        # the DGEMM peak probe (2 x 512 MB operands) runs after the secondary
+        # measurements; roofline is filled in then
+        fp64 = 35.5
         hbm = float(peaks.get("hbm_gbs", 6650.0))
         # dominant kernel family by device time; DRAM traffic per launch from the
         # committed ncu capture of one factorization (profiles/, scripts/ncu_traffic.py)
@@ -338,6 +341,14 @@ def main():
                                 "sample": f"{len(times_c)} full cfg2 factorization(s) with oracle/skel_oracle.py "
                                           f"(numpy/scipy restatement of the reference, BLAS 1 thread)"}
     if rank == 0:
+        gc_ = __import__("gc")
+        gc_.collect()
+        fp64 = measure_fp64_peak(torch)
+        line["fp64_dgemm_tflops"] = fp64
+        roof = line["roofline"]
+        if roof["unit"] == "TFLOP/s":
+            roof["peak"] = fp64
+            roof["frac"] = roof["achieved"] / fp64
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.barrier()

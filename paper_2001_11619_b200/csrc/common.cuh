@@ -243,8 +243,12 @@ SideStreams& side();
 inline int side_init() {
   SideStreams& S = side();
   if (!S.init) {
+    // the size classes of the QR / QRCP are the factorization's critical path:
+    // highest stream priority, so they win the SMs over the Schur / sweep work
+    int least = 0, greatest = 0;
+    SKB_RET(cudaDeviceGetStreamPriorityRange(&least, &greatest));
     for (int i = 0; i < SideStreams::kN; ++i) {
-      SKB_RET(cudaStreamCreateWithFlags(&S.st[i], cudaStreamNonBlocking));
+      SKB_RET(cudaStreamCreateWithPriority(&S.st[i], cudaStreamNonBlocking, greatest));
       SKB_RET(cudaEventCreateWithFlags(&S.join_ev[i], cudaEventDisableTiming));
     }
     SKB_RET(cudaEventCreateWithFlags(&S.fork_ev, cudaEventDisableTiming));

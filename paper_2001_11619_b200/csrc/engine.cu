@@ -19,6 +19,7 @@
 #include <string.h>
 
 #include <atomic>
+#include <chrono>
 #include <condition_variable>
 #include <mutex>
 #include <thread>
@@ -93,7 +94,25 @@ int64_t append(Engine& E, const int64_t* a, int64_t n) {
   return o;
 }
 
+struct ETimer {
+  static bool on() {
+    static const bool v = getenv("SKB_ENGINE_TIMING") != nullptr;
+    return v;
+  }
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  char buf[512];
+  int n = 0;
+  void tick(const char* name) {
+    if (!on()) return;
+    const auto t = std::chrono::steady_clock::now();
+    n += snprintf(buf + n, sizeof(buf) - n, " %s %.0f", name,
+                  std::chrono::duration<double, std::micro>(t - t0).count());
+    t0 = t;
+  }
+};
+
 int run_level(Engine& E, int64_t L, LevelOut& R) {
+  ETimer tm;
   const int64_t b0 = E.level_start[L], B = E.level_start[L + 1] - b0;
   R.B = B;
   R.box0 = b0;
@@ -117,6 +136,7 @@ int run_level(Engine& E, int64_t L, LevelOut& R) {
       E.a_len[i] = (int64_t)tmp.size();
     }
   }
+  tm.tick("internal");
   R.act_off.assign(B + 1, 0);
   for (int64_t b = 0; b < B; ++b) R.act_off[b + 1] = R.act_off[b] + E.a_len[idx[b]];
   R.na = R.act_off[B];
@@ -136,9 +156,11 @@ int run_level(Engine& E, int64_t L, LevelOut& R) {
                             E.px, E.py, far_off.data(), far.data(), (int64_t)far.size(), &need);
   }
   if (rc) return 8;
+  tm.tick("far");
   const int64_t P = E.P;
   std::vector<double> pts(B * P * 2), pn(B * P * 2), pw(B);
   skb_host_proxies(B, idx.data(), E.center, E.hw, E.factor, P, E.cs, pts.data(), pn.data(), pw.data());
+  tm.tick("proxies");
   // stack layout (column-major per box, ld = rows)
   R.rows.resize(B);
   std::vector<int64_t> nB(B), stack_off(B + 1, 0);
@@ -171,13 +193,16 @@ int run_level(Engine& E, int64_t L, LevelOut& R) {
   const int64_t o_pn = add(pn.data(), B * P * 2);
   const int64_t o_pw = add(pw.data(), B);
   const int64_t o_so = add(stack_off.data(), B);
+  tm.tick("pack");
   if ((rc = upload(pk.data(), (int64_t)pk.size(), s, &R.dup))) return rc;
+  tm.tick("upload");
   R.h2d += 8 * (int64_t)pk.size();
   if ((rc = skb_assemble_stack(E.pos, E.nrm, E.w, B, R.dup + o_ao, R.dup + R.o_act, R.dup + o_fo,
                                R.dup + o_f, (const double*)(R.dup + o_pt),
                                (const double*)(R.dup + o_pn), (const double*)(R.dup + o_pw),
                                (int32_t)P, R.dup + o_so, R.stack, maxnB, maxitems, s)))
     return rc;
+  tm.tick("asm");
   // Householder pre-reduction of the tall stacks (dense.py:56-59)
   R.A.resize(B);
   R.mq.resize(B);
@@ -191,6 +216,7 @@ int run_level(Engine& E, int64_t L, LevelOut& R) {
   if (!pm.empty() && (rc = geqrf_batched((int64_t)pm.size(), pm.data(), pn_.data(), pm.data(),
                                          pA.data(), s)))
     return rc;
+  tm.tick("geqrf");
   // QRCP with rank at tol (dense.py:60-68)
   const int64_t na = R.na;
   const int64_t o_gap = 8 * std::max<int64_t>(na, 1);
@@ -210,7 +236,9 @@ int run_level(Engine& E, int64_t L, LevelOut& R) {
   SKB_RET(cudaMemcpyAsync(E.pinned, R.dbuf + o_gap, hb, cudaMemcpyDeviceToHost, s));
   R.d2h += (int64_t)hb;
   SKB_RET(cudaEventRecord(R.ev, s));
+  tm.tick("qrcp");
   SKB_RET(cudaEventSynchronize(R.ev));
+  tm.tick("WAIT");
   const double* gap = (const double*)E.pinned;
   const int32_t* ih = (const int32_t*)(E.pinned + (R.o_int - o_gap));
   R.gap.assign(gap, gap + B);
@@ -227,6 +255,8 @@ int run_level(Engine& E, int64_t L, LevelOut& R) {
     E.s_start[i] = o;
     E.s_len[i] = kk;
   }
+  tm.tick("skel");
+  if (ETimer::on()) fprintf(stderr, "engine level %lld (%lld boxes):%s us\n", (long long)L, (long long)B, tm.buf);
   return 0;
 }
 
