@@ -291,8 +291,15 @@ int skb_engine_start(const void* const* tree, int64_t depth, const double* root,
 /* Block until level L is done: sizes = {rc, B, na, box0, o_int, o_act, h2d bytes,
  * d2h bytes}; ptrs =
  * {act_off, act, rows, A, m_q, perm, k, steps, gap (host), stack, dbuf, dup
- * (device), event}.  Host arrays stay valid until skb_engine_free.          */
+ * (device), event, idx (host: the compressed boxes)}.  Host arrays stay valid until skb_engine_free.          */
 int skb_engine_wait(int64_t handle, int64_t L, int64_t* sizes, int64_t* ptrs);
+/* Update mode (start with lev_lo <= 0 = deferred): recompress only the boxes
+ * with todo[i] != 0; clean boxes take their skeleton from clean_off/clean_skel
+ * (CSR over all boxes).  skb_engine_go starts a deferred engine.  In update
+ * mode sizes[1] counts the recompressed boxes and ptrs[13] lists them.       */
+int skb_engine_set_update(int64_t handle, const uint8_t* todo, const int64_t* clean_off,
+                          const int64_t* clean_skel);
+int skb_engine_go(int64_t handle);
 /* stream waits for level L's compression */
 int skb_engine_stream_wait(int64_t handle, int64_t L, void* stream);
 /* free level L's device buffers, stream-ordered on stream */

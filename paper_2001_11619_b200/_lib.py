@@ -69,6 +69,8 @@ SIGNATURES = {
     "skb_engine_release": [_i64, _i64, _vp],
     "skb_engine_stop": [_i64],
     "skb_engine_ack": [_i64, _i64],
+    "skb_engine_set_update": [_i64, _vp, _vp, _vp],
+    "skb_engine_go": [_i64],
     "skb_engine_set_lead": [_i64, _i64],
     "skb_engine_free": [_i64, _vp],
     # native host runtime (host arrays only, no device)

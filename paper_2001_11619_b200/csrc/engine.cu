@@ -54,6 +54,7 @@ struct LevelOut {
   int64_t o_int = 0;             // byte offset of perm in dbuf
   int64_t o_act = 0;             // element offset of act in dup
   int64_t h2d = 0, d2h = 0;      // bytes moved host<->device for this level
+  std::vector<int64_t> idx;      // boxes compressed (all of the level, or the dirty ones)
   cudaEvent_t ev = nullptr;
 };
 
@@ -84,6 +85,11 @@ struct Engine {
   char* pinned = nullptr;
   size_t pinned_size = 0;
   bool* shared_pinned = nullptr;   // set: the pinned buffer is the shared one
+  // update mode: boxes to recompress (uint8 per box) and the clean boxes'
+  // skeletons (CSR over boxes); nullptr = factor every box
+  const uint8_t* todo = nullptr;
+  const int64_t* clean_off = nullptr;
+  const int64_t* clean_skel = nullptr;
 };
 
 int64_t append(Engine& E, const int64_t* a, int64_t n) {
@@ -113,16 +119,20 @@ struct ETimer {
 
 int run_level(Engine& E, int64_t L, LevelOut& R) {
   ETimer tm;
-  const int64_t b0 = E.level_start[L], B = E.level_start[L + 1] - b0;
-  R.B = B;
+  const int64_t b0 = E.level_start[L], nall = E.level_start[L + 1] - b0;
   R.box0 = b0;
-  if (B == 0) return 0;
-  std::vector<int64_t> idx(B);
-  for (int64_t b = 0; b < B; ++b) idx[b] = b0 + b;
-  // assign_internal_actives: active = concat of the children's skeletons in child order
+  // boxes to compress: all of the level (factor) or the dirty ones (update)
+  std::vector<int64_t> idx;
+  for (int64_t b = 0; b < nall; ++b)
+    if (!E.todo || E.todo[b0 + b]) idx.push_back(b0 + b);
+  const int64_t B = (int64_t)idx.size();
+  R.B = B;
+  R.idx = idx;
+  // assign_internal_actives (every box of the level: clean colleagues feed the
+  // dirty boxes' far fields): active = concat of the children's skeletons
   {
     std::vector<int64_t> tmp;
-    for (int64_t i : idx) {
+    for (int64_t i = b0; i < b0 + nall; ++i) {
       if (E.leaf[i]) continue;
       tmp.clear();
       for (int q = 0; q < 4; ++q) {
@@ -137,6 +147,17 @@ int run_level(Engine& E, int64_t L, LevelOut& R) {
     }
   }
   tm.tick("internal");
+  // clean boxes (update): skeletons carried over from the previous factorization
+  if (E.todo)
+    for (int64_t i = b0; i < b0 + nall; ++i) {
+      if (E.todo[i]) continue;
+      const int64_t n0 = E.clean_off[i], nk = E.clean_off[i + 1] - n0;
+      const int64_t o = append(E, E.clean_skel + n0, nk);
+      if (o < 0) return 7;
+      E.s_start[i] = o;
+      E.s_len[i] = nk;
+    }
+  if (B == 0) return 0;
   R.act_off.assign(B + 1, 0);
   for (int64_t b = 0; b < B; ++b) R.act_off[b + 1] = R.act_off[b] + E.a_len[idx[b]];
   R.na = R.act_off[B];
@@ -339,10 +360,11 @@ int skb_engine_start(const void* const* tree, int64_t depth, const double* root,
   E->P = P;
   E->tol = tol;
   E->s = (cudaStream_t)stream;
-  E->lev_lo = lev_lo;
+  const bool deferred = lev_lo <= 0;     // started later by skb_engine_go
+  E->lev_lo = deferred ? 1 : lev_lo;
   cudaGetDevice(&E->dev);
   E->out.resize(depth + 1);
-  for (int64_t L = lev_lo; L <= depth; ++L)
+  for (int64_t L = E->lev_lo; L <= depth; ++L)
     SKB_RET(cudaEventCreateWithFlags(&E->out[L].ev, cudaEventDisableTiming));
   // pinned landing buffer for the per-level device->host copy: kept across
   // factorizations (cudaHostAlloc / cudaFreeHost would synchronise the device)
@@ -367,8 +389,27 @@ int skb_engine_start(const void* const* tree, int64_t depth, const double* root,
       E->pinned_size = want;
     }
   }
-  E->th = std::thread(engine_main, E);
+  if (!deferred) E->th = std::thread(engine_main, E);
   *handle = (int64_t)E;
+  return 0;
+}
+
+int skb_engine_go(int64_t handle) {
+  Engine* E = (Engine*)handle;
+  if (!E->th.joinable()) E->th = std::thread(engine_main, E);
+  return 0;
+}
+
+// Update mode: compress only the boxes with todo[i] != 0; clean boxes take
+// their skeleton from clean_off/clean_skel (CSR over all boxes).  Call right
+// after skb_engine_start with lev_lo = depth + 1 (engine idle), then
+// skb_engine_go to run.
+int skb_engine_set_update(int64_t handle, const uint8_t* todo, const int64_t* clean_off,
+                          const int64_t* clean_skel) {
+  Engine* E = (Engine*)handle;
+  E->todo = todo;
+  E->clean_off = clean_off;
+  E->clean_skel = clean_skel;
   return 0;
 }
 
@@ -390,6 +431,7 @@ int skb_engine_wait(int64_t handle, int64_t L, int64_t* sizes, int64_t* ptrs) {
   ptrs[6] = (int64_t)R.k.data(); ptrs[7] = (int64_t)R.steps.data(); ptrs[8] = (int64_t)R.gap.data();
   ptrs[9] = (int64_t)R.stack; ptrs[10] = (int64_t)R.dbuf; ptrs[11] = (int64_t)R.dup;
   ptrs[12] = (int64_t)R.ev;
+  ptrs[13] = (int64_t)R.idx.data();
   return 0;
 }
 

@@ -1454,7 +1454,7 @@ def _i64p(vals):
 class _Engine:
     """Host handle of the native level engine (csrc/engine.cu)."""
 
-    def __init__(self, ctx: "_Ctx", store: "ActStore"):
+    def __init__(self, ctx: "_Ctx", store: "ActStore", update=None):
         t, g = ctx.t, ctx.g
         nv = _tree_native(t)
         self.lib = _lib.load()
@@ -1473,16 +1473,23 @@ class _Engine:
                      self.cs.ctypes.data])
         self.h = ctypes.c_int64(0)
         rc = self.lib.skb_engine_start(tree, t.depth, nv["root"].ctypes.data, ctx.factor, st,
-                                       len(store.big), geo, ctx.P, ctx.tol, _stream(), 1,
+                                       len(store.big), geo, ctx.P, ctx.tol, _stream(),
+                                       0 if update is not None else 1,
                                        2 * t.n_nodes + 3 * len(t.lev) + 16, ctypes.byref(self.h))
         if rc:
             raise _lib.SkbError(f"skb_engine_start returned {rc}")
         self.h = self.h.value
+        if update is not None:
+            self._upd = update                      # kept alive while the engine runs
+            todo, coff, cskel = update
+            self.lib.skb_engine_set_update(self.h, todo.ctypes.data, coff.ctypes.data,
+                                           cskel.ctypes.data)
+            self.lib.skb_engine_go(self.h)
         lead = os.environ.get("SKB_ENGINE_LEAD")
         if lead is not None:
             self.lib.skb_engine_set_lead(self.h, int(lead))
         self.sizes = np.zeros(8, np.int64)
-        self.ptrs = np.zeros(13, np.int64)
+        self.ptrs = np.zeros(14, np.int64)
 
     @staticmethod
     def _arr(addr, n, dt):
@@ -1498,12 +1505,14 @@ class _Engine:
         if rc:
             raise _lib.SkbError(f"native level engine failed at level {L} (rc {rc})")
         p = self.ptrs
+        if B == 0:
+            return None
         act_off = self._arr(p[0], B + 1, np.int64)
         act = self._arr(p[1], na, np.int64)
         rows = self._arr(p[2], B, np.int64)
         nB = np.diff(act_off)
         dbuf, dup = int(p[10]), int(p[11])
-        h = dict(idx=np.arange(box0, box0 + B, dtype=np.int64), act_off=act_off, act=act, nB=nB,
+        h = dict(idx=self._arr(p[13], B, np.int64), act_off=act_off, act=act, nB=nB,
                  rows=rows, pre=rows > nB, m_q=self._arr(p[4], B, np.int64),
                  A=self._arr(p[3], B, np.int64), lda=rows, engine=self, lev=L,
                  dev=(dup, dup + 8 * o_act, dbuf + o_int),
@@ -1550,7 +1559,60 @@ def _run_levels_engine(ctx: _Ctx):
         eng.close(stop=True)
 
 
-def _engine_loop(ctx, eng, store):
+def _clean_skeletons(t: Tree, old_levels: dict, dmask):
+    """Skeletons of the clean boxes of an update, carried over from the previous
+    factorization (reference run_level reuse path, skel.py:342-353), as a CSR
+    over all boxes of the new tree (dirty boxes empty)."""
+    nbox = len(t.lev)
+    lens = np.zeros(nbox, np.int64)
+    parts = []
+    for lev in range(1, t.depth + 1):
+        idx = t.level_indices(lev)
+        clean = idx[~dmask[idx]]
+        if len(clean) == 0:
+            continue
+        L = old_levels.get(lev)
+        if L is None:
+            raise _EngineAbort()
+        ot, ob = L.tree, L.batch
+        side = np.int64(1) << np.int64(lev)
+        oc = ot.ix[L.idx] * side + ot.iy[L.idx]
+        nc = t.ix[clean] * side + t.iy[clean]
+        pos = np.searchsorted(oc, nc)
+        if np.any(pos >= len(oc)) or np.any(oc[np.minimum(pos, len(oc) - 1)] != nc):
+            raise _EngineAbort()
+        k = ob.k[pos]
+        _, pp = _seg_gather(ob.perm.astype(np.int64), ob.act_off[pos], k)
+        sk = ob.act[np.repeat(ob.act_off[pos], k) + pp]
+        lens[clean] = k
+        parts.append((clean, k, sk))
+    off = np.zeros(nbox + 1, np.int64)
+    np.cumsum(lens, out=off[1:])
+    flat = np.zeros(max(int(off[-1]), 1), np.int64)
+    for clean, k, sk in parts:
+        _, dst = _seg_gather(np.arange(len(flat)), off[clean], k)
+        flat[dst] = sk
+    return off, flat
+
+
+def _run_levels_engine_update(ctx: _Ctx, old: dict, dmask):
+    """_run_levels(reuse=old) on the native engine: only the dirty boxes are
+    recompressed; clean boxes keep the previous factors."""
+    t = ctx.t
+    coff, cskel = _clean_skeletons(t, old, dmask)
+    store = ActStore(t, engine=True)
+    ctx.store = store
+    eng = _Engine(ctx, store, update=(np.ascontiguousarray(dmask, np.uint8), coff, cskel))
+    try:
+        with torch.cuda.stream(ctx.sstream):
+            out = _engine_loop(ctx, eng, store, reuse=old, dirty=dmask)
+        torch.cuda.current_stream().wait_stream(ctx.sstream)
+        return out
+    finally:
+        eng.close(stop=True)
+
+
+def _engine_loop(ctx, eng, store, reuse=None, dirty=None):
         t = ctx.t
         pairs = t.hole_pairs(np.asarray(ctx.b.offsets, np.int64)) if ctx.b.n_holes else None
         pipe = _AugPipe(ctx)
@@ -1559,20 +1621,31 @@ def _engine_loop(ctx, eng, store):
         prev = None
         for lev in range(t.depth, 0, -1):
             h = eng.wait(lev)
-            bt = BoxBatch(h["idx"], h["act_off"], h["act"])
-            bt.perm[:] = h["perm"]
-            bt.k[:] = h["k"]
-            bt.steps[:] = h["steps"]
-            bt.gap[:] = h["gap"]
-            bt._launch = h
-            if prev is not None:
+            bt_new = None
+            if h is not None:
+                bt_new = BoxBatch(h["idx"], h["act_off"], h["act"])
+                bt_new.perm[:] = h["perm"]
+                bt_new.k[:] = h["k"]
+                bt_new.steps[:] = h["steps"]
+                bt_new.gap[:] = h["gap"]
+                bt_new._launch = h
+            if prev is not None and prev[1] is not None:
                 with _ht("migrate"):
                     pb = prev[1]
                     pb.resolve()
                     if (((pb.info >= 0) | (pb.ratio < PIVOT_RATIO_FLOOR)) & (pb.k < pb.nB)).any():
                         raise _EngineAbort()
-            with _ht("schur"):
-                ctx.schur(bt, store)
+            if reuse is None:
+                bt = bt_new
+            else:
+                if bt_new is not None:
+                    ctx.layout(bt_new)                # the merge copies factor pointers
+                idx_all = t.level_indices(lev)
+                todo = bt_new.idx if bt_new is not None else np.zeros(0, np.int64)
+                bt = _merge_level(ctx, idx_all, store, todo, bt_new, reuse)
+            if bt_new is not None:
+                with _ht("schur"):
+                    ctx.schur(bt_new, store)
             store.xss[bt.idx] = bt.ptr["Xss"]
             if prev is not None:
                 with _ht("aug_submit"):
@@ -1580,8 +1653,8 @@ def _engine_loop(ctx, eng, store):
             with _ht("levelfactors"):
                 cols_off, cols = _hole_columns(t, ctx.b, bt.idx, pairs)
                 levels.append(LevelFactors(lev, t, bt, cols_off, cols))
-            prev = (lev, bt)
-        if prev is not None:
+            prev = (lev, bt_new)
+        if prev is not None and prev[1] is not None:
             pb = prev[1]
             pb.resolve()
             if (((pb.info >= 0) | (pb.ratio < PIVOT_RATIO_FLOOR)) & (pb.k < pb.nB)).any():
@@ -1589,7 +1662,7 @@ def _engine_loop(ctx, eng, store):
         eng.close()
         if levels:
             pipe.submit(levels[-1])
-        return levels, store, sum(len(L.idx) for L in levels)
+        return levels, store, sum(len(L.idx) for L in levels) if reuse is None else 0
 
 
 def _run_levels(ctx: _Ctx, reuse=None, dirty=None):
@@ -1774,7 +1847,16 @@ def update(fct: Factorization, b_new, report, workers: int = 1) -> Factorization
     ctx = _Ctx(fct.spec, b_new, t_new, fct.tol, fct.proxy_count, fct.proxy_factor)
     torch.cuda.current_stream().synchronize()
     with torch.cuda.stream(_compress_stream()):
-        levels, store, n_recomp = _run_levels(ctx, reuse=old, dirty=dmask)
+        levels = None
+        if _ENGINE_ON and not _Prof.enabled:
+            try:
+                levels, store, n_recomp = _run_levels_engine_update(ctx, old, dmask)
+            except _EngineAbort:
+                torch.cuda.current_stream().wait_stream(ctx.sstream)
+                ctx = _Ctx(fct.spec, b_new, t_new, fct.tol, fct.proxy_count, fct.proxy_factor)
+                levels = None
+        if levels is None:
+            levels, store, n_recomp = _run_levels(ctx, reuse=old, dirty=dmask)
         rd, E_root, top, ipiv, UH, PsiV, UH_div, q, ratio = _finish_top(ctx, levels, store, ctx.pipe)
     torch.cuda.synchronize()
     stats = {"k_per_level": {L.lev: int(L.k.max(initial=0)) for L in levels},
