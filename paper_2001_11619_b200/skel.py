@@ -1599,10 +1599,13 @@ def _run_levels_engine_update(ctx: _Ctx, old: dict, dmask):
     """_run_levels(reuse=old) on the native engine: only the dirty boxes are
     recompressed; clean boxes keep the previous factors."""
     t = ctx.t
-    coff, cskel = _clean_skeletons(t, old, dmask)
-    store = ActStore(t, engine=True)
+    with _ht("U.clean"):
+        coff, cskel = _clean_skeletons(t, old, dmask)
+    with _ht("U.store"):
+        store = ActStore(t, engine=True)
     ctx.store = store
-    eng = _Engine(ctx, store, update=(np.ascontiguousarray(dmask, np.uint8), coff, cskel))
+    with _ht("U.engine"):
+        eng = _Engine(ctx, store, update=(np.ascontiguousarray(dmask, np.uint8), coff, cskel))
     try:
         with torch.cuda.stream(ctx.sstream):
             out = _engine_loop(ctx, eng, store, reuse=old, dirty=dmask)
@@ -1837,10 +1840,12 @@ def update(fct: Factorization, b_new, report, workers: int = 1) -> Factorization
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     try:
-        t_new = refit_tree(fct.tree, b_new.positions)
+        with _ht("U.refit"):
+            t_new = refit_tree(fct.tree, b_new.positions)
     except ValueError as e:
         raise RootBoxExceededError("perturbed node escaped the root box; refactor with a fresh tree") from e
-    dmask = dirty_mask(fct.tree, t_new, b_new, report, fct.proxy_factor)
+    with _ht("U.dirty"):
+        dmask = dirty_mask(fct.tree, t_new, b_new, report, fct.proxy_factor)
     if not np.array_equal(report.old_to_new, np.arange(len(report.old_to_new))):
         raise NotImplementedError("only DOF-preserving edits (hole moves) are supported")
     old = {L.lev: L for L in fct.levels}
