@@ -40,7 +40,7 @@ int main(int argc, char** argv) {
     const int own = (p + 1) % CL;
     long long* q = t + own * 512 + p * 4;
     long long* o = t + (p % CL) * 512 + p * 4;
-    printf("step %2d: at %7lld  next-owner r%d: ahead %6lld panel %6lld rest %6lld | r%d rest %6lld\n", p,
+    printf("step %2d: at %7lld  next-owner r%d: copy %6lld apply %6lld panel %6lld | r%d total %6lld\n", p,
            q[0] - t0, own, q[1] - q[0], q[2] - q[1], q[3] - q[2], p % CL, o[3] - o[0]);
   }
   return 0;
