@@ -16,12 +16,16 @@ namespace skb {
 int gemm_grouped(SkbGemm* probs, int64_t nprob, cudaStream_t s);
 
 constexpr int LB = 64;  // LU block width
+#ifndef SKB_PANEL_NT
+#define SKB_PANEL_NT 512    // threads of the panel CTA (1024: no gain at n=849)
+#endif
 
 struct LuPanel {
   double* A;
   int64_t n, ld, j0, jb;
   int32_t* ipiv;
   int32_t* info;
+  int32_t* swp;   // [2*LB] destination rows (-1: skip), [2*LB] source rows, relative to j0
 };
 
 struct AbsMax {
@@ -33,80 +37,200 @@ __device__ __forceinline__ AbsMax absmax_merge(AbsMax a, AbsMax b) {
   return (b.v > a.v || (b.v == a.v && b.idx < a.idx)) ? b : a;
 }
 
-// dgetf2 on the panel A[j0:n, j0:j0+jb], staged column-major in shared memory
-// (contiguous column scans for the pivot search), then the panel's row
-// interchanges are applied to the columns outside the panel (dlaswp).
+// Exact |max| with the lowest row index among ties, over a warp: max of the
+// values, then the minimum index among the lanes holding it.
+__device__ __forceinline__ void warp_absmax(double& v, int& idx) {
+  double m = v;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  idx = __reduce_min_sync(0xffffffffu, v == m ? idx : INT_MAX);
+  v = m;
+}
+
+// dgetf2 on the panel A[j0:n, j0:j0+jb], staged row-major in shared memory
+// with an odd row length (pld = jb | 1: conflict-free 64-bit column scans and
+// row sweeps).  A thread owns rows; it owns the same rows in the update of
+// column c and the pivot search of column c+1, so a column costs two
+// barriers.  The pivot row is copied to s_u with its entries at and left of
+// column c zeroed, so the row update is one predicate-free sweep over 8-column
+// groups (all loads of a group issue before its stores) followed by the
+// multiplier store.  Then the panel's interchanges are composed into one
+// permutation of the touched rows and applied to the columns outside the
+// panel through a shared-memory stage (dlaswp with every load of a chunk in
+// flight at once).
 template <int NT>
 __global__ void __launch_bounds__(NT) k_getf2_panel(const LuPanel* __restrict__ descs) {
-  extern __shared__ double P[];
-  __shared__ AbsMax red[NT / 32];
+  extern __shared__ __align__(16) double P[];
+  constexpr int NW = NT / 32;
+  __shared__ double red_v[NW];
+  __shared__ int red_i[NW];
+  __shared__ __align__(16) double s_u[LB + 8];
+  __shared__ double s_pv;
+  __shared__ int s_piv[LB];
   const LuPanel D = descs[blockIdx.x];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t rows = D.n - D.j0;
+  const int rows = (int)(D.n - D.j0);
   const int jb = (int)D.jb;
-  for (int64_t e = threadIdx.x; e < rows * jb; e += NT) {
-    const int64_t r = e / jb, c = e - r * jb;
-    P[c * rows + r] = D.A[(D.j0 + r) * D.ld + D.j0 + c];
-  }
+  const int pld = jb | 1;
+  const int ng = (jb + 7) >> 3;                      // 8-column groups
+  for (int t = threadIdx.x; t < LB + 8; t += NT) s_u[t] = 0.0;
+  // global loads batched 8 rows deep per lane (one dependent round trip per batch)
+  for (int cc = lane; cc < jb; cc += 32)
+    for (int r0 = warp; r0 < rows; r0 += 8 * NW) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int r = r0 + u * NW;
+        if (r < rows) v[u] = D.A[(D.j0 + r) * D.ld + D.j0 + cc];
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (r0 + u * NW < rows) P[(r0 + u * NW) * pld + cc] = v[u];
+    }
   __syncthreads();
   int info = -1;
   for (int c = 0; c < jb; ++c) {
-    const double* col = P + (int64_t)c * rows;
-    AbsMax loc{-1.0, INT64_MAX};
-    for (int64_t r = c + threadIdx.x; r < rows; r += NT) {
-      const double v = fabs(col[r]);
-      if (v > loc.v) { loc.v = v; loc.idx = r; }
+    double bv = -1.0;
+    int bi = INT_MAX;
+    for (int r = c + threadIdx.x; r < rows; r += NT) {
+      const double v = fabs(P[r * pld + c]);
+      if (v > bv) { bv = v; bi = r; }
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      AbsMax y{__shfl_xor_sync(0xffffffffu, loc.v, o), __shfl_xor_sync(0xffffffffu, loc.idx, o)};
-      loc = absmax_merge(loc, y);
-    }
-    if (lane == 0) red[warp] = loc;
+    warp_absmax(bv, bi);
+    if (lane == 0) { red_v[warp] = bv; red_i[warp] = bi; }
     __syncthreads();
-    AbsMax best = red[0];
-#pragma unroll
-    for (int w = 1; w < NT / 32; ++w) best = absmax_merge(best, red[w]);
-    const int64_t p = best.idx;
-    const double piv = col[p];
-    if (threadIdx.x == 0) D.ipiv[D.j0 + c] = (int32_t)(D.j0 + p);
-    if (piv == 0.0) {
+    double gv = lane < NW ? red_v[lane] : -1.0;
+    int gi = lane < NW ? red_i[lane] : INT_MAX;
+    warp_absmax(gv, gi);
+    const int p = gi == INT_MAX ? c : gi;
+    if (threadIdx.x == 0) {
+      D.ipiv[D.j0 + c] = (int32_t)(D.j0 + p);
+      s_piv[c] = p;
+    }
+    if (gv == 0.0) {       // |pivot| == 0: no interchange, no update
       if (info < 0) info = (int)(D.j0 + c);
-      __syncthreads();
+      __syncthreads();     // red_* are rewritten by the next search
       continue;
     }
-    // every thread has read the pivot before thread c swaps it out of col[p]
-    __syncthreads();
-    if (p != c && threadIdx.x < jb) {
-      double* a = P + (int64_t)threadIdx.x * rows;
-      const double t = a[c]; a[c] = a[p]; a[p] = t;
-    }
-    __syncthreads();
-    const double rinv = 1.0 / piv;
-    for (int64_t r = c + 1 + threadIdx.x; r < rows; r += NT) {
-      const double l = col[r] * rinv;
-      P[(int64_t)c * rows + r] = l;
-      for (int cc = c + 1; cc < jb; ++cc) P[(int64_t)cc * rows + r] -= l * P[(int64_t)cc * rows + c];
-    }
-    __syncthreads();
-  }
-  for (int64_t e = threadIdx.x; e < rows * jb; e += NT) {
-    const int64_t r = e / jb, c = e - r * jb;
-    D.A[(D.j0 + r) * D.ld + D.j0 + c] = P[c * rows + r];
-  }
-  if (threadIdx.x == 0 && info >= 0 && *D.info < 0) *D.info = info;
-  // dlaswp on the columns left and right of the panel
-  for (int64_t col = threadIdx.x; col < D.n - jb; col += NT) {
-    const int64_t cg = col < D.j0 ? col : col + jb;
-    for (int c = 0; c < jb; ++c) {
-      const int64_t p = D.ipiv[D.j0 + c];
-      if (p != D.j0 + c) {
-        double* x = D.A + (D.j0 + c) * D.ld + cg;
-        double* y = D.A + p * D.ld + cg;
-        const double t = *x; *x = *y; *y = t;
+    if (threadIdx.x < jb) {   // pivot row -> s_u (left part zeroed), interchange rows c and p
+      const int k = threadIdx.x;
+      const double t = P[p * pld + k];
+      s_u[k] = k > c ? t : 0.0;
+      if (k == c) s_pv = t;
+      if (p != c) {
+        P[p * pld + k] = P[c * pld + k];
+        P[c * pld + k] = t;
       }
     }
+    __syncthreads();
+    const double rinv = 1.0 / s_pv;
+    const int g0 = c >> 3;
+    for (int r = c + 1 + threadIdx.x; r < rows; r += NT) {
+      double* pr = P + r * pld;
+      const double l = pr[c] * rinv;
+      for (int g = g0; g < ng; ++g) {
+        double* q = pr + 8 * g;
+        const double2* u2 = reinterpret_cast<const double2*>(s_u + 8 * g);
+        double a[8];
+        if (8 * g + 8 <= jb) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) a[k] = q[k];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const double2 u = u2[k];
+            a[2 * k] = a[2 * k] - l * u.x;
+            a[2 * k + 1] = a[2 * k + 1] - l * u.y;
+          }
+#pragma unroll
+          for (int k = 0; k < 8; ++k) q[k] = a[k];
+        } else {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) if (8 * g + k < jb) a[k] = q[k];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const double2 u = u2[k];
+            a[2 * k] = a[2 * k] - l * u.x;
+            a[2 * k + 1] = a[2 * k + 1] - l * u.y;
+          }
+#pragma unroll
+          for (int k = 0; k < 8; ++k) if (8 * g + k < jb) q[k] = a[k];
+        }
+      }
+      pr[c] = l;
+    }
   }
+  __syncthreads();
+  for (int r = warp; r < rows; r += NW) {
+    double* dst = D.A + (D.j0 + r) * D.ld + D.j0;
+    for (int cc = lane; cc < jb; cc += 32) dst[cc] = P[r * pld + cc];
+  }
+  if (threadIdx.x == 0 && info >= 0 && *D.info < 0) *D.info = info;
+  // compose the interchanges (perm[d] = source row of destination d) into a
+  // list of moved rows for k_laswp
+  __syncthreads();
+  int* perm = reinterpret_cast<int*>(P);
+  for (int i = threadIdx.x; i < rows; i += NT) perm[i] = i;
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int c = 0; c < jb; ++c) {
+      const int q = s_piv[c];
+      const int t = perm[c]; perm[c] = perm[q]; perm[q] = t;
+    }
+  __syncthreads();
+  if (threadIdx.x < 2 * LB) {
+    const int t = threadIdx.x;
+    int d = -1, sr = 0;
+    if (t < 2 * jb) {
+      d = t < jb ? t : s_piv[t - jb];
+      if ((t >= jb && d < jb) || perm[d] == d) d = -1;   // listed already / unmoved
+      else sr = perm[d];
+    }
+    D.swp[t] = d;
+    D.swp[2 * LB + t] = sr;
+  }
+}
+
+// dlaswp of one panel on the columns outside it: every CTA stages a 32-column
+// tile of the moved rows (all loads in flight), then writes them to their
+// destinations.  grid = (column tiles, matrices).
+__global__ void __launch_bounds__(256) k_laswp(const LuPanel* __restrict__ descs) {
+  const LuPanel D = descs[blockIdx.y];
+  const int jb = (int)D.jb;
+  const int ncol = (int)D.n - jb;
+  const int k = blockIdx.x * 32 + (threadIdx.x & 31);
+  if (blockIdx.x * 32 >= ncol) return;
+  __shared__ int s_d[2 * LB], s_s[2 * LB];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x < 2 * LB) {
+    s_d[threadIdx.x] = D.swp[threadIdx.x];
+    s_s[threadIdx.x] = D.swp[2 * LB + threadIdx.x];
+  }
+  __syncthreads();
+  double* base = D.A + D.j0 * D.ld;
+  const int g = k < D.j0 ? k : k + jb;
+  const bool on = k < ncol;
+  double v[2 * LB / 8];
+#pragma unroll
+  for (int u = 0; u < 2 * LB / 8; ++u) {
+    const int t = warp + 8 * u;
+    if (on && t < 2 * jb && s_d[t] >= 0) v[u] = base[(int64_t)s_s[t] * D.ld + g];
+  }
+  __syncthreads();   // every load of the tile precedes every store
+#pragma unroll
+  for (int u = 0; u < 2 * LB / 8; ++u) {
+    const int t = warp + 8 * u;
+    if (on && t < 2 * jb && s_d[t] >= 0) base[(int64_t)s_d[t] * D.ld + g] = v[u];
+  }
+  (void)lane;
+}
+
+// a / b from the reciprocal y = 1/b: one residual correction of a*y (the
+// final step of the hardware-style division).  Keeps the upper solves free of
+// the division slow-path call (which forced the x[] register block to spill);
+// every upper solve uses it, so results do not depend on the kernel variant.
+__device__ __forceinline__ double div_rcp(double a, double b, double y) {
+  const double q = a * y;
+  return fma(fma(-b, q, a), y, q);
 }
 
 // In-place triangular solve of a jb-row block B (row-major, ldb) against the
@@ -123,12 +247,14 @@ struct TrsmDesc {
 template <bool UPPER>
 __global__ void __launch_bounds__(256) k_trsm_block(const TrsmDesc* __restrict__ descs) {
   __shared__ double Ls[LB][LB + 1];
+  __shared__ double Linv[LB];
   const TrsmDesc D = descs[blockIdx.y];
   const int jb = (int)D.jb;
   for (int t = threadIdx.x; t < jb * jb; t += blockDim.x) {
     const int i = t / jb, p = t % jb;
     Ls[i][p] = D.L[i * D.ldl + p];
   }
+  if (UPPER && threadIdx.x < jb) Linv[threadIdx.x] = 1.0 / D.L[threadIdx.x * D.ldl + threadIdx.x];
   __syncthreads();
   const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (c >= D.ncols) return;
@@ -155,7 +281,7 @@ __global__ void __launch_bounds__(256) k_trsm_block(const TrsmDesc* __restrict__
 #pragma unroll
       for (int p = LB - 1; p > 0; --p)
         if (p > i && p < jb) s -= Ls[i][p] * x[p];
-      x[i] = s / Ls[i][i];
+      x[i] = div_rcp(s, Ls[i][i], Linv[i]);
     }
   }
 #pragma unroll
@@ -182,7 +308,8 @@ __global__ void __launch_bounds__(128) k_trsm_warp(const TrsmDesc* __restrict__ 
   } else {
     for (int p = jb - 1; p >= 0; --p) {
       double xp = __shfl_sync(0xffffffffu, p < 32 ? x0 : x1, p & 31);
-      xp = xp / D.L[p * D.ldl + p];
+      const double d = D.L[p * D.ldl + p];
+      xp = div_rcp(xp, d, 1.0 / d);
       if (lane == (p & 31)) { if (p < 32) x0 = xp; else x1 = xp; }
       if (lane < p) x0 -= D.L[lane * D.ldl + p] * xp;
       if (lane + 32 < p) x1 -= D.L[(lane + 32) * D.ldl + p] * xp;
@@ -312,15 +439,24 @@ __global__ void __launch_bounds__(NT) k_getrf_small(const SmallLU* __restrict__ 
     __syncthreads();
     const double rinv = 1.0 / piv;
     prev_rinv = rinv;
-    // rank-1 update of the trailing block, one thread per (row, 8-column chunk);
-    // column j itself is only read here and scaled at the next step
+    // rank-1 update of the trailing block, one thread per (row, 8-column chunk),
+    // consecutive threads on consecutive rows (odd row stride: conflict-free);
+    // the chunk's loads all issue before its stores.  Column j itself is only
+    // read here and scaled at the next step
     const int rows = n - j - 1, cols = n - j - 1;
     const int cpr = cols > 0 ? (cols + 7) / 8 : 1;
     for (int e = threadIdx.x; e < rows * cpr; e += NT) {
-      const int r = j + 1 + e / cpr;
-      const int c0 = j + 1 + (e % cpr) * 8;
+      const int q = e / rows;
+      const int r = j + 1 + (e - q * rows);
+      const int c0 = j + 1 + q * 8;
       const double l = M[r * L + j] * rinv;
-      for (int c = c0; c < c0 + 8 && c < n; ++c) M[r * L + c] -= l * M[j * L + c];
+      double a[8], u[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (c0 + k < n) { a[k] = M[r * L + c0 + k]; u[k] = M[j * L + c0 + k]; }
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (c0 + k < n) M[r * L + c0 + k] = a[k] - l * u[k];
     }
     __syncthreads();
   }
@@ -362,21 +498,27 @@ int getrf_batched(int64_t nbox, const SkbMat* a, const int64_t* ipiv, int32_t* i
   std::vector<SkbGemm> gd;
   // panel width: a function of each matrix's own order only (so results do not
   // depend on the batch composition): as wide as shared memory allows (<= 64)
-  constexpr size_t kPanelSmem = 220 * 1024;
+  // (rows are stored with an odd stride PB + 1)
+  constexpr size_t kPanelSmem = 224 * 1024;
   auto pbw = [&](int64_t n) {
     int64_t PB = LB;
-    while (PB > 8 && (size_t)n * PB * sizeof(double) > kPanelSmem) PB /= 2;
+    while (PB > 8 && (size_t)n * (PB + 1) * sizeof(double) > kPanelSmem) PB /= 2;
     return PB;
   };
   int64_t rounds = 0;
   for (int64_t b = 0; b < nbox; ++b)
     if (a[b].rows > kSmallLU) rounds = std::max(rounds, (a[b].rows + pbw(a[b].rows) - 1) / pbw(a[b].rows));
+  int32_t* swp = nullptr;   // moved-row lists of one round's panels (k_laswp)
   if (rounds > 0) {
-    SKB_RET(smem_optin((const void*)k_getf2_panel<512>));
+    SKB_RET(smem_optin((const void*)k_getf2_panel<SKB_PANEL_NT>));
+    int64_t nbig = 0;
+    for (int64_t b = 0; b < nbox; ++b) nbig += a[b].rows > kSmallLU;
+    SKB_RET(cudaMallocAsync(reinterpret_cast<void**>(&swp), sizeof(int32_t) * 4 * LB * nbig, s));
   }
   for (int64_t rd_ = 0; rd_ < rounds; ++rd_) {
     pd.clear(); td.clear(); gd.clear();
     size_t smem = 0;
+    int64_t maxcol = 0;
     for (int64_t b = 0; b < nbox; ++b) {
       const int64_t n = a[b].rows;
       if (n <= kSmallLU) continue;
@@ -384,10 +526,13 @@ int getrf_batched(int64_t nbox, const SkbMat* a, const int64_t* ipiv, int32_t* i
       const int64_t j0 = rd_ * PB;
       if (j0 >= n) continue;
       const int64_t jb = std::min<int64_t>(PB, n - j0), n2 = n - j0 - jb;
-      smem = std::max(smem, sizeof(double) * (size_t)(n - j0) * (size_t)PB);
+      smem = std::max(smem, sizeof(double) * (size_t)(n - j0) * (size_t)(PB + 1));
+      smem = std::max(smem, sizeof(int) * (size_t)(n - j0));   // composed permutation
       double* A = a[b].ptr;
       const int64_t ld = a[b].ld;
-      pd.push_back(LuPanel{A, n, ld, j0, jb, reinterpret_cast<int32_t*>(ipiv[b]), info_out + b});
+      pd.push_back(LuPanel{A, n, ld, j0, jb, reinterpret_cast<int32_t*>(ipiv[b]), info_out + b,
+                           swp + (int64_t)pd.size() * 4 * LB});
+      maxcol = std::max(maxcol, n - jb);
       if (n2 > 0) {
         td.push_back(TrsmDesc{A + j0 * ld + j0, ld, A + j0 * ld + j0 + jb, ld, jb, n2});
         SkbGemm g{};
@@ -404,13 +549,16 @@ int getrf_batched(int64_t nbox, const SkbMat* a, const int64_t* ipiv, int32_t* i
     if ((rc = upload(pd.data(), (int64_t)pd.size(), s, &dp))) return rc;
     {
       ProfScope ps(F_GETRF, s);
-      k_getf2_panel<512><<<(unsigned)pd.size(), 512, smem, s>>>(dp);
+      k_getf2_panel<SKB_PANEL_NT><<<(unsigned)pd.size(), SKB_PANEL_NT, smem, s>>>(dp);
+      SKB_LAUNCH_CHECK();
+      if (maxcol > 0) k_laswp<<<dim3((unsigned)((maxcol + 31) / 32), (unsigned)pd.size()), 256, 0, s>>>(dp);
     }
     SKB_LAUNCH_CHECK();
     cudaFreeAsync(dp, s);
     if ((rc = launch_trsm(td, false, s))) return rc;
     if ((rc = gemm_grouped(gd.data(), (int64_t)gd.size(), s))) return rc;
   }
+  if (swp) cudaFreeAsync(swp, s);
   std::vector<RatioDesc> rd(nbox);
   for (int64_t b = 0; b < nbox; ++b) rd[b] = RatioDesc{a[b].ptr, a[b].rows, a[b].ld};
   RatioDesc* dr = nullptr;

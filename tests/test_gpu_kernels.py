@@ -116,6 +116,26 @@ def test_getrf_singular_reports_index():
     assert int(info.cpu()[0]) == 1     # reference SPEC.md:194-197: SingularPivotError index 1
 
 
+@pytest.mark.parametrize("n", [300, 849])
+def test_getrf_blocked_zero_column(n):
+    """Blocked panel path: an exactly zero column reports its (0-based) index
+    and leaves the other columns' interchanges LAPACK-identical up to it."""
+    rng = np.random.default_rng(7 + n)
+    A = rng.standard_normal((n, n))
+    z = n - 37
+    A[:, z] = 0.0
+    dA = _dev(A)
+    ip = torch.empty(n, dtype=torch.int32, device="cuda")
+    info = torch.empty(1, dtype=torch.int32, device="cuda")
+    ratio = torch.empty(1, dtype=torch.float64, device="cuda")
+    call("skb_getrf_batched", 1, skel._mats(np.array([dA.data_ptr()], np.uint64), [n], [n], [n]),
+         np.array([ip.data_ptr()], np.uint64), info, ratio, skel._stream())
+    torch.cuda.synchronize()
+    assert int(info.cpu()[0]) == z
+    _, piv = sla.lu_factor(A, check_finite=False)
+    assert np.array_equal(ip.cpu().numpy()[:z], piv[:z].astype(np.int32))
+
+
 def _golden_boxes(g, prefix):
     keys = [tuple(k) for k in g[prefix + "keys"]]
     out = {}
