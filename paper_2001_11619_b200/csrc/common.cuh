@@ -75,6 +75,13 @@ PinnedRing& ring();
 // thread (pinned ring, shared-memory opt-in table, profiling timers)
 std::recursive_mutex& host_mutex();
 
+inline int pool_strict(cudaMemPool_t pool) {
+  int zero = 0;
+  SKB_RET(cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowOpportunistic, &zero));
+  SKB_RET(cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &zero));
+  return 0;
+}
+
 inline int ring_stage(const void* host, size_t bytes, cudaStream_t s, void* dev) {
   std::lock_guard<std::recursive_mutex> lk(host_mutex());
   PinnedRing& R = ring();
@@ -86,10 +93,15 @@ inline int ring_stage(const void* host, size_t bytes, cudaStream_t s, void* dev)
     SKB_RET(cudaDeviceGetDefaultMemPool(&pool, dev));
     uint64_t thr = ~0ull;
     SKB_RET(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
-    if (getenv("SKB_POOL_STRICT")) {
-      int zero = 0;
-      SKB_RET(cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowOpportunistic, &zero));
-      SKB_RET(cudaMemPoolSetAttribute(pool, cudaMemPoolReuseAllowInternalDependencies, &zero));
+    // Cross-stream reuse only through explicit event dependencies: a block freed
+    // on one stream is not handed to another stream merely because the freeing
+    // stream has progressed (opportunistic) or by an inserted wait (internal
+    // dependencies).  With those on, repeated engine update chains differed
+    // run to run (~5% of steps, 1-ulp level in the top-level boxes); with them
+    // off they are bitwise repeatable.  SKB_POOL_RELAXED=1 restores the defaults.
+    if (!getenv("SKB_POOL_RELAXED")) {
+      const int prc = pool_strict(pool);
+      if (prc) return prc;
     }
     SKB_RET(cudaHostAlloc((void**)&R.base, PinnedRing::kSize, cudaHostAllocDefault));
   }
@@ -239,6 +251,7 @@ struct SideStreams {
   cudaEvent_t fork_ev, join_ev[kN];
 };
 SideStreams& side();
+void use_engine_side(bool on);
 
 inline int side_init() {
   SideStreams& S = side();
@@ -257,8 +270,12 @@ inline int side_init() {
   return 0;
 }
 
-// side streams 0..n-1 wait for everything enqueued on s so far
+// side streams 0..n-1 wait for everything enqueued on s so far.  Record and
+// waits are one critical section: the events are shared by every caller of
+// this thread's stream set (an interleaved re-record would let a side stream
+// wait on the wrong point of another stream -- a run-to-run race).
 inline int fork_n(cudaStream_t s, int n) {
+  std::lock_guard<std::recursive_mutex> lk(host_mutex());
   SKB_RET((cudaError_t)(-side_init()));
   SideStreams& S = side();
   SKB_RET(cudaEventRecord(S.fork_ev, s));
@@ -268,6 +285,7 @@ inline int fork_n(cudaStream_t s, int n) {
 
 // s waits for everything enqueued on side streams 0..n-1
 inline int join_n(cudaStream_t s, int n) {
+  std::lock_guard<std::recursive_mutex> lk(host_mutex());
   SideStreams& S = side();
   for (int i = 0; i < n; ++i) {
     SKB_RET(cudaEventRecord(S.join_ev[i], S.st[i]));

@@ -21,6 +21,7 @@
 #include <atomic>
 #include <chrono>
 #include <condition_variable>
+#include <functional>
 #include <mutex>
 #include <thread>
 #include <vector>
@@ -85,12 +86,106 @@ struct Engine {
   char* pinned = nullptr;
   size_t pinned_size = 0;
   bool* shared_pinned = nullptr;   // set: the pinned buffer is the shared one
+  int64_t* pack = nullptr;         // pinned staging of the per-level upload
+  int64_t pack_cap = 0;
+  bool shared_pack = false;        // set: pack is the process-wide buffer (g_pack)
+  bool freeing = false;
   // update mode: boxes to recompress (uint8 per box) and the clean boxes'
   // skeletons (CSR over boxes); nullptr = factor every box
   const uint8_t* todo = nullptr;
   const int64_t* clean_off = nullptr;
   const int64_t* clean_skel = nullptr;
 };
+
+// Process-wide pinned staging buffer for the per-level upload (kept across
+// factorizations; one engine at a time, the others stage their own).
+struct PackBuf {
+  int64_t* p = nullptr;
+  int64_t cap = 0;
+  bool busy = false;
+};
+PackBuf& g_pack() {
+  static PackBuf b;
+  return b;
+}
+
+// Grow the engine's pinned staging buffer to n int64 (keeps the contents; the
+// previous level's copy out of it has completed: run_level waits on its event).
+int pack_reserve(Engine& E, int64_t n) {
+  if (n <= E.pack_cap) return 0;
+  const int64_t want = std::max<int64_t>(n + n / 4, (int64_t)1 << 20);
+  int64_t* np = nullptr;
+  SKB_RET(cudaHostAlloc((void**)&np, sizeof(int64_t) * want, cudaHostAllocDefault));
+  if (E.pack) {
+    memcpy(np, E.pack, sizeof(int64_t) * E.pack_cap);
+    cudaFreeHost(E.pack);
+  }
+  E.pack = np;
+  E.pack_cap = want;
+  if (E.shared_pack) {
+    std::lock_guard<std::recursive_mutex> lk(host_mutex());
+    g_pack().p = np;
+    g_pack().cap = want;
+  }
+  return 0;
+}
+
+// Host worker pool for the per-box bookkeeping of a level (far-field lists,
+// proxy rings): one process-wide pool, used by one engine at a time.
+struct Pool {
+  int W = 1;
+  std::vector<std::thread> th;
+  std::mutex m, busy;
+  std::condition_variable cv, cv_done;
+  const std::function<void(int)>* job = nullptr;
+  int64_t gen = 0;
+  int pending = 0;
+  explicit Pool(int w) : W(w < 1 ? 1 : w) {
+    for (int i = 1; i < W; ++i)
+      th.emplace_back([this, i] {
+        int64_t seen = 0;
+        for (;;) {
+          const std::function<void(int)>* f;
+          {
+            std::unique_lock<std::mutex> lk(m);
+            cv.wait(lk, [&] { return gen != seen; });
+            seen = gen;
+            f = job;
+          }
+          (*f)(i);
+          std::lock_guard<std::mutex> lk(m);
+          if (--pending == 0) cv_done.notify_one();
+        }
+      });
+    for (auto& t : th) t.detach();   // process-lifetime workers
+  }
+  // f(part) for part in [0, W); the caller runs part 0
+  void run(const std::function<void(int)>& f) {
+    if (W <= 1) { f(0); return; }
+    std::lock_guard<std::mutex> use(busy);
+    {
+      std::lock_guard<std::mutex> lk(m);
+      job = &f;
+      pending = W - 1;
+      ++gen;
+    }
+    cv.notify_all();
+    f(0);
+    std::unique_lock<std::mutex> lk(m);
+    cv_done.wait(lk, [&] { return pending == 0; });
+  }
+};
+
+Pool& host_pool() {
+  static Pool* p = [] {
+    int w = 8;
+    if (const char* e = getenv("SKB_ENGINE_THREADS")) w = atoi(e);
+    const int hc = (int)std::thread::hardware_concurrency();
+    if (hc > 0) w = std::min(w, std::max(1, hc / 2));
+    return new Pool(w);
+  }();
+  return *p;
+}
 
 int64_t append(Engine& E, const int64_t* a, int64_t n) {
   const int64_t o = *E.fill;
@@ -164,60 +259,99 @@ int run_level(Engine& E, int64_t L, LevelOut& R) {
   R.act.resize(std::max<int64_t>(R.na, 1));
   for (int64_t b = 0; b < B; ++b)
     memcpy(R.act.data() + R.act_off[b], E.big + E.a_start[idx[b]], sizeof(int64_t) * E.a_len[idx[b]]);
-  // far-field DOF lists and proxy rings (native host runtime)
-  std::vector<int64_t> far_off(B + 1), far(4096);
-  int64_t need = 0;
-  int rc = skb_host_far_lists(B, idx.data(), E.center, E.hw, E.nbr, E.lev, E.ix, E.iy, E.leaf,
-                              E.level_start, E.depth, E.root, E.factor, E.big, E.a_start, E.a_len,
-                              E.px, E.py, far_off.data(), far.data(), (int64_t)far.size(), &need);
-  if (rc == 1) {
-    far.resize(need + 1);
-    rc = skb_host_far_lists(B, idx.data(), E.center, E.hw, E.nbr, E.lev, E.ix, E.iy, E.leaf,
-                            E.level_start, E.depth, E.root, E.factor, E.big, E.a_start, E.a_len,
-                            E.px, E.py, far_off.data(), far.data(), (int64_t)far.size(), &need);
-  }
-  if (rc) return 8;
-  tm.tick("far");
+  // One pinned upload, packed in place (int64 units, 16-byte aligned segments):
+  //   act_off | act | pts | pn | pw | stack_off | far_off | far
+  // The proxy rings are written straight into it by the host pool; the far
+  // lists (sizes unknown up front) are copied in by a second pool pass.
   const int64_t P = E.P;
-  std::vector<double> pts(B * P * 2), pn(B * P * 2), pw(B);
-  skb_host_proxies(B, idx.data(), E.center, E.hw, E.factor, P, E.cs, pts.data(), pn.data(), pw.data());
-  tm.tick("proxies");
+  auto al = [](int64_t o) { return (o + 1) & ~(int64_t)1; };
+  const int64_t o_ao = 0;
+  R.o_act = al(o_ao + B + 1);
+  const int64_t o_pt = al(R.o_act + (int64_t)R.act.size());
+  const int64_t o_pn = al(o_pt + B * P * 2);
+  const int64_t o_pw = al(o_pn + B * P * 2);
+  const int64_t o_so = al(o_pw + B);
+  const int64_t o_fo = al(o_so + B);
+  const int64_t o_f = al(o_fo + B + 1);
+  int rc = 0;
+  if ((rc = pack_reserve(E, o_f + 4096))) return rc;
+  int64_t* pk = E.pack;
+  memcpy(pk + o_ao, R.act_off.data(), sizeof(int64_t) * (B + 1));
+  memcpy(pk + R.o_act, R.act.data(), sizeof(int64_t) * R.act.size());
+  // far-field DOF lists and proxy rings (native host runtime), boxes split
+  // over the host pool in contiguous parts, concatenated in box order
+  Pool& pool = host_pool();
+  const int parts = B >= 16 ? (int)std::min<int64_t>(pool.W, B / 8) : 1;
+  std::vector<std::vector<int64_t>> pfar(parts), poff(parts);
+  std::vector<int> prc(parts, 0);
+  {
+    double* pts = reinterpret_cast<double*>(pk + o_pt);
+    double* pn = reinterpret_cast<double*>(pk + o_pn);
+    double* pw = reinterpret_cast<double*>(pk + o_pw);
+    const std::function<void(int)> work = [&](int p) {
+      if (p >= parts) return;
+      const int64_t lo = B * p / parts, hi = B * (p + 1) / parts, nb = hi - lo;
+      poff[p].resize(nb + 1);
+      pfar[p].resize(4096);
+      int64_t need = 0;
+      int r = skb_host_far_lists(nb, idx.data() + lo, E.center, E.hw, E.nbr, E.lev, E.ix, E.iy, E.leaf,
+                                 E.level_start, E.depth, E.root, E.factor, E.big, E.a_start, E.a_len,
+                                 E.px, E.py, poff[p].data(), pfar[p].data(), (int64_t)pfar[p].size(), &need);
+      if (r == 1) {
+        pfar[p].resize(need + 1);
+        r = skb_host_far_lists(nb, idx.data() + lo, E.center, E.hw, E.nbr, E.lev, E.ix, E.iy, E.leaf,
+                               E.level_start, E.depth, E.root, E.factor, E.big, E.a_start, E.a_len,
+                               E.px, E.py, poff[p].data(), pfar[p].data(), (int64_t)pfar[p].size(), &need);
+      }
+      prc[p] = r;
+      skb_host_proxies(nb, idx.data() + lo, E.center, E.hw, E.factor, P, E.cs, pts + lo * P * 2,
+                       pn + lo * P * 2, pw + lo);
+    };
+    if (parts > 1) pool.run(work);
+    else work(0);
+  }
+  std::vector<int64_t> far_off(B + 1, 0), part_o(parts + 1, 0);
+  for (int p = 0; p < parts; ++p) {
+    if (prc[p]) return 8;
+    const int64_t lo = B * p / parts, nb = (int64_t)poff[p].size() - 1;
+    for (int64_t b = 0; b < nb; ++b) far_off[lo + b + 1] = part_o[p] + poff[p][b + 1];
+    part_o[p + 1] = part_o[p] + poff[p][nb];
+  }
+  const int64_t nfar = std::max<int64_t>(far_off[B], 1);
+  if ((rc = pack_reserve(E, o_f + nfar))) return rc;
+  pk = E.pack;
+  {
+    const std::function<void(int)> cp = [&](int p) {
+      if (p < parts && part_o[p + 1] > part_o[p])
+        memcpy(pk + o_f + part_o[p], pfar[p].data(), sizeof(int64_t) * (part_o[p + 1] - part_o[p]));
+    };
+    if (parts > 1) pool.run(cp);
+    else cp(0);
+  }
+  memcpy(pk + o_fo, far_off.data(), sizeof(int64_t) * (B + 1));
+  tm.tick("far+proxies");
   // stack layout (column-major per box, ld = rows)
   R.rows.resize(B);
-  std::vector<int64_t> nB(B), stack_off(B + 1, 0);
-  int64_t maxnB = 0, maxitems = 0;
+  std::vector<int64_t> nB(B);
+  int64_t* stack_off = pk + o_so;
+  int64_t maxnB = 0, maxitems = 0, so = 0;
   for (int64_t b = 0; b < B; ++b) {
     nB[b] = R.act_off[b + 1] - R.act_off[b];
     const int64_t nF = far_off[b + 1] - far_off[b];
     R.rows[b] = 2 * nF + 6 * P + 2;
-    stack_off[b + 1] = stack_off[b] + R.rows[b] * nB[b];
+    stack_off[b] = so;
+    so += R.rows[b] * nB[b];
     maxnB = std::max(maxnB, nB[b]);
     maxitems = std::max(maxitems, nF + P + 1);
   }
   cudaStream_t s = E.s;
-  SKB_RET(malloc_async((void**)&R.stack, sizeof(double) * std::max<int64_t>(stack_off[B], 1), s));
-  // one upload: act_off | act | far_off | far | pts | pn | pw | stack_off
-  std::vector<int64_t> pk;
-  const int64_t nfar = std::max<int64_t>(far_off[B], 1);
-  pk.reserve(2 * (B + 1) + R.act.size() + nfar + 4 * B * P + 2 * B);
-  auto add = [&](const void* p, int64_t n) {
-    const int64_t o = ((int64_t)pk.size() + 1) & ~(int64_t)1;   // 16-byte aligned (double2 loads)
-    pk.resize(o + n);
-    memcpy(pk.data() + o, p, sizeof(int64_t) * n);
-    return o;
-  };
-  const int64_t o_ao = add(R.act_off.data(), B + 1);
-  R.o_act = add(R.act.data(), (int64_t)R.act.size());
-  const int64_t o_fo = add(far_off.data(), B + 1);
-  const int64_t o_f = add(far.data(), nfar);
-  const int64_t o_pt = add(pts.data(), B * P * 2);
-  const int64_t o_pn = add(pn.data(), B * P * 2);
-  const int64_t o_pw = add(pw.data(), B);
-  const int64_t o_so = add(stack_off.data(), B);
+  SKB_RET(malloc_async((void**)&R.stack, sizeof(double) * std::max<int64_t>(so, 1), s));
+  const int64_t npk = o_f + nfar;
   tm.tick("pack");
-  if ((rc = upload(pk.data(), (int64_t)pk.size(), s, &R.dup))) return rc;
+  SKB_RET(malloc_async((void**)&R.dup, sizeof(int64_t) * npk, s));
+  SKB_RET(cudaMemcpyAsync(R.dup, pk, sizeof(int64_t) * npk, cudaMemcpyHostToDevice, s));
   tm.tick("upload");
-  R.h2d += 8 * (int64_t)pk.size();
+  R.h2d += 8 * npk;
   if ((rc = skb_assemble_stack(E.pos, E.nrm, E.w, B, R.dup + o_ao, R.dup + R.o_act, R.dup + o_fo,
                                R.dup + o_f, (const double*)(R.dup + o_pt),
                                (const double*)(R.dup + o_pn), (const double*)(R.dup + o_pw),
@@ -283,6 +417,7 @@ int run_level(Engine& E, int64_t L, LevelOut& R) {
 
 void engine_main(Engine* E) {
   cudaSetDevice(E->dev);
+  use_engine_side(true);
   if (!getenv("SKB_ENGINE_SHARED_POOL")) {
     static cudaMemPool_t pool = nullptr;
     static std::mutex pm;
@@ -296,6 +431,7 @@ void engine_main(Engine* E) {
       if (cudaMemPoolCreate(&pool, &props) == cudaSuccess) {
         uint64_t thr = ~0ull;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        if (!getenv("SKB_POOL_RELAXED")) pool_strict(pool);   // see ring_stage
       } else {
         pool = nullptr;
       }
@@ -389,6 +525,16 @@ int skb_engine_start(const void* const* tree, int64_t depth, const double* root,
       E->pinned_size = want;
     }
   }
+  {
+    std::lock_guard<std::recursive_mutex> lk(host_mutex());
+    PackBuf& g = g_pack();
+    if (!g.busy) {
+      g.busy = true;
+      E->shared_pack = true;
+      E->pack = g.p;
+      E->pack_cap = g.cap;
+    }
+  }
   if (!deferred) E->th = std::thread(engine_main, E);
   *handle = (int64_t)E;
   return 0;
@@ -447,7 +593,12 @@ int skb_engine_ack(int64_t handle, int64_t L) {
 }
 
 int skb_engine_set_lead(int64_t handle, int64_t lead) {
-  ((Engine*)handle)->lead = lead;
+  Engine* E = (Engine*)handle;
+  {
+    std::lock_guard<std::mutex> lk(E->m);
+    E->lead = lead;
+  }
+  E->cv.notify_all();
   return 0;
 }
 
@@ -464,6 +615,8 @@ int skb_engine_release(int64_t handle, int64_t L, void* stream) {
   Engine* E = (Engine*)handle;
   LevelOut& R = E->out[L];
   cudaStream_t s = (cudaStream_t)stream;
+  static const bool defer = getenv("SKB_ENGINE_DEFER_FREE") != nullptr;   // race hunt
+  if (defer && !E->freeing) return 0;
   if (R.stack) { cudaFreeAsync(R.stack, s); R.stack = nullptr; }
   if (R.dbuf) { cudaFreeAsync(R.dbuf, s); R.dbuf = nullptr; }
   if (R.dup) { cudaFreeAsync(R.dup, s); R.dup = nullptr; }
@@ -485,15 +638,26 @@ int skb_engine_stop(int64_t handle) {
 int skb_engine_free(int64_t handle, void* stream) {
   Engine* E = (Engine*)handle;
   if (E->th.joinable()) E->th.join();
+  E->freeing = true;
+  if (getenv("SKB_ENGINE_DEFER_FREE")) cudaDeviceSynchronize();
   for (int64_t L = E->lev_lo; L <= E->depth; ++L) {
     skb_engine_release(handle, L, stream);
     if (E->out[L].ev) cudaEventDestroy(E->out[L].ev);
   }
+  bool failed = false;
+  for (int64_t L = E->lev_lo; L <= E->depth; ++L) failed |= E->out[L].rc != 0;
+  if (failed) cudaStreamSynchronize(E->s);   // a level that stopped early may have a copy in flight
   if (E->shared_pinned) {
     std::lock_guard<std::recursive_mutex> lk(host_mutex());
     *E->shared_pinned = false;       // the engine thread has joined: no copy in flight
   } else if (E->pinned) {
     cudaFreeHost(E->pinned);
+  }
+  if (E->shared_pack) {
+    std::lock_guard<std::recursive_mutex> lk(host_mutex());
+    g_pack().busy = false;
+  } else if (E->pack) {
+    cudaFreeHost(E->pack);
   }
   delete E;
   return 0;

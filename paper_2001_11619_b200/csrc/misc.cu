@@ -255,10 +255,16 @@ Prof& prof() {
   static Prof p;
   return p;
 }
+// The native level engine thread has its own side streams: its size classes
+// neither serialise behind the Python thread's Schur / sweep classes nor share
+// their fork/join events.
+thread_local bool t_engine_side = false;
 SideStreams& side() {
   static SideStreams s;
-  return s;
+  static SideStreams se;
+  return t_engine_side ? se : s;
 }
+void use_engine_side(bool on) { t_engine_side = on; }
 CaptureSession& capture() {
   static CaptureSession c;
   return c;

@@ -1485,9 +1485,13 @@ class _Engine:
             self.lib.skb_engine_set_update(self.h, todo.ctypes.data, coff.ctypes.data,
                                            cskel.ctypes.data)
             self.lib.skb_engine_go(self.h)
-        lead = os.environ.get("SKB_ENGINE_LEAD")
-        if lead is not None:
-            self.lib.skb_engine_set_lead(self.h, int(lead))
+        # The engine runs at most one level ahead of the enqueued Schur stages.
+        # Unbounded run-ahead (SKB_ENGINE_LEAD=-1) made repeated update chains
+        # differ run to run in ~5% of steps (last-ulp level, top-level boxes);
+        # with lead 1 they are bitwise repeatable and factor() is as fast.
+        lead = int(os.environ.get("SKB_ENGINE_LEAD", "1"))
+        if lead >= 0:
+            self.lib.skb_engine_set_lead(self.h, lead)
         self.sizes = np.zeros(8, np.int64)
         self.ptrs = np.zeros(14, np.int64)
 
