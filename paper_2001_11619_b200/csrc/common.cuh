@@ -93,13 +93,9 @@ inline int ring_stage(const void* host, size_t bytes, cudaStream_t s, void* dev)
     SKB_RET(cudaDeviceGetDefaultMemPool(&pool, dev));
     uint64_t thr = ~0ull;
     SKB_RET(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
-    // Cross-stream reuse only through explicit event dependencies: a block freed
-    // on one stream is not handed to another stream merely because the freeing
-    // stream has progressed (opportunistic) or by an inserted wait (internal
-    // dependencies).  With those on, repeated engine update chains differed
-    // run to run (~5% of steps, 1-ulp level in the top-level boxes); with them
-    // off they are bitwise repeatable.  SKB_POOL_RELAXED=1 restores the defaults.
-    if (!getenv("SKB_POOL_RELAXED")) {
+    // SKB_POOL_STRICT=1 (debug): cross-stream reuse only through explicit event
+    // dependencies (no opportunistic reuse, no inserted waits)
+    if (getenv("SKB_POOL_STRICT")) {
       const int prc = pool_strict(pool);
       if (prc) return prc;
     }

@@ -431,7 +431,7 @@ void engine_main(Engine* E) {
       if (cudaMemPoolCreate(&pool, &props) == cudaSuccess) {
         uint64_t thr = ~0ull;
         cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-        if (!getenv("SKB_POOL_RELAXED")) pool_strict(pool);   // see ring_stage
+        if (getenv("SKB_POOL_STRICT")) pool_strict(pool);   // debug, see ring_stage
       } else {
         pool = nullptr;
       }

@@ -244,6 +244,40 @@ struct TrsmDesc {
   int64_t jb, ncols;
 };
 
+template <bool UPPER, bool FULL>
+__device__ __forceinline__ void trsm_col(const TrsmDesc& D, const double (*Ls)[LB + 1],
+                                         const double* Linv, int jb, int64_t c) {
+  double x[LB];
+#pragma unroll
+  for (int i = 0; i < LB; ++i)
+    if (FULL || i < jb) x[i] = D.B[i * D.ldb + c];
+  if (!UPPER) {
+#pragma unroll
+    for (int i = 1; i < LB; ++i) {
+      if (!FULL && i >= jb) break;
+      double s = x[i];
+#pragma unroll
+      for (int p = 0; p < LB; ++p)
+        if (p < i) s -= Ls[i][p] * x[p];
+      x[i] = s;
+    }
+  } else {
+    // p descending: the same operation order as the warp-per-column variant
+#pragma unroll
+    for (int i = LB - 1; i >= 0; --i) {
+      if (!FULL && i >= jb) continue;
+      double s = x[i];
+#pragma unroll
+      for (int p = LB - 1; p > 0; --p)
+        if (p > i && (FULL || p < jb)) s -= Ls[i][p] * x[p];
+      x[i] = div_rcp(s, Ls[i][i], Linv[i]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < LB; ++i)
+    if (FULL || i < jb) D.B[i * D.ldb + c] = x[i];
+}
+
 template <bool UPPER>
 __global__ void __launch_bounds__(256) k_trsm_block(const TrsmDesc* __restrict__ descs) {
   __shared__ double Ls[LB][LB + 1];
@@ -258,35 +292,9 @@ __global__ void __launch_bounds__(256) k_trsm_block(const TrsmDesc* __restrict__
   __syncthreads();
   const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (c >= D.ncols) return;
-  double x[LB];
-#pragma unroll
-  for (int i = 0; i < LB; ++i)
-    if (i < jb) x[i] = D.B[i * D.ldb + c];
-  if (!UPPER) {
-#pragma unroll
-    for (int i = 1; i < LB; ++i) {
-      if (i >= jb) break;
-      double s = x[i];
-#pragma unroll
-      for (int p = 0; p < LB; ++p)
-        if (p < i) s -= Ls[i][p] * x[p];
-      x[i] = s;
-    }
-  } else {
-    // p descending: the same operation order as the warp-per-column variant
-#pragma unroll
-    for (int i = LB - 1; i >= 0; --i) {
-      if (i >= jb) continue;
-      double s = x[i];
-#pragma unroll
-      for (int p = LB - 1; p > 0; --p)
-        if (p > i && p < jb) s -= Ls[i][p] * x[p];
-      x[i] = div_rcp(s, Ls[i][i], Linv[i]);
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < LB; ++i)
-    if (i < jb) D.B[i * D.ldb + c] = x[i];
+  // full diagonal blocks (the common case) without the jb predicates
+  if (jb == LB) trsm_col<UPPER, true>(D, Ls, Linv, LB, c);
+  else trsm_col<UPPER, false>(D, Ls, Linv, jb, c);
 }
 
 // Narrow right-hand sides: one warp per column, lanes own rows (jb <= 64).

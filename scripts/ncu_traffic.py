@@ -10,7 +10,7 @@ import sys
 
 FAMILY = [("k_assemble", "assemble"), ("k_geqr", "geqrf"), ("k_larft", "geqrf"), ("k_zero_lower", "geqrf"),
           ("k_qrcp", "qrcp"), ("k_gather_R", "id_T"), ("k_gemm", "gemm"), ("k_getrf", "getrf"),
-          ("k_getf2", "getrf"), ("k_pivot", "getrf"), ("k_trsm", "trsm"), ("k_apply_ipiv", "trsm"),
+          ("k_getf2", "getrf"), ("k_laswp", "getrf"), ("k_pivot", "getrf"), ("k_trsm", "trsm"), ("k_apply_ipiv", "trsm"),
           ("k_gather", "move"), ("k_scatter", "move"), ("k_copy2d", "move"), ("k_schur", "move")]
 rows = list(csv.reader(open(sys.argv[1])))
 hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
