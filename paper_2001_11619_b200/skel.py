@@ -222,11 +222,18 @@ class ActStore:
             cap = 2 * t.n_nodes * (2 * t.depth + 3) + 16
         self.big = np.empty(cap, np.int64)
         self.fill = 0
-        self.a_start = np.zeros(nbox, np.int64)
-        self.a_len = np.zeros(nbox, np.int64)
         self.s_start = np.zeros(nbox, np.int64)
         self.s_len = np.zeros(nbox, np.int64)
         self.xss = np.zeros(nbox, np.uint64)
+        init = getattr(t, "_store_init", None)     # leaf actives depend on the tree only
+        if init is not None:
+            fill, a_start, a_len, prefix = init
+            self.big[:fill] = prefix
+            self.fill = fill
+            self.a_start, self.a_len = a_start.copy(), a_len.copy()
+            return
+        self.a_start = np.zeros(nbox, np.int64)
+        self.a_len = np.zeros(nbox, np.int64)
         leaves = np.flatnonzero(t.is_leaf)
         # leaf actives: dofs 2*node + {0,1} of the sorted owned nodes (skel.py:243-249)
         for l in range(t.depth + 1):
@@ -237,6 +244,7 @@ class ActStore:
             dofs = (2 * nodes[:, None] + np.arange(2)[None, :]).ravel()
             self.a_start[li] = self._append(dofs) + 2 * off[:-1]
             self.a_len[li] = 2 * t.node_cnt[li]
+        t._store_init = (self.fill, self.a_start.copy(), self.a_len.copy(), self.big[:self.fill].copy())
 
     @classmethod
     def replay(cls, t: Tree, act_of: dict) -> "ActStore":
@@ -1472,10 +1480,11 @@ class _Engine:
         geo = _i64p([self.px.ctypes.data, self.py.ctypes.data, ptr(g.pos), ptr(g.nrm), ptr(g.w),
                      self.cs.ctypes.data])
         self.h = ctypes.c_int64(0)
-        rc = self.lib.skb_engine_start(tree, t.depth, nv["root"].ctypes.data, ctx.factor, st,
-                                       len(store.big), geo, ctx.P, ctx.tol, _stream(),
-                                       0 if update is not None else 1,
-                                       2 * t.n_nodes + 3 * len(t.lev) + 16, ctypes.byref(self.h))
+        with _ht("E.start.c"):
+            rc = self.lib.skb_engine_start(tree, t.depth, nv["root"].ctypes.data, ctx.factor, st,
+                                           len(store.big), geo, ctx.P, ctx.tol, _stream(),
+                                           0 if update is not None else 1,
+                                           2 * t.n_nodes + 3 * len(t.lev) + 16, ctypes.byref(self.h))
         if rc:
             raise _lib.SkbError(f"skb_engine_start returned {rc}")
         self.h = self.h.value
@@ -1551,9 +1560,11 @@ def _run_levels_engine(ctx: _Ctx):
     engine thread; this loop only consumes finished levels (Schur stage,
     migration check, augmentation sweep, level descriptors)."""
     t = ctx.t
-    store = ActStore(t, engine=True)
+    with _ht("E.store"):
+        store = ActStore(t, engine=True)
     ctx.store = store
-    eng = _Engine(ctx, store)
+    with _ht("E.start"):
+        eng = _Engine(ctx, store)
     try:
         with torch.cuda.stream(ctx.sstream):      # host-side work rides the level stream
             out = _engine_loop(ctx, eng, store)
@@ -1813,7 +1824,8 @@ def factor(spec, b, t: Tree, tol: float, workers: int = 1,
         raise NotImplementedError("propagate_zeros is a sequential CPU validation mode")
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    ctx = _Ctx(spec, b, t, tol, proxy_count, proxy_factor)
+    with _ht("ctx"):
+        ctx = _Ctx(spec, b, t, tol, proxy_count, proxy_factor)
     with torch.cuda.stream(_compress_stream()):
         with _ht("run_levels"):
             levels = None

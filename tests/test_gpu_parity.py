@@ -194,3 +194,25 @@ def test_engine_repeatable_cfg2():
         xs.append(f.solve(wl.extra["rhs"]))
         del f
     assert np.array_equal(xs[0], xs[1]) and np.array_equal(xs[0], xs[2])
+
+
+def test_engine_update_chains_repeatable():
+    """Two identical hole-move update chains on the engine give bitwise equal
+    solves at every step (regression for the run-ahead race: with unbounded
+    run-ahead ~5 % of steps differed in the last ulp)."""
+    wl = configs.cfg2()
+    b = wl.boundary
+    rhs = wl.extra["rhs"]
+    seq = configs.hole_move_sequence(b, 4)
+    runs = []
+    for _ in range(3):
+        cur = _factor(wl)
+        xs = []
+        for (h, d, nb, rep) in seq:
+            cur = update(cur, nb, rep)
+            xs.append(cur.solve(rhs))
+        runs.append(xs)
+        del cur
+    for xs in runs[1:]:
+        for s, (a, c) in enumerate(zip(runs[0], xs)):
+            assert np.array_equal(a, c), s
