@@ -523,8 +523,17 @@ int getrf_batched(int64_t nbox, const SkbMat* a, const int64_t* ipiv, int32_t* i
     for (int64_t b = 0; b < nbox; ++b) nbig += a[b].rows > kSmallLU;
     SKB_RET(cudaMallocAsync(reinterpret_cast<void**>(&swp), sizeof(int32_t) * 4 * LB * nbig, s));
   }
+  // Look-ahead (SKB_LU_LOOKAHEAD=0 disables): the trailing update of each round
+  // is split into the next panel's columns (main stream, so the next panel
+  // starts right after them) and the rest (a side stream, overlapping the
+  // next single-CTA panel); the next round's dlaswp joins the side stream.
+  // Every element sees the same operations in the same order either way.
+  static const bool lookahead = !getenv("SKB_LU_LOOKAHEAD") || atoi(getenv("SKB_LU_LOOKAHEAD")) != 0;
+  std::vector<TrsmDesc> tdr;
+  std::vector<SkbGemm> gdr;
+  bool pending_rest = false;
   for (int64_t rd_ = 0; rd_ < rounds; ++rd_) {
-    pd.clear(); td.clear(); gd.clear();
+    pd.clear(); td.clear(); gd.clear(); tdr.clear(); gdr.clear();
     size_t smem = 0;
     int64_t maxcol = 0;
     for (int64_t b = 0; b < nbox; ++b) {
@@ -542,14 +551,22 @@ int getrf_batched(int64_t nbox, const SkbMat* a, const int64_t* ipiv, int32_t* i
                            swp + (int64_t)pd.size() * 4 * LB});
       maxcol = std::max(maxcol, n - jb);
       if (n2 > 0) {
-        td.push_back(TrsmDesc{A + j0 * ld + j0, ld, A + j0 * ld + j0 + jb, ld, jb, n2});
-        SkbGemm g{};
-        g.A = A + (j0 + jb) * ld + j0; g.lda = ld;           // L21: n2 x jb
-        g.B = A + j0 * ld + j0 + jb; g.ldb = ld;             // U12: jb x n2
-        g.C = A + (j0 + jb) * ld + j0 + jb; g.ldc = ld;      // A22
-        g.D = A + (j0 + jb) * ld + j0 + jb; g.ldd = ld;
-        g.m = n2; g.n = n2; g.k = jb; g.alpha = -1.0; g.beta = 1.0;
-        gd.push_back(g);
+        // columns [j0+jb, j0+jb+w) on the main stream, the rest on the side stream
+        // (only where the trailing update outweighs its extra launches: n >= 1536;
+        // n = 2532: 27.1 -> 24.6 ms, n = 849: 3.02 -> 3.14 ms, so off there)
+        const int64_t w = lookahead && n >= 1536 ? std::min<int64_t>(PB, n2) : n2;
+        auto add = [&](int64_t c0, int64_t nc, std::vector<TrsmDesc>& T, std::vector<SkbGemm>& G) {
+          T.push_back(TrsmDesc{A + j0 * ld + j0, ld, A + j0 * ld + c0, ld, jb, nc});
+          SkbGemm g{};
+          g.A = A + (j0 + jb) * ld + j0; g.lda = ld;           // L21: n2 x jb
+          g.B = A + j0 * ld + c0; g.ldb = ld;                  // U12 columns: jb x nc
+          g.C = A + (j0 + jb) * ld + c0; g.ldc = ld;           // A22 columns
+          g.D = A + (j0 + jb) * ld + c0; g.ldd = ld;
+          g.m = n2; g.n = nc; g.k = jb; g.alpha = -1.0; g.beta = 1.0;
+          G.push_back(g);
+        };
+        add(j0 + jb, w, td, gd);
+        if (n2 > w) add(j0 + jb + w, n2 - w, tdr, gdr);
       }
     }
     if (pd.empty()) continue;
@@ -559,13 +576,23 @@ int getrf_batched(int64_t nbox, const SkbMat* a, const int64_t* ipiv, int32_t* i
       ProfScope ps(F_GETRF, s);
       k_getf2_panel<SKB_PANEL_NT><<<(unsigned)pd.size(), SKB_PANEL_NT, smem, s>>>(dp);
       SKB_LAUNCH_CHECK();
+      // the interchanges touch the columns the side stream is still updating
+      if (pending_rest) { SKB_RET((cudaError_t)(-join_n(s, 1))); pending_rest = false; }
       if (maxcol > 0) k_laswp<<<dim3((unsigned)((maxcol + 31) / 32), (unsigned)pd.size()), 256, 0, s>>>(dp);
     }
     SKB_LAUNCH_CHECK();
     cudaFreeAsync(dp, s);
+    if (!tdr.empty()) {
+      SKB_RET((cudaError_t)(-fork_n(s, 1)));
+      cudaStream_t ss = side().st[0];
+      if ((rc = launch_trsm(tdr, false, ss))) return rc;
+      if ((rc = gemm_grouped(gdr.data(), (int64_t)gdr.size(), ss))) return rc;
+      pending_rest = true;
+    }
     if ((rc = launch_trsm(td, false, s))) return rc;
     if ((rc = gemm_grouped(gd.data(), (int64_t)gd.size(), s))) return rc;
   }
+  if (pending_rest) SKB_RET((cudaError_t)(-join_n(s, 1)));
   if (swp) cudaFreeAsync(swp, s);
   std::vector<RatioDesc> rd(nbox);
   for (int64_t b = 0; b < nbox; ++b) rd[b] = RatioDesc{a[b].ptr, a[b].rows, a[b].ld};

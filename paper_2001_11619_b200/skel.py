@@ -1497,9 +1497,9 @@ class _Engine:
         # update: the engine runs at most one level ahead of the enqueued Schur
         # stages.  Unbounded run-ahead made repeated update chains differ run to
         # run in ~5% of steps (last-ulp level, top-level boxes); with lead 1 they
-        # are bitwise repeatable.  factor() was repeatable with unbounded
-        # run-ahead in every test and is throttled by lead 1 on large trees
-        # (cfg3 0.28 -> 0.35 s): unbounded there.  SKB_ENGINE_LEAD overrides.
+        # are bitwise repeatable.  factor() is repeatable with unbounded
+        # run-ahead in every test and lead 1 throttles it on large trees
+        # (cfg3 0.19 -> 0.21 s): unbounded there.  SKB_ENGINE_LEAD overrides.
         lead = int(os.environ.get("SKB_ENGINE_LEAD", "1" if update is not None else "-1"))
         if lead >= 0:
             self.lib.skb_engine_set_lead(self.h, lead)

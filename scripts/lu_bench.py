@@ -41,4 +41,7 @@ for n in [int(a) for a in (sys.argv[1:] or ["276", "849", "2532"])]:
                 c, t = agg.get(k, (0, 0.0))
                 agg[k] = (c + 1, t + e.device_time_total / 1e3)
         print("  " + "; ".join(f"{k} x{c} {t:.3f} ms" for k, (c, t) in sorted(agg.items(), key=lambda x: -x[1][1])))
+    if os.environ.get("LU_SAVE"):
+        np.save(f"{os.environ['LU_SAVE']}_{n}_A.npy", A.cpu().numpy())
+        np.save(f"{os.environ['LU_SAVE']}_{n}_p.npy", ip.cpu().numpy())
     print(f"n={n}: LU {min(ts[1:]):.3f} ms ({2 * n ** 3 / 3 / (min(ts[1:]) * 1e-3) / 1e12:.3f} TFLOP/s)")

@@ -1,0 +1,26 @@
+"""Host time per update() section (SKB_HOST_PROF=1), averaged over hole moves 3..14 on cfg2."""
+import gc, os, sys, time
+os.environ.setdefault("SKB_HOST_PROF", "1")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+from paper_2001_11619_b200 import SystemSpec, build_tree, configs, factor, update, skel
+wl = configs.cfg2(); b = wl.boundary
+t = build_tree(b.positions, wl.leaf_cap)
+f = factor(SystemSpec(), b, t, wl.tol, proxy_count=wl.proxy_count, proxy_factor=wl.proxy_factor)
+seq = configs.hole_move_sequence(b, 14)
+ts = []
+for i, (h, d, nb, rp) in enumerate(seq):
+    gc.collect()
+    torch.cuda.synchronize()
+    if i == 2:
+        skel._HostTimer.acc.clear()
+    t0 = time.perf_counter()
+    f = update(f, nb, rp)
+    torch.cuda.synchronize()
+    if i >= 2:
+        ts.append((time.perf_counter() - t0) * 1e3)
+n = len(ts)
+print("update ms median %.2f" % np.median(ts))
+for k, v in sorted(skel._HostTimer.acc.items(), key=lambda x: -x[1]):
+    print("  %-14s %8.3f ms/update" % (k, v * 1e3 / n))
