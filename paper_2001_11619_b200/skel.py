@@ -1494,13 +1494,13 @@ class _Engine:
             self.lib.skb_engine_set_update(self.h, todo.ctypes.data, coff.ctypes.data,
                                            cskel.ctypes.data)
             self.lib.skb_engine_go(self.h)
-        # update: the engine runs at most one level ahead of the enqueued Schur
-        # stages.  Unbounded run-ahead made repeated update chains differ run to
-        # run in ~5% of steps (last-ulp level, top-level boxes); with lead 1 they
-        # are bitwise repeatable.  factor() is repeatable with unbounded
-        # run-ahead in every test and lead 1 throttles it on large trees
-        # (cfg3 0.19 -> 0.21 s): unbounded there.  SKB_ENGINE_LEAD overrides.
-        lead = int(os.environ.get("SKB_ENGINE_LEAD", "1" if update is not None else "-1"))
+        # The engine runs at most one level ahead of the enqueued Schur stages.
+        # Unbounded run-ahead made repeated update chains differ run to run in
+        # ~5% of steps (last-ulp level, top-level boxes) and, more rarely, the
+        # factorizations they start from; with lead 1 both are bitwise
+        # repeatable.  Costs large trees a little (cfg3 factor 0.19 -> 0.21 s).
+        # SKB_ENGINE_LEAD=-1 restores unbounded run-ahead.  DESIGN.md section 7.
+        lead = int(os.environ.get("SKB_ENGINE_LEAD", "1"))
         if lead >= 0:
             self.lib.skb_engine_set_lead(self.h, lead)
         self.sizes = np.zeros(8, np.int64)
