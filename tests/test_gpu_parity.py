@@ -109,12 +109,18 @@ def test_system_matvec_vs_oracle(builder):
 
 
 @pytest.mark.slow
-def test_cfg4_update_sequence_vs_oracle():
+def test_cfg4_update_sequence_vs_oracle(monkeypatch):
     """cfg4 regime (hole moves on cfg2): the GPU dirty set equals the reference
     rules' (oracle) at every step; update == refactor bitwise while the reference
     rules guarantee it (first 10 moves here), and to rounding afterwards -- the
     reference's own update differs from its refactor by ~6e-15 from move 15 on
-    (a coarse-leaf split reorders a clean box's far-field rows)."""
+    (a coarse-leaf split reorders a clean box's far-field rows).
+
+    Runs on the Python level loop: the native engine's run-ahead has a rare
+    last-ulp nondeterminism, so bitwise update == refactor
+    is asserted on the bitwise-repeatable loop; the engine's agreement to 1e-13
+    is test_update_chains_repeatable's."""
+    monkeypatch.setattr(skel, "_ENGINE_ON", False)
     wl = configs.cfg2()
     b = wl.boundary
     f = _factor(wl)
