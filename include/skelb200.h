@@ -311,6 +311,10 @@ int skb_engine_set_lead(int64_t handle, int64_t lead);
 /* stop after the current level and join the engine thread */
 int skb_engine_stop(int64_t handle);
 int skb_engine_free(int64_t handle, void* stream);
+/* Debug (SKB_ENGINE_SNAP=<level>): host copy of the snapshot `which` of that
+ * level's ID stacks (0 after assembly, 1 after pre-reduction, 2 after QRCP);
+ * returns the element count, -1 when no snapshot was taken.                  */
+int64_t skb_debug_snap(int32_t which, double* host, int64_t n_host);
 
 /* ---- native host runtime (host arrays, no device; csrc/host.cpp) ---------
  * Per-level bookkeeping the reference does per box in Python.  Tree arrays as

@@ -178,13 +178,24 @@ def id_stack(g, box_dofs, far, center, radius, count):
                       k_out, proxy_outgoing(g, box_dofs, pts, pw), e_out])
 
 
-def aug_columns(points, centers):
-    """Stokeslet/rotlet columns H, kernels.py:201-223."""
+def aug_columns(points, centers, workers=1):
+    """Stokeslet/rotlet columns H, kernels.py:201-223 (``workers`` threads over
+    the centres: every column is computed by the same NumPy expressions)."""
     points = np.atleast_2d(np.asarray(points, float))
     centers = np.atleast_2d(np.asarray(centers, float))
     H = np.empty((2 * len(points), 3 * len(centers)))
-    pref = 1.0 / (4 * np.pi)
+    if workers > 1 and len(centers) > 1:
+        with ThreadPoolExecutor(max_workers=workers) as ex:
+            list(ex.map(lambda i: _aug_column(points, centers[i], i, H), range(len(centers))))
+        return H
     for i, c in enumerate(centers):
+        _aug_column(points, c, i, H)
+    return H
+
+
+def _aug_column(points, c, i, H):
+    pref = 1.0 / (4 * np.pi)
+    if True:
         r = points - c[None, :]
         r2 = (r * r).sum(axis=1)
         lg = -0.5 * np.log(r2)
@@ -194,7 +205,6 @@ def aug_columns(points, centers):
         H[1::2, 3 * i + 1] = pref * (lg + r[:, 1] * r[:, 1] / r2)
         H[0::2, 3 * i + 2] = pref * (-r[:, 1]) / r2
         H[1::2, 3 * i + 2] = pref * r[:, 0] / r2
-    return H
 
 
 def aug_functionals(g):
@@ -593,8 +603,23 @@ class _Pass:
             sweep.append((lev, keys))
         return sweep
 
-    def top(self, sweep):
-        """_finish_top, skel.py:364-425."""
+    def _sweep_box(self, k, UH, PsiV, UH_div):
+        """One box of the augmentation sweep (skel.py:384-395); returns its
+        q x q Schur contribution PsiV_R^T w."""
+        bf = self.out[k]
+        sd, r = bf.skel, bf.red
+        UH[r] -= bf.T.T @ UH[sd]
+        w = bf.lu.solve(UH[r])
+        UH[sd] -= bf.Xsr @ w
+        UH_div[r] = w
+        PsiV[r] -= bf.T.T @ PsiV[sd]
+        PsiV[sd] -= bf.Xrs_div.T @ PsiV[r]
+        return PsiV[r].T @ w
+
+    def top(self, sweep, workers=1):
+        """_finish_top, skel.py:364-425.  With ``workers`` > 1 the boxes of a
+        level run on threads (they touch disjoint rows) and their Schur
+        contributions are added in box order: bitwise the serial result."""
         g, t = self.g, self.tree
         root = t.boxes[ROOT]
         if root.leaf:
@@ -609,21 +634,22 @@ class _Pass:
         nonroot = np.ones(nd, dtype=bool)
         nonroot[rd] = False
         if q:
-            UH = aug_columns(g.positions, g.hole_centers)
+            UH = aug_columns(g.positions, g.hole_centers, workers)
             PsiV = aug_functionals(g)
             UH_div = np.zeros_like(UH)
             schur = np.zeros((q, q))
-            for _, keys in sweep:
-                for k in keys:
-                    bf = self.out[k]
-                    sd, r = bf.skel, bf.red
-                    UH[r] -= bf.T.T @ UH[sd]
-                    w = bf.lu.solve(UH[r])
-                    UH[sd] -= bf.Xsr @ w
-                    UH_div[r] = w
-                    PsiV[r] -= bf.T.T @ PsiV[sd]
-                    PsiV[sd] -= bf.Xrs_div.T @ PsiV[r]
-                    schur += PsiV[r].T @ w
+            ex = ThreadPoolExecutor(max_workers=workers) if workers > 1 else None
+            try:
+                for _, keys in sweep:
+                    if ex is not None and len(keys) > 1:
+                        parts = list(ex.map(lambda k: self._sweep_box(k, UH, PsiV, UH_div), keys))
+                    else:
+                        parts = [self._sweep_box(k, UH, PsiV, UH_div) for k in keys]
+                    for part in parts:
+                        schur += part
+            finally:
+                if ex is not None:
+                    ex.shutdown()
             ns = len(rd)
             C = np.zeros((ns + q, ns + q))
             C[:ns, :ns] = E_root
@@ -646,7 +672,7 @@ def factor(g, tree, tol, proxy_count=64, proxy_factor=1.5, workers=1, record=Non
         p = _Pass(g, tree, tol, proxy_count, proxy_factor)
         p.record = record
         sweep = p.run(workers)
-        f = p.top(sweep)
+        f = p.top(sweep, workers)
     f.stats["factor_time"] = time.perf_counter() - t0
     return f
 
@@ -743,7 +769,7 @@ def update(fct, b_new, report, workers=1):
     with threadpool_limits(limits=1):          # skel.py:469
         p = _Pass(b_new, t_new, fct.tol, fct.proxy_count, fct.proxy_factor)
         sweep = p.run(workers, reuse=fct.boxes, dirty=dirty)
-        f = p.top(sweep)
+        f = p.top(sweep, workers)
     f.proxy_count, f.proxy_factor = fct.proxy_count, fct.proxy_factor
     f.stats["update_time"] = time.perf_counter() - t0
     f.stats["n_dirty"] = len(dirty)

@@ -73,6 +73,7 @@ SIGNATURES = {
     "skb_engine_go": [_i64],
     "skb_engine_set_lead": [_i64, _i64],
     "skb_engine_free": [_i64, _vp],
+    "skb_debug_snap": [_i32, _vp, _i64],
     # native host runtime (host arrays only, no device)
     "skb_host_far_lists": [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _f64,
                            _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp],
@@ -103,7 +104,7 @@ def load(path: str = LIB_PATH):
     for name, args in SIGNATURES.items():
         fn = getattr(lib, name)
         fn.argtypes = args
-        fn.restype = ctypes.c_int
+        fn.restype = ctypes.c_int64 if name == "skb_debug_snap" else ctypes.c_int
     lib.skb_host_init()
     _LIB = lib
     return lib

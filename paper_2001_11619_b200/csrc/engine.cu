@@ -212,6 +212,37 @@ struct ETimer {
   }
 };
 
+// Debug snapshots (SKB_ENGINE_SNAP=<level>): device copies of that level's
+// ID stacks after assembly, after the Householder pre-reduction and after the
+// QRCP, read back with skb_debug_snap (race localisation; off by default).
+struct Snap {
+  double* buf[3] = {nullptr, nullptr, nullptr};
+  int64_t cap = 0, n = 0;
+};
+Snap& g_snap() {
+  static Snap s;
+  return s;
+}
+int64_t snap_level() {
+  static const int64_t v = getenv("SKB_ENGINE_SNAP") ? atoll(getenv("SKB_ENGINE_SNAP")) : -1;
+  return v;
+}
+int snap_copy(int which, const double* src, int64_t n, cudaStream_t s) {
+  Snap& S = g_snap();
+  if (n > S.cap) {
+    SKB_RET(cudaStreamSynchronize(s));
+    for (auto& b : S.buf) {
+      if (b) cudaFree(b);
+      b = nullptr;
+    }
+    for (auto& b : S.buf) SKB_RET(cudaMalloc((void**)&b, sizeof(double) * n));
+    S.cap = n;
+  }
+  S.n = n;
+  SKB_RET(cudaMemcpyAsync(S.buf[which], src, sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  return 0;
+}
+
 int run_level(Engine& E, int64_t L, LevelOut& R) {
   ETimer tm;
   const int64_t b0 = E.level_start[L], nall = E.level_start[L + 1] - b0;
@@ -357,6 +388,7 @@ int run_level(Engine& E, int64_t L, LevelOut& R) {
                                (const double*)(R.dup + o_pn), (const double*)(R.dup + o_pw),
                                (int32_t)P, R.dup + o_so, R.stack, maxnB, maxitems, s)))
     return rc;
+  if (snap_level() == L && (rc = snap_copy(0, R.stack, so, s))) return rc;
   tm.tick("asm");
   // Householder pre-reduction of the tall stacks (dense.py:56-59)
   R.A.resize(B);
@@ -364,13 +396,14 @@ int run_level(Engine& E, int64_t L, LevelOut& R) {
   std::vector<int64_t> pm, pn_, pA;
   for (int64_t b = 0; b < B; ++b) {
     R.A[b] = (int64_t)(R.stack + stack_off[b]);
-    const bool pre = R.rows[b] > nB[b];
+    const bool pre = R.rows[b] > 2 * nB[b];     // dense.py:56 branch
     R.mq[b] = pre ? nB[b] : R.rows[b];
     if (pre) { pm.push_back(R.rows[b]); pn_.push_back(nB[b]); pA.push_back(R.A[b]); }
   }
   if (!pm.empty() && (rc = geqrf_batched((int64_t)pm.size(), pm.data(), pn_.data(), pm.data(),
                                          pA.data(), s)))
     return rc;
+  if (snap_level() == L && (rc = snap_copy(1, R.stack, so, s))) return rc;
   tm.tick("geqrf");
   // QRCP with rank at tol (dense.py:60-68)
   const int64_t na = R.na;
@@ -385,6 +418,7 @@ int run_level(Engine& E, int64_t L, LevelOut& R) {
                          R.act_off.data(), ints, (double*)R.dbuf, ints + na, ints + na + B,
                          (double*)(R.dbuf + o_gap), s)))
     return rc;
+  if (snap_level() == L && (rc = snap_copy(2, R.stack, so, s))) return rc;
   // one device->host copy: gap | perm | k | steps
   const size_t hb = (size_t)(dbytes - o_gap);
   if (hb > E.pinned_size) return 9;
@@ -418,6 +452,7 @@ int run_level(Engine& E, int64_t L, LevelOut& R) {
 void engine_main(Engine* E) {
   cudaSetDevice(E->dev);
   use_engine_side(true);
+  use_engine_ring(true);          // descriptor uploads through the engine's own pinned ring
   if (!getenv("SKB_ENGINE_SHARED_POOL")) {
     static cudaMemPool_t pool = nullptr;
     static std::mutex pm;
@@ -451,6 +486,10 @@ void engine_main(Engine* E) {
       std::lock_guard<std::mutex> lk(E->m);
       R.rc = rc;
       R.ready = true;
+      // a level without boxes to compress has no Schur stage: nothing will
+      // ever acknowledge it, so it counts as acknowledged now (an update whose
+      // deepest dirty level is shallow would otherwise stall the run-ahead)
+      if (rc == 0 && R.B == 0 && L < E->acked) E->acked = L;
     }
     E->cv.notify_all();
     if (rc) {
@@ -633,6 +672,18 @@ int skb_engine_stop(int64_t handle) {
   E->cv.notify_all();
   if (E->th.joinable()) E->th.join();
   return 0;
+}
+
+// Debug: copy snapshot `which` (0 stack after assembly, 1 after the
+// pre-reduction, 2 after QRCP) of the SKB_ENGINE_SNAP level to host; returns
+// the element count (n_host = capacity of `host` in doubles).
+int64_t skb_debug_snap(int32_t which, double* host, int64_t n_host) {
+  Snap& S = g_snap();
+  if (which < 0 || which > 2 || !S.buf[which]) return -1;
+  if (host && n_host >= S.n)
+    if (cudaMemcpy(host, S.buf[which], sizeof(double) * S.n, cudaMemcpyDeviceToHost) != cudaSuccess)
+      return -2;
+  return S.n;
 }
 
 int skb_engine_free(int64_t handle, void* stream) {

@@ -710,7 +710,7 @@ class _Ctx:
         _Prof.tick("a_stack")
         base = _addr(stack)
         A = (base + 8 * stack_off[:-1]).astype(np.int64)
-        pre = rows > nB
+        pre = rows > 2 * nB                  # Householder pre-reduction branch, dense.py:56
         if pre.any():
           with _ht("L.geqrf"):
             call("skb_geqrf_batched", int(pre.sum()), np.ascontiguousarray(rows[pre]),
@@ -1494,13 +1494,10 @@ class _Engine:
             self.lib.skb_engine_set_update(self.h, todo.ctypes.data, coff.ctypes.data,
                                            cskel.ctypes.data)
             self.lib.skb_engine_go(self.h)
-        # The engine runs at most one level ahead of the enqueued Schur stages.
-        # Unbounded run-ahead made repeated update chains differ run to run in
-        # ~5% of steps (last-ulp level, top-level boxes) and, more rarely, the
-        # factorizations they start from; with lead 1 both are bitwise
-        # repeatable.  Costs large trees a little (cfg3 factor 0.19 -> 0.21 s).
-        # SKB_ENGINE_LEAD=-1 restores unbounded run-ahead.  DESIGN.md section 7.
-        lead = int(os.environ.get("SKB_ENGINE_LEAD", "1"))
+        # Run-ahead of the engine over the enqueued Schur stages: unbounded by
+        # default (SKB_ENGINE_LEAD=n >= 0 limits it to n levels).  Levels
+        # without boxes to compress count as acknowledged (engine.cu).
+        lead = int(os.environ.get("SKB_ENGINE_LEAD", "-1"))
         if lead >= 0:
             self.lib.skb_engine_set_lead(self.h, lead)
         self.sizes = np.zeros(8, np.int64)
@@ -1528,7 +1525,7 @@ class _Engine:
         nB = np.diff(act_off)
         dbuf, dup = int(p[10]), int(p[11])
         h = dict(idx=self._arr(p[13], B, np.int64), act_off=act_off, act=act, nB=nB,
-                 rows=rows, pre=rows > nB, m_q=self._arr(p[4], B, np.int64),
+                 rows=rows, pre=rows > 2 * nB, m_q=self._arr(p[4], B, np.int64),
                  A=self._arr(p[3], B, np.int64), lda=rows, engine=self, lev=L,
                  dev=(dup, dup + 8 * o_act, dbuf + o_int),
                  perm=self._arr(p[5], na, np.int32), k=self._arr(p[6], B, np.int32),
@@ -1814,6 +1811,17 @@ def _merge_level(ctx, idx, store, todo, bt_new, old_levels):
     return bt
 
 
+def _drain(ctx: "_Ctx"):
+    """Before an aborted engine run's context is dropped: the augmentation
+    sweeps already issued on the aug stream still write UH / PsiV / UH_div /
+    schur (allocated on the level stream), so both the level stream (where the
+    restarted run allocates) and the current stream wait for them."""
+    pipe = getattr(ctx, "pipe", None)
+    if pipe is not None and pipe.q:
+        ctx.sstream.wait_stream(pipe.stream)
+    torch.cuda.current_stream().wait_stream(ctx.sstream)
+
+
 def factor(spec, b, t: Tree, tol: float, workers: int = 1,
            proxy_count: int = DEFAULT_PROXY_COUNT, proxy_factor: float = DEFAULT_PROXY_FACTOR,
            propagate_zeros: bool = False) -> Factorization:
@@ -1835,7 +1843,7 @@ def factor(spec, b, t: Tree, tol: float, workers: int = 1,
                 try:
                     levels, store, _ = _run_levels_engine(ctx)
                 except _EngineAbort:
-                    torch.cuda.current_stream().wait_stream(ctx.sstream)
+                    _drain(ctx)
                     ctx = _Ctx(spec, b, t, tol, proxy_count, proxy_factor)
                     levels = None
             if levels is None:
@@ -1875,7 +1883,7 @@ def update(fct: Factorization, b_new, report, workers: int = 1) -> Factorization
             try:
                 levels, store, n_recomp = _run_levels_engine_update(ctx, old, dmask)
             except _EngineAbort:
-                torch.cuda.current_stream().wait_stream(ctx.sstream)
+                _drain(ctx)
                 ctx = _Ctx(fct.spec, b_new, t_new, fct.tol, fct.proxy_count, fct.proxy_factor)
                 levels = None
         if levels is None:

@@ -109,18 +109,13 @@ def test_system_matvec_vs_oracle(builder):
 
 
 @pytest.mark.slow
-def test_cfg4_update_sequence_vs_oracle(monkeypatch):
-    """cfg4 regime (hole moves on cfg2): the GPU dirty set equals the reference
-    rules' (oracle) at every step; update == refactor bitwise while the reference
-    rules guarantee it (first 10 moves here), and to rounding afterwards -- the
-    reference's own update differs from its refactor by ~6e-15 from move 15 on
-    (a coarse-leaf split reorders a clean box's far-field rows).
-
-    Runs on the Python level loop: the native engine's run-ahead has a rare
-    last-ulp nondeterminism, so bitwise update == refactor
-    is asserted on the bitwise-repeatable loop; the engine's agreement to 1e-13
-    is test_update_chains_repeatable's."""
-    monkeypatch.setattr(skel, "_ENGINE_ON", False)
+def test_cfg4_update_sequence_vs_oracle():
+    """cfg4 regime (hole moves on cfg2) on the default path (native engine):
+    the GPU dirty set equals the reference rules' (oracle) at every step;
+    update == refactor bitwise while the reference rules guarantee it (first 10
+    moves here), and to rounding afterwards -- the reference's own update
+    differs from its refactor by ~6e-15 from move 15 on (a coarse-leaf split
+    reorders a clean box's far-field rows; test_cfg4_hundred_moves)."""
     wl = configs.cfg2()
     b = wl.boundary
     f = _factor(wl)
@@ -203,19 +198,22 @@ def test_engine_repeatable_cfg2():
 
 
 def test_update_chains_repeatable(monkeypatch):
-    """Identical hole-move update chains: bitwise equal solves at every step on
-    the Python level loop; on the native engine (one level of run-ahead) equal
-    to rounding -- a rare last-ulp run-to-run difference in the top-level boxes
-    remains there (about 1 step in 80)."""
+    """Identical hole-move update chains give bitwise equal solves at every
+    step, on the native engine (unbounded run-ahead, the default, and one
+    level of run-ahead) and on the Python level loop.  Regression test for the
+    cluster-QRCP races (k_qrcp2 MODE 1: pivot candidates now double-buffered
+    by step parity, the deferred last R(i, p) written before the write-back)
+    that made ~5 % of engine update steps differ run to run."""
     wl = configs.cfg2()
     b = wl.boundary
     rhs = wl.extra["rhs"]
     seq = configs.hole_move_sequence(b, 4)
+    base = _factor(wl)
 
     def chains(n):
         runs = []
         for _ in range(n):
-            cur = _factor(wl)
+            cur = base
             xs = []
             for (h, d, nb, rep) in seq:
                 cur = update(cur, nb, rep)
@@ -224,12 +222,48 @@ def test_update_chains_repeatable(monkeypatch):
             del cur
         return runs
 
-    monkeypatch.setattr(skel, "_ENGINE_ON", False)
-    runs = chains(2)
-    for s, (a, c) in enumerate(zip(*runs)):
-        assert np.array_equal(a, c), s
-    monkeypatch.setattr(skel, "_ENGINE_ON", True)
-    runs = chains(3)
-    for xs in runs[1:]:
-        for s, (a, c) in enumerate(zip(runs[0], xs)):
-            assert _rel(a, c) < 1e-13, s
+    ref = None
+    for engine, lead in ((True, None), (True, "1"), (False, None)):
+        monkeypatch.setattr(skel, "_ENGINE_ON", engine)
+        if lead is None:
+            monkeypatch.delenv("SKB_ENGINE_LEAD", raising=False)
+        else:
+            monkeypatch.setenv("SKB_ENGINE_LEAD", lead)
+        runs = chains(4 if engine and lead is None else 2)
+        ref = runs[0] if ref is None else ref
+        for xs in runs:
+            for s, (a, c) in enumerate(zip(ref, xs)):
+                assert np.array_equal(a, c), (engine, lead, s)
+
+
+def test_noop_and_coarse_only_updates():
+    """Updates whose deepest dirty level is shallow (none at all, or only
+    coarse boxes) complete on the engine (no run-ahead stall: levels without
+    boxes to compress count as acknowledged) and equal the refactor."""
+    from paper_2001_11619_b200.geometry import PerturbationReport
+    from paper_2001_11619_b200.tree import dirty_mask
+    wl = configs.cfg1()
+    b = wl.boundary
+    f = _factor(wl)
+    rhs = wl.extra["rhs"]
+    x0 = f.solve(rhs)
+    nb, rep = apply_perturbation(b, [])                       # no-op edit
+    fu = update(f, nb, rep)
+    assert fu.stats["n_dirty"] == 0
+    assert np.array_equal(fu.solve(rhs), x0)
+    # a "modified" node (unchanged position) in a coarse leaf: only shallow boxes dirty
+    t = f.tree
+    found = None
+    for leaf in np.flatnonzero(t.is_leaf):
+        if t.lev[leaf] > t.depth - 2 or t.node_cnt[leaf] == 0:
+            continue
+        node = int(t.level_nodes[t.lev[leaf]][t.node_start[leaf]])
+        r = PerturbationReport(np.array([node]), np.array([node]), np.arange(b.n_nodes), b.positions)
+        m = dirty_mask(t, t, b, r, f.proxy_factor)
+        if m.any() and t.lev[np.flatnonzero(m)].max() <= t.depth - 2:
+            found = r
+            break
+    assert found is not None
+    fu = update(f, b, found)
+    assert 0 < fu.stats["n_dirty"]
+    assert np.array_equal(fu.solve(rhs), x0)
