@@ -1,17 +1,20 @@
 """Benchmark: level-batched skeletonization factorization on B200 (fp64).
 
-Headline (BASELINE.json metric, configs[1] = cfg2, 16-hole multiply-connected
-Stokes geometry, 49 200 unknowns): factorization unknowns/s.  One step = one
-full factorization (all levels + augmentation sweep + corner LU).  Secondary
-numbers: ms per local hole-move update (cfg4 regime on cfg2) and RHS/s of a
-256-RHS solve.
+Headline (BASELINE.json metric, its largest single-GPU configuration
+configs[2] = cfg3: outer circle R=40 + 256 ellipse holes, 295 680 unknowns,
+eps 1e-8, leaf 128, 96 proxies): factorization unknowns/s.  One step = build
+the quadtree + one full factorization (all levels, augmentation sweep, corner
+LU) with the geometry resident in HBM.  Secondary numbers on the same line:
+RHS/s of the 256-RHS solve on the cfg3 factorization (cfg5) and ms per local
+hole-move update on cfg2 (cfg4 regime, >= 20 moves).
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
 N > 1 (torchrun): independent replicas, one per GPU (the path does not shard,
 DESIGN.md "replicas only"); value = total unknowns of all ranks / max rank time.
 ``--impl reference`` times the CPU reference restatement (oracle/, the
-reference itself is pure Python and does not ship to the GPU box) on rank 0.
+reference itself is pure Python and does not ship to the GPU box) on rank 0,
+one full cfg3 factorization per step on all host cores (oracle/parallel.py).
 """
 
 from __future__ import annotations
@@ -118,28 +121,47 @@ def measure_fp64_peak(torch):
     return best
 
 
-def cpu_reference_run(wl, steps, warmup, budget_s=150.0):
-    """Time the CPU reference restatement (oracle) on the host cores."""
+def host_info():
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "cpu_count": os.cpu_count() or 1}
+
+
+def cpu_reference_run(wl, steps, warmup, procs=None, budget_s=None):
+    """The CPU reference restatement (oracle) on the host cores: per step the
+    quadtree build + one full factorization, boxes of a level and the
+    augmentation sweep spread over ``procs`` forked processes (bitwise the
+    serial oracle, oracle/parallel.py)."""
     from oracle import skel_oracle as O
+    from oracle import parallel as OP
     b = wl.boundary
-    ncores = os.cpu_count() or 1
-    cands = [1] if ncores == 1 else [1, ncores]
-    t_best, workers = None, 1
-    for w in cands[: max(1, warmup)] if warmup else cands[:1]:
+    procs = procs or os.cpu_count() or 1
+
+    def one():
         t0 = time.perf_counter()
-        O.factor_full(b, wl.leaf_cap, wl.tol, wl.proxy_count, wl.proxy_factor, workers=w)
-        dt = time.perf_counter() - t0
-        if t_best is None or dt < t_best:
-            t_best, workers = dt, w
+        OP.factor_full(b, wl.leaf_cap, wl.tol, wl.proxy_count, wl.proxy_factor, procs=procs)
+        return time.perf_counter() - t0
+
+    for _ in range(warmup):
+        one()
     times = []
     t_start = time.perf_counter()
     for _ in range(steps):
-        t0 = time.perf_counter()
-        O.factor_full(b, wl.leaf_cap, wl.tol, wl.proxy_count, wl.proxy_factor, workers=workers)
-        times.append(time.perf_counter() - t0)
-        if time.perf_counter() - t_start > budget_s:
+        times.append(one())
+        if budget_s is not None and time.perf_counter() - t_start > budget_s:
             break
-    return times, workers
+    return times, procs
+
+
+WORKLOAD = ("cfg3: outer circle R=40 (16384 nodes) + 256 ellipse holes (512 nodes each, "
+            "a~U[0.3,0.9], aspect U[1,3], seeded non-overlapping), Stokes double layer + "
+            "augmentation, eps=1e-8, leaf 128, proxy 96 @ 1.5x half-width")
 
 
 def main():
@@ -154,24 +176,29 @@ def main():
     rank, world, local = _dist()
 
     from paper_2001_11619_b200 import configs
-    wl = configs.cfg2()
+    wl = configs.cfg3()
     n_unk = 2 * wl.boundary.n_nodes + 3 * wl.boundary.n_holes
-    cfg = {"workload": "cfg2: outer circle R=10 (8192 nodes) + 16 holes r=0.5 (1024 nodes each), "
-                       "Stokes double layer + augmentation, eps=1e-10, leaf 64, proxy 64 @ 1.5x half-width",
-           "n_unknowns": n_unk, "seed": wl.seed, "parallelism": "replicas" if world > 1 else "single"}
+    cfg = {"workload": WORKLOAD, "n_unknowns": n_unk, "seed": wl.seed,
+           "parallelism": "replicas" if world > 1 else "single"}
 
     if args.impl == "reference":
         if rank != 0:
             return
-        times, workers = cpu_reference_run(wl, args.steps, args.warmup)
+        # the CPU path needs no warm-up beyond one untimed step (page faults, imports)
+        w = min(args.warmup, 1)
+        times, procs = cpu_reference_run(wl, args.steps, w)
         v = n_unk * len(times) / sum(times)
         line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": len(times),
-                "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(times)),
+                "warmup": w, "ms_per_step": 1e3 * float(np.mean(times)),
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic", "config": cfg, "impl": "reference",
-                "cpu_baseline": {"value": v, "unit": UNIT, "cores": workers, "kind": "port",
-                                 "sample": f"{len(times)} full cfg2 factorizations, oracle/skel_oracle.py "
-                                           f"(numpy/scipy restatement, workers={workers}, BLAS 1 thread)"},
+                "step_ms": [round(1e3 * x, 1) for x in times],
+                "cpu_baseline": {"value": v, "unit": UNIT, "cores": procs, "kind": "port",
+                                 "host": host_info(),
+                                 "sample": f"{len(times)} full cfg3 factorizations (quadtree build + "
+                                           f"factor), oracle/skel_oracle.py per-box code on {procs} "
+                                           f"forked processes (oracle/parallel.py, bitwise the serial "
+                                           f"oracle), BLAS 1 thread per process"},
                 "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return
@@ -193,11 +220,11 @@ def main():
 
     b = wl.boundary
     spec = SystemSpec()
-    tree = build_tree(b.positions, wl.leaf_cap)
     b._skb_device = S.DeviceBoundary(b)         # inputs resident in HBM for `value`
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")  # > L2 (126 MB)
 
     def step():
+        tree = build_tree(b.positions, wl.leaf_cap)     # fresh tree: no cached descriptors
         return factor(spec, b, tree, wl.tol, proxy_count=wl.proxy_count, proxy_factor=wl.proxy_factor)
 
     for _ in range(max(3, args.warmup)):
@@ -217,9 +244,9 @@ def main():
         times.append(e0.elapsed_time(e1))
         del f
     clk = clocks.stop()
-    # per-kernel-family device times from the library's CUDA-event timers, on two
-    # extra steps of the same workload (event records perturb the timed pipeline)
-    prof_steps = 2
+    # per-kernel-family device times from the library's CUDA-event timers, on one
+    # extra step of the same workload (event records perturb the timed pipeline)
+    prof_steps = 1
     _lib.prof_enable(True)
     _lib.prof_read(reset=True)
     for _ in range(prof_steps):
@@ -229,6 +256,7 @@ def main():
     torch.cuda.synchronize()
     fam = _lib.prof_read(reset=True)
     _lib.prof_enable(False)
+
     def reduce_max(x):
         t_ = torch.tensor([x], dtype=torch.float64, device="cuda")
         if world > 1:
@@ -259,37 +287,9 @@ def main():
     e2e_value, _ = aggregate(e2e_times, world, n_unk, reduce_max)
 
     line = None
-    fp64 = None
     if rank == 0:
         peaks = _peaks()
-        # the DGEMM peak probe (2 x 512 MB operands) runs after the secondary
-        # measurements; roofline is filled in then
-        fp64 = 35.5
         hbm = float(peaks.get("hbm_gbs", 6650.0))
-        # dominant kernel family by device time; DRAM traffic per launch from the
-        # committed ncu capture of one factorization (profiles/, scripts/ncu_traffic.py)
-        dom = max(fam, key=lambda k: fam[k]["ms"])
-        traffic = None
-        try:
-            tr = json.load(open(os.path.join(ROOT, "profiles", "r01_cfg2_traffic.json")))["families"]
-            # per launch of the family's timed scopes (bench launch count per step)
-            per_step = fam[dom]["launches"] / prof_steps
-            traffic = tr[dom]["dram_bytes"] / per_step if dom in tr and per_step else None
-        except Exception:
-            traffic = None
-        d = fam[dom]
-        per = max(d["launches"], 1)
-        if d["flops"] > 0:
-            ach = d["flops"] / (d["ms"] * 1e-3) / 1e12
-            roof = {"bound": "tensor", "achieved": ach, "peak": fp64, "unit": "TFLOP/s",
-                    "frac": ach / fp64, "traffic": traffic, "kernel": dom,
-                    "peak_source": "measured cuBLAS DGEMM 8192^3 (torch.matmul float64) in this run",
-                    "avg_launch_ms": d["ms"] / per}
-        else:
-            ach = d["bytes"] / (d["ms"] * 1e-3) / 1e9
-            roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
-                    "frac": ach / hbm, "traffic": traffic, "kernel": dom,
-                    "peak_source": "MEASURED_PEAKS.json hbm_gbs", "avg_launch_ms": d["ms"] / per}
         fam_summary = {k: {"ms_per_step": v["ms"] / prof_steps, "launches_per_step": v["launches"] / prof_steps,
                            **({"tflops": v["flops"] / (v["ms"] * 1e-3) / 1e12} if v["flops"] and v["ms"] else {}),
                            **({"gbs": v["bytes"] / (v["ms"] * 1e-3) / 1e9} if v["bytes"] and v["ms"] else {})}
@@ -297,31 +297,26 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": max(3, args.warmup), "ms_per_step": total_ms / args.steps,
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-                "data": "synthetic", "config": {**cfg, "l2": "flushed (256 MB write) before every timed step"},
+                "data": "synthetic", "config": cfg,
+                "l2": "flushed (256 MB write) before every timed step",
                 "step_ms": [round(x, 3) for x in times], "e2e_step_ms": [round(x, 3) for x in e2e_times],
-                "roofline": roof, "kernel_families": fam_summary,
-                "kernel_families_note": f"CUDA-event timers on {prof_steps} extra steps after the timed region", "fp64_dgemm_tflops": fp64,
+                "kernel_families": fam_summary,
+                "kernel_families_note": f"CUDA-event timers on {prof_steps} extra step(s) after the timed region",
                 "gpu_launches": int(launches),
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                         "d2h_bytes_per_step": int(d2h),
                         "path": "host Boundary -> build_tree -> factor() (public API), geometry + "
                                 "level descriptors H2D, ranks/pivots D2H inside the timed region"},
                 "clocks": clk}
+        line["_fam"] = (fam, prof_steps, hbm)
 
-    # ---- secondary: hole-move updates (cfg4 regime) and 256-RHS solve
+    # ---- secondary: cfg5 256-RHS solve on the cfg3 factorization, cfg4 hole-move updates on cfg2
     if rank == 0 and not args.no_secondary:
         import gc
         gc.collect()
         f = step()
-        seq = configs.hole_move_sequence(b, 12)
-        upd = []
-        cur = update(f, seq[0][2], seq[0][3])       # warm-up moves
-        cur = update(cur, seq[1][2], seq[1][3])
-        for _, _, nb, rep in seq[2:]:
-            torch.cuda.synchronize()
-            cur = update(cur, nb, rep)
-            upd.append(cur.stats["update_time"] * 1e3)
-        X = torch.from_numpy(np.random.default_rng(5).standard_normal((f.dim, 256))).cuda()
+        Xh = configs.cfg5_rhs(b, 256)
+        X = torch.from_numpy(Xh).cuda()
         f.solve(X)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -329,30 +324,98 @@ def main():
             f.solve(X)
         torch.cuda.synchronize()
         rhs_s = 3 * 256 / (time.perf_counter() - t0)
-        line["secondary"] = {"update_ms_mean": float(np.mean(upd)),
-                             "update_ms_median": float(np.median(upd)), "update_ms": upd,
-                             "update_n_dirty": cur.stats["n_dirty"], "solve_256rhs_per_s": rhs_s,
-                             "factor_ms": total_ms / args.steps}
+        Xp = torch.from_numpy(Xh).pin_memory()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(3):
+            Y = f.solve(Xp.cuda(non_blocking=True)).cpu()
+        rhs_s_e2e = 3 * 256 / (time.perf_counter() - t0)
+        del f, X, Y
+        gc.collect()
+        w2 = configs.cfg2()
+        b2 = w2.boundary
+        t2 = build_tree(b2.positions, w2.leaf_cap)
+        f2 = factor(spec, b2, t2, w2.tol, proxy_count=w2.proxy_count, proxy_factor=w2.proxy_factor)
+        seq = configs.hole_move_sequence(b2, 24)
+        upd, nd_ = [], []
+        cur = update(f2, seq[0][2], seq[0][3])       # warm-up moves
+        cur = update(cur, seq[1][2], seq[1][3])
+        for _, _, nb, rep in seq[2:]:
+            torch.cuda.synchronize()
+            cur = update(cur, nb, rep)
+            upd.append(cur.stats["update_time"] * 1e3)
+            nd_.append(cur.stats["n_dirty"])
+        line["secondary"] = {
+            "cfg5_solve_256rhs_per_s": rhs_s,
+            "cfg5_solve_256rhs_per_s_e2e": rhs_s_e2e,
+            "cfg5_note": "256 N(0,1) RHS padded with 768 zero lambda rows; device-resident, and host "
+                         "pinned in / host out (e2e)",
+            "cfg4_update_ms_mean": float(np.mean(upd)), "cfg4_update_ms_median": float(np.median(upd)),
+            "cfg4_update_ms": [round(x, 2) for x in upd], "cfg4_n_dirty_mean": float(np.mean(nd_)),
+            "cfg4_boxes": int(len(cur.tree.lev)),
+            "cfg4_note": f"{len(upd)} successive seeded hole moves (|d| = 0.1) on cfg2, wall time of "
+                         "update() incl. tree refit and dirty set",
+            "factor_ms": total_ms / args.steps}
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        times_c, workers = cpu_reference_run(wl, 2, 0, budget_s=30.0)
+        times_c, procs = cpu_reference_run(wl, 1, 0)
         line["cpu_baseline"] = {"value": n_unk * len(times_c) / sum(times_c), "unit": UNIT,
-                                "cores": workers, "kind": "port",
-                                "sample": f"{len(times_c)} full cfg2 factorization(s) with oracle/skel_oracle.py "
-                                          f"(numpy/scipy restatement of the reference, BLAS 1 thread)"}
+                                "cores": procs, "kind": "port", "host": host_info(),
+                                "sample": f"{len(times_c)} full cfg3 factorization(s) (quadtree build "
+                                          f"+ factor) with the oracle's per-box code on {procs} forked "
+                                          f"processes (oracle/parallel.py), BLAS 1 thread each"}
     if rank == 0:
-        gc_ = __import__("gc")
+        import gc as gc_
         gc_.collect()
         fp64 = measure_fp64_peak(torch)
+        fam, prof_steps, hbm = line.pop("_fam")
         line["fp64_dgemm_tflops"] = fp64
-        roof = line["roofline"]
-        if roof["unit"] == "TFLOP/s":
-            roof["peak"] = fp64
-            roof["frac"] = roof["achieved"] / fp64
+        line["roofline"] = roofline(fam, prof_steps, fp64, hbm)
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.barrier()
         torch.distributed.destroy_process_group()
+
+
+TRAFFIC = os.path.join(ROOT, "profiles", "r02_cfg3_traffic.json")
+
+
+def roofline(fam, prof_steps, fp64, hbm):
+    """Dominant kernel family by device time against its bound (DMMA peak for
+    flop-counted families, HBM for byte-counted ones), plus the HBM fraction
+    of assembly + ID (north_star's second roofline)."""
+    traffic = {}
+    try:
+        traffic = json.load(open(TRAFFIC))["families"]
+    except Exception:
+        traffic = {}
+    dom = max(fam, key=lambda k: fam[k]["ms"])
+    d = fam[dom]
+    per = max(d["launches"], 1)
+    tr = traffic.get(dom, {}).get("dram_bytes_per_launch")
+    if d["flops"] > 0:
+        ach = d["flops"] / (d["ms"] * 1e-3) / 1e12
+        roof = {"bound": "tensor", "achieved": ach, "peak": fp64, "unit": "TFLOP/s", "frac": ach / fp64,
+                "traffic": tr, "kernel": dom,
+                "peak_source": "measured cuBLAS DGEMM 8192^3 (torch.matmul float64) in this run",
+                "avg_launch_ms": d["ms"] / per}
+    else:
+        ach = d["bytes"] / (d["ms"] * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                "traffic": tr, "kernel": dom, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                "avg_launch_ms": d["ms"] / per}
+    # assembly + ID as HBM work: stack / self-block bytes written by assembly, stack
+    # (or R) bytes read by the Householder pre-reduction and the QRCP
+    ks = ("assemble", "geqrf", "qrcp")
+    by = sum(fam.get(k, {}).get("bytes", 0.0) for k in ks)
+    id_ms = sum(fam.get(k, {}).get("ms", 0.0) for k in ks)
+    if by and id_ms:
+        gbs = by / (id_ms * 1e-3) / 1e9
+        roof["assembly_id_hbm"] = {"achieved": gbs, "peak": hbm, "unit": "GB/s", "frac": gbs / hbm,
+                                   "bytes_per_step": by / prof_steps,
+                                   "note": "algorithmic bytes (assembly writes + stack/R reads of "
+                                           "geqrf and QRCP) / their summed device time"}
+    return roof
 
 
 if __name__ == "__main__":

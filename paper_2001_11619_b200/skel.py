@@ -776,12 +776,14 @@ class _Ctx:
             rows, pre = h["rows"], h["pre"]
             _lib.prof_add("assemble", 0.0, 8.0 * float((rows * nB).sum() + (nB * nB).sum()))
             mr, nr_ = rows[pre].astype(float), nB[pre].astype(float)
-            _lib.prof_add("geqrf", float((2 * mr * nr_ ** 2 - 2.0 / 3.0 * nr_ ** 3).sum()))
+            # geqrf / QRCP bytes: the stack (or R) they read once from HBM
+            _lib.prof_add("geqrf", float((2 * mr * nr_ ** 2 - 2.0 / 3.0 * nr_ ** 3).sum()),
+                          8.0 * float((mr * nr_).sum()))
             fq = 0.0
             for mm, nn, st in zip(h["m_q"], nB, bt.steps):
                 i_ = np.arange(st, dtype=float)
                 fq += 2.0 * mm * nn + float((4.0 * (mm - i_) * (nn - i_ - 1)).sum())
-            _lib.prof_add("qrcp", fq)
+            _lib.prof_add("qrcp", fq, 8.0 * float((h["m_q"] * nB).sum()))
         # factor storage (one slab), allocated for the level stream that fills it
         dev = _dev()
         with torch.cuda.stream(self.sstream):
