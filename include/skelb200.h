@@ -233,6 +233,17 @@ int skb_system_matvec(const double* pos, const double* nrm, const double* w, con
                       int64_t n_nodes, const double* hole_centers, int64_t n_holes,
                       const int64_t* curve_off_dev, const double* x, int64_t nrhs, double* y,
                       void* stream);
+/* Field at interior targets from a solve() output, out (2m x nrhs) row-major:
+ * u = D mu + H lam (reference evaluate_interior skel.py:537-564,
+ * eval_forward_block kernels.py:171-198).  x: (2N + 3p) x nrhs row-major.    */
+int skb_eval_interior(const double* pos, const double* nrm, const double* w, int64_t n_nodes,
+                      const double* hole_centers, int64_t n_holes, const double* x, int64_t nrhs,
+                      const double* targets, int64_t m, double* out, void* stream);
+/* Boundary.point_in_domain (reference geometry.py:179-192): winding numbers of
+ * the node polylines (curve_off: ncurves + 1 node offsets, device) and
+ * nearest-node distance > 1e-12; inside[m] = 1 / 0.                           */
+int skb_point_in_domain(const double* pos, const int64_t* curve_off_dev, int64_t ncurves,
+                        const double* targets, int64_t m, uint8_t* inside, void* stream);
 
 /* dst[idx[i]*ld + c] = value for i < nidx, c < ncols (the nonroot mask of
  * skel.py:181-188 applied by zeroing root rows of a copy). unused: NULL.    */

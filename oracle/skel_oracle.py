@@ -221,6 +221,70 @@ def aug_functionals(g):
     return Psi
 
 
+def winding(points, poly, chunk=512):
+    """Integer winding numbers of a closed polyline, geometry.py:221-233."""
+    out = np.empty(len(points), dtype=np.int64)
+    nxt = np.roll(poly, -1, axis=0)
+    for s in range(0, len(points), chunk):
+        p = points[s:s + chunk]
+        a = poly[None, :, :] - p[:, None, :]
+        b = nxt[None, :, :] - p[:, None, :]
+        cross = a[..., 0] * b[..., 1] - a[..., 1] * b[..., 0]
+        dot = (a * b).sum(-1)
+        ang = np.arctan2(cross, dot).sum(axis=1)
+        out[s:s + chunk] = np.rint(ang / (2 * np.pi)).astype(np.int64)
+    return out
+
+
+def point_in_domain(g, points):
+    """Boundary.point_in_domain, geometry.py:179-199 (winding + nearest node)."""
+    from scipy.spatial import cKDTree
+    pts = np.atleast_2d(np.asarray(points, float))
+    inside = winding(pts, g.curves[0].nodes) != 0
+    for c in g.curves[1:]:
+        inside &= winding(pts, c.nodes) == 0
+    d, _ = cKDTree(g.positions).query(pts)
+    return inside & (d > 1e-12)
+
+
+def forward_block(g, targets, cols):
+    """Interior-evaluation rows (Stokes), kernels.py:171-198."""
+    targets = np.atleast_2d(np.asarray(targets, float))
+    nc, cc = _split(cols)
+    pc = g.positions[nc]
+    rx = targets[:, None, 0] - pc[None, :, 0]
+    ry = targets[:, None, 1] - pc[None, :, 1]
+    r2 = rx * rx + ry * ry
+    w = g.weights[nc][None, :]
+    nsc = g.normals[nc]
+    rdn = rx * nsc[None, :, 0] + ry * nsc[None, :, 1]
+    coef = rdn / (np.pi * r2 * r2) * w
+    rcb = np.where((cc == 0)[None, :], rx, ry)
+    out = np.empty((2 * len(targets), len(nc)))
+    out[0::2] = coef * rx * rcb
+    out[1::2] = coef * ry * rcb
+    return out
+
+
+def evaluate_interior(g, solution, targets, chunk=256):
+    """u = D mu + H lam at interior targets, skel.py:537-564 (Stokes)."""
+    targets = np.atleast_2d(np.asarray(targets, float))
+    if not np.all(point_in_domain(g, targets)):
+        raise ValueError("targets must lie strictly inside the domain")
+    sol = np.asarray(solution, float)
+    nd = 2 * len(g.positions)
+    mu, lam = sol[:nd], sol[nd:]
+    dofs = np.arange(nd)
+    out = np.empty((len(targets), 2))
+    for s in range(0, len(targets), chunk):
+        tt = targets[s:s + chunk]
+        vals = forward_block(g, tt, dofs) @ mu
+        if len(lam):
+            vals = vals + aug_columns(tt, g.hole_centers) @ lam
+        out[s:s + chunk] = vals.reshape(-1, 2)
+    return out
+
+
 def dense_system(g):
     """Full augmented matrix, kernels.py:377-390."""
     nd = 2 * len(g.positions)

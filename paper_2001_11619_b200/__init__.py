@@ -10,6 +10,7 @@ from .geometry import (Boundary, Curve, GeometryError, MoveHole, PerturbationRep
                        apply_perturbation)
 from .tree import Tree, TreeError, build_tree, default_root_box, proxy_radius, refit_tree
 from .skel import (BoxFactors, Factorization, RootBoxExceededError, SingularPivotError, STOKES,
-                   SystemSpec, factor, system_matvec, update)
+                   SystemSpec, evaluate_interior, factor, point_in_domain,
+                   system_matvec, update)
 
 __version__ = "0.1.0"

@@ -59,6 +59,8 @@ SIGNATURES = {
     "skb_psi_dot": [_i64, _vp, _vp, _vp, _i64, _vp, _i64, _i64, _vp, _i64, _f64, _vp, _i64, _vp],
     "skb_sum_partials": [_i64, _i32, _vp, _i64, _vp, _f64, _vp, _vp],
     "skb_system_matvec": [_vp, _vp, _vp, _vp, _i64, _vp, _i64, _vp, _vp, _i64, _vp, _vp],
+    "skb_eval_interior": [_vp, _vp, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _vp],
+    "skb_point_in_domain": [_vp, _vp, _i64, _vp, _i64, _vp, _vp],
     "skb_level_schur": [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                         _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "skb_level_aug": [_i64, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,

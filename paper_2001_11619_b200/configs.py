@@ -102,13 +102,17 @@ def holes_circle(seed: int, R: float, n_outer: int, n_holes: int, r_hole: float,
     return Boundary(curves)
 
 
-def cfg2(seed: int = 0) -> Workload:
-    """Outer circle R=10 (8192 nodes) + 16 holes r=0.5 (1024 nodes), centres sep >= 1.5."""
-    b = holes_circle(seed, 10.0, 8192, 16, 0.5, 1024, 1.5, 8.5, phases=True)
+def cfg2(seed: int = 0, phases: bool = True) -> Workload:
+    """Outer circle R=10 (8192 nodes) + 16 holes r=0.5 (1024 nodes), centres sep >= 1.5.
+    ``phases=False`` keeps every curve's nodes at t_j = 2 pi j / n: the mirror
+    symmetries of equispaced circles then produce exact QRCP pivot ties (the
+    tie-rich parity fixture)."""
+    b = holes_circle(seed, 10.0, 8192, 16, 0.5, 1024, 1.5, 8.5, phases=phases)
     rng = np.random.default_rng(seed + 1000)
     f = rng.standard_normal(2 * b.n_nodes)
     rhs = np.concatenate([f, np.zeros(3 * b.n_holes)])
-    return Workload("cfg2_16holes_N24576", b, 1e-10, 64, 64, seed=seed, extra={"rhs": rhs})
+    return Workload("cfg2_16holes_N24576" + ("" if phases else "_unphased"), b, 1e-10, 64, 64,
+                    seed=seed, extra={"rhs": rhs})
 
 
 def cfg3(seed: int = 0) -> Workload:
@@ -150,6 +154,27 @@ def mini_holes(seed: int = 0, n_outer: int = 1024, n_holes: int = 3, n_per_hole:
     rng = np.random.default_rng(seed + 7)
     rhs = np.concatenate([rng.standard_normal(2 * b.n_nodes), np.zeros(3 * n_holes)])
     return Workload(f"mini_{n_holes}holes", b, 1e-10, 64, 64, seed=seed, extra={"rhs": rhs})
+
+
+def interior_targets(b: Boundary, m: int, seed: int = 9, exterior: int = 0) -> np.ndarray:
+    """Seeded evaluation points inside the fluid domain (inside the outer curve
+    at radius < 0.9 of its smallest node radius, >= 0.1 away from every hole's
+    bounding circle), plus ``exterior`` points inside holes / outside the
+    outer curve for the rejection path."""
+    rng = np.random.default_rng(seed)
+    rmin = np.sqrt((b.curves[0].nodes ** 2).sum(axis=1)).min()
+    ctr = b.hole_centers
+    rad = np.array([c.bound_radius for c in b.curves[1:]])
+    out = []
+    while len(out) < m:
+        u, v = rng.random(2)
+        p = 0.9 * rmin * np.sqrt(u) * np.array([np.cos(2 * np.pi * v), np.sin(2 * np.pi * v)])
+        if len(ctr) and np.any(np.sqrt(((ctr - p) ** 2).sum(axis=1)) < rad + 0.1):
+            continue
+        out.append(p)
+    ext = [ctr[i % len(ctr)] for i in range(exterior)] if len(ctr) else []
+    ext += [np.array([2.0 * rmin, 0.0])] * (exterior - len(ext))
+    return np.array(out + ext).reshape(-1, 2)
 
 
 def hole_move_sequence(b: Boundary, steps: int, seed: int = 4, step_len: float = 0.1,

@@ -156,6 +156,104 @@ __global__ void k_mv_psi(const double2* __restrict__ pos, const double* __restri
   }
 }
 
+
+// Interior evaluation u(t) = D mu + H lam at targets off the boundary --
+// reference evaluate_interior (skel.py:537-564) with eval_forward_block
+// (kernels.py:171-198, Stokes: no jump, no completion term) and
+// stokeslet_rotlet_columns (kernels.py:201-223).  One thread per target,
+// sources tiled through shared memory, summed in node order.
+__global__ void __launch_bounds__(MV_T)
+k_eval_interior(const double2* __restrict__ pos, const double2* __restrict__ nrm,
+                const double* __restrict__ w, int64_t n, const double2* __restrict__ ctr,
+                int64_t p, const double* __restrict__ x, int64_t nr, int64_t r0, int rc,
+                const double2* __restrict__ tgt, int64_t m, double* __restrict__ out) {
+  __shared__ double2 sp[MV_T], sn[MV_T];
+  __shared__ double sw[MV_T];
+  __shared__ double sx[MV_T][2 * MV_R];
+  const int64_t i = blockIdx.x * (int64_t)MV_T + threadIdx.x;
+  const bool act = i < m;
+  const double2 ti = act ? tgt[i] : make_double2(0, 0);
+  double a0[MV_R] = {0, 0, 0, 0}, a1[MV_R] = {0, 0, 0, 0};
+  for (int64_t j0 = 0; j0 < n; j0 += MV_T) {
+    __syncthreads();
+    const int64_t j = j0 + threadIdx.x;
+    if (j < n) {
+      sp[threadIdx.x] = pos[j];
+      sn[threadIdx.x] = nrm[j];
+      sw[threadIdx.x] = w[j];
+      for (int q = 0; q < rc; ++q) {
+        sx[threadIdx.x][2 * q] = x[(2 * j) * nr + r0 + q];
+        sx[threadIdx.x][2 * q + 1] = x[(2 * j + 1) * nr + r0 + q];
+      }
+    }
+    __syncthreads();
+    const int jn = (int)((n - j0) < MV_T ? (n - j0) : MV_T);
+    if (!act) continue;
+    for (int jj = 0; jj < jn; ++jj) {
+      const double2 pj = sp[jj], nj = sn[jj];
+      const double rx = ti.x - pj.x, ry = ti.y - pj.y;
+      const double r2 = rx * rx + ry * ry;
+      const double c = (rx * nj.x + ry * nj.y) / (MV_PI * r2 * r2) * sw[jj];
+      for (int q = 0; q < MV_R; ++q) {
+        if (q >= rc) break;
+        const double proj = rx * sx[jj][2 * q] + ry * sx[jj][2 * q + 1];
+        a0[q] += c * rx * proj;
+        a1[q] += c * ry * proj;
+      }
+    }
+  }
+  if (!act) return;
+  const double pref = 1.0 / (4.0 * MV_PI);
+  for (int q = 0; q < rc; ++q) {
+    double y0 = a0[q], y1 = a1[q];
+    for (int64_t h = 0; h < p; ++h) {
+      const double2 c = ctr[h];
+      const double rx = ti.x - c.x, ry = ti.y - c.y;
+      const double r2 = rx * rx + ry * ry;
+      const double lg = -0.5 * log(r2);
+      const double l0 = x[(2 * n + 3 * h) * nr + r0 + q];
+      const double l1 = x[(2 * n + 3 * h + 1) * nr + r0 + q];
+      const double l2 = x[(2 * n + 3 * h + 2) * nr + r0 + q];
+      y0 += pref * (lg + rx * rx / r2) * l0 + pref * (rx * ry / r2) * l1 + pref * (-ry) / r2 * l2;
+      y1 += pref * (ry * rx / r2) * l0 + pref * (lg + ry * ry / r2) * l1 + pref * rx / r2 * l2;
+    }
+    out[(2 * i) * nr + r0 + q] = y0;
+    out[(2 * i + 1) * nr + r0 + q] = y1;
+  }
+}
+
+// Boundary.point_in_domain (reference geometry.py:179-192, _winding
+// geometry.py:221-233): winding number of every curve's node polyline around
+// each target (inside the outer curve, outside every hole) and nearest-node
+// distance > 1e-12.  One warp per target; per-curve angle sums in node order
+// per lane, then a fixed-order warp reduction.
+__global__ void k_point_in_domain(const double2* __restrict__ pos, const int64_t* __restrict__ off,
+                                  int64_t ncurves, const double2* __restrict__ tgt, int64_t m,
+                                  uint8_t* __restrict__ inside) {
+  const int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (t >= m) return;
+  const double2 q = tgt[t];
+  bool ok = true;
+  double dmin2 = 1e300;
+  for (int64_t c = 0; c < ncurves; ++c) {
+    const int64_t a = off[c], b = off[c + 1];
+    double ang = 0.0;
+    for (int64_t j = a + lane; j < b; j += 32) {
+      const double2 p0 = pos[j], p1 = pos[j + 1 < b ? j + 1 : a];
+      const double ax = p0.x - q.x, ay = p0.y - q.y, bx = p1.x - q.x, by = p1.y - q.y;
+      ang += atan2(ax * by - ay * bx, ax * bx + ay * by);
+      dmin2 = fmin(dmin2, ax * ax + ay * ay);
+    }
+    ang = warp_sum(ang);
+    const double wn = rint(ang / (2.0 * MV_PI));
+    ok = ok && (c == 0 ? wn != 0.0 : wn == 0.0);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) dmin2 = fmin(dmin2, __shfl_xor_sync(0xffffffffu, dmin2, o));
+  if (lane == 0) inside[t] = (ok && sqrt(dmin2) > 1e-12) ? 1 : 0;
+}
+
 }  // namespace skb
 
 using namespace skb;
@@ -182,4 +280,30 @@ extern "C" int skb_system_matvec(const double* pos, const double* nrm, const dou
   cudaError_t e = cudaGetLastError();
   cudaFreeAsync(parts, s);
   return e == cudaSuccess ? 0 : -(int)e;
+}
+
+extern "C" int skb_eval_interior(const double* pos, const double* nrm, const double* w,
+                                 int64_t n_nodes, const double* hole_centers, int64_t n_holes,
+                                 const double* x, int64_t nrhs, const double* targets, int64_t m,
+                                 double* out, void* stream) {
+  if (m <= 0 || nrhs <= 0) return 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  for (int64_t r0 = 0; r0 < nrhs; r0 += MV_R) {
+    const int rc = (int)((nrhs - r0) < MV_R ? (nrhs - r0) : MV_R);
+    k_eval_interior<<<(unsigned)((m + MV_T - 1) / MV_T), MV_T, 0, s>>>(
+        (const double2*)pos, (const double2*)nrm, w, n_nodes, (const double2*)hole_centers, n_holes,
+        x, nrhs, r0, rc, (const double2*)targets, m, out);
+  }
+  SKB_LAUNCH_CHECK();
+  return 0;
+}
+
+extern "C" int skb_point_in_domain(const double* pos, const int64_t* curve_off_dev, int64_t ncurves,
+                                   const double* targets, int64_t m, uint8_t* inside, void* stream) {
+  if (m <= 0) return 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  k_point_in_domain<<<(unsigned)((m * 32 + 255) / 256), 256, 0, s>>>(
+      (const double2*)pos, curve_off_dev, ncurves, (const double2*)targets, m, inside);
+  SKB_LAUNCH_CHECK();
+  return 0;
 }

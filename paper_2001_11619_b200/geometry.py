@@ -78,6 +78,12 @@ class Boundary:
     def curve_nodes(self, c: int) -> np.ndarray:
         return np.arange(self.offsets[c], self.offsets[c + 1])
 
+    def point_in_domain(self, points) -> np.ndarray:
+        """Strictly inside the fluid domain (reference geometry.py:179-192); the
+        winding numbers run on the GPU (skel.point_in_domain)."""
+        from .skel import point_in_domain
+        return point_in_domain(self, points)
+
     def curve_of_node(self) -> np.ndarray:
         out = np.empty(self.n_nodes, dtype=np.int64)
         for c in range(len(self.curves)):

@@ -1925,3 +1925,52 @@ def system_matvec(spec, b, x):
         return Y.reshape(x.shape)
     out = Y.cpu().numpy()
     return out.reshape(np.asarray(x).shape)
+
+
+def point_in_domain(b, points) -> np.ndarray:
+    """True where a point lies strictly inside the fluid domain (reference
+    Boundary.point_in_domain, geometry.py:179-192): winding number of every
+    curve's node polyline (inside the outer curve, outside each hole) and
+    nearest node farther than 1e-12 -- one warp per point on the GPU."""
+    pts = np.ascontiguousarray(np.atleast_2d(np.asarray(points, float)), np.float64)
+    m = len(pts)
+    if m == 0:
+        return np.zeros(0, bool)
+    g = getattr(b, "_skb_device", None) or DeviceBoundary(b)
+    up = _upload(co=np.ascontiguousarray(b.offsets, np.int64), tg=pts.reshape(-1))
+    out = torch.empty(m, dtype=torch.uint8, device=_dev())
+    call("skb_point_in_domain", g.pos, up["co"], len(b.offsets) - 1, up["tg"], m, out, _stream())
+    return out.cpu().numpy().astype(bool)
+
+
+def evaluate_interior(spec, b, solution, targets, chunk: int = 256):
+    """Field at interior targets from a solve() output (reference
+    evaluate_interior, skel.py:537-564): u = D mu + H lam by direct summation
+    on the GPU (eval_forward_block kernels.py:171-198 + the Stokeslet/rotlet
+    columns kernels.py:201-223).  Returns (m, 2); ``solution`` may also be a
+    (dim, nrhs) matrix (then (m, 2, nrhs)).  Exterior targets are rejected.
+    ``chunk`` is accepted for signature parity (all targets run in one launch)."""
+    tg = np.ascontiguousarray(np.atleast_2d(np.asarray(targets, float)), np.float64)
+    if not np.all(point_in_domain(b, tg)):
+        raise ValueError("targets must lie strictly inside the domain")
+    is_t = isinstance(solution, torch.Tensor)
+    sol = solution if is_t else np.asarray(solution, float)
+    nd, q = 2 * b.n_nodes, 3 * b.n_holes if spec.augmented(b) else 0
+    if sol.shape[0] != nd + q:
+        raise ValueError("dimension mismatch")
+    vec = sol.ndim == 1
+    dev = _dev()
+    X = (sol.to(device=dev, dtype=torch.float64) if is_t
+         else torch.from_numpy(np.ascontiguousarray(sol)).to(dev)).reshape(nd + q, -1).contiguous()
+    nr = X.shape[1]
+    g = getattr(b, "_skb_device", None) or DeviceBoundary(b)
+    up = _upload(hc=np.ascontiguousarray(b.hole_centers, np.float64).reshape(-1)
+                 if b.n_holes else np.zeros(2), tg=tg.reshape(-1))
+    m = len(tg)
+    Y = torch.empty((2 * m, nr), dtype=torch.float64, device=dev)
+    call("skb_eval_interior", g.pos, g.nrm, g.w, b.n_nodes, up["hc"], q // 3, X, nr, up["tg"], m, Y,
+         _stream())
+    Y = Y.reshape(m, 2, nr)
+    if vec:
+        Y = Y[:, :, 0]
+    return Y if is_t else Y.cpu().numpy()

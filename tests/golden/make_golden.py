@@ -160,6 +160,11 @@ def main():
     X = rng.standard_normal((fct.dim, 3))
     out["cfg1_multi_in"] = X
     out["cfg1_multi_x"] = fct.solve(X)
+    # interior evaluation (skel.py:537-564) and the domain test (geometry.py:179-192)
+    tg = configs.interior_targets(wl.boundary, 64, exterior=2)
+    out["cfg1_targets"] = tg
+    out["cfg1_in_domain"] = b.point_in_domain(tg)
+    out["cfg1_interior"] = s.evaluate_interior(spec, b, x, tg[:64])
     print("cfg1 boxes", len(rec), "k/level", fct.stats["k_per_level"], "root", fct.stats["root_size"])
 
     # ---- mini multiply-connected case + one hole-move update
@@ -176,6 +181,10 @@ def main():
     out["mini_apply_in"] = v
     out["mini_apply_out"] = fct.apply(v)
     out["mini_corner_n"] = np.array(fct.top.n)
+    tg = configs.interior_targets(wl.boundary, 64, exterior=3)
+    out["mini_targets"] = tg
+    out["mini_in_domain"] = b.point_in_domain(tg)
+    out["mini_interior"] = s.evaluate_interior(spec, b, out["mini_x"], tg[:64])
     # hole move through the reference's own apply_perturbation/update
     nb_mine, rep_mine = apply_perturbation(wl.boundary, [MoveHole(2, translation=(0.1, -0.05))])
     b_new, rep = s.apply_perturbation(b, [s.MoveHole(2, translation=(0.1, -0.05))])
@@ -197,6 +206,21 @@ def main():
     out["mini_upd_dirty"] = np.array(sorted(dirty_seen["d"]), dtype=np.int64)
     out["mini_upd_x"] = fu.solve(rhs)
     print("mini boxes", len(rec), "k/level", fct.stats["k_per_level"], "n_dirty", fu.stats["n_dirty"])
+
+    # ---- unphased cfg2: equispaced circles centred on box axes -> exact pivot
+    # ties; per-box active sets, skeletons and |R_jj| for the tie-classified replay
+    wl = configs.cfg2(phases=False)
+    b, spec, tree, fct, rec = record_factor(s, wl)
+    keys = sorted(rec)
+    out["cfg2u_keys"] = np.array(keys, dtype=np.int64)
+    out["cfg2u_k"] = np.array([rec[k]["k"] for k in keys], dtype=np.int64)
+    for nm, fld in (("S", "S"), ("act", "active"), ("diag", "diag")):
+        arrs = [np.asarray(rec[k][fld]) for k in keys]
+        out[f"cfg2u_{nm}_off"] = np.concatenate([[0], np.cumsum([len(x) for x in arrs])]).astype(np.int64)
+        out[f"cfg2u_{nm}"] = np.concatenate(arrs)
+    out["cfg2u_root_dofs"] = np.array(fct.root_dofs, dtype=np.int64)
+    out["cfg2u_x"] = fct.solve(wl.extra["rhs"])
+    print("cfg2 unphased boxes", len(rec), "k/level", fct.stats["k_per_level"])
 
     path = os.path.join(HERE, "reference_golden.npz")
     np.savez_compressed(path, **{k: np.asarray(v) for k, v in out.items()})

@@ -213,23 +213,22 @@ def test_self_block_bitwise(name, builder):
         assert np.array_equal(got, ref)
 
 
-@pytest.mark.parametrize("name,builder", [("cfg1_", configs.cfg1), ("mini_", configs.mini_holes)])
-def test_id_replay_skeletons(golden, name, builder):
-    """(b) Replay every box on the reference's exact active sets: GPU stack ->
-    Householder -> QRCP must select the reference's skeleton (same order)."""
-    wl = builder()
+def _replay_ids(wl, ref):
+    """Run the ID part (GPU stack -> Householder -> QRCP) of every box on the
+    reference's exact active sets, level by level; returns the boxes whose
+    skeleton (set and order) differs: (key, k_gpu, k_ref, gpu min pivot gap,
+    reference threshold margin)."""
     t = build_tree(wl.boundary.positions, wl.leaf_cap)
     ctx = skel._Ctx(skel.SystemSpec(), wl.boundary, t, wl.tol, wl.proxy_count, wl.proxy_factor)
-    ref = _golden_boxes(golden, name)
     act_of = {j: ref[t.key(j)]["act"] for j in range(len(t.lev)) if t.key(j) in ref}
+    store = skel.ActStore.replay(t, act_of)
     mism = []
     for lev in range(t.depth, 0, -1):
         idx = t.level_indices(lev)
-        # run only the ID part (stack + QR) to avoid needing children's Xss
         B = len(idx)
         act_off, act = skel._csr([act_of[int(i)] for i in idx])
         nB = np.diff(act_off)
-        far_off, far = ctx.far_lists(idx, skel.ActStore.replay(t, act_of))
+        far_off, far = ctx.far_lists(idx, store)
         nF = np.diff(far_off)
         pts, pn, pw = ctx.proxies(idx)
         P = wl.proxy_count
@@ -243,9 +242,11 @@ def test_id_replay_skeletons(golden, name, builder):
         call("skb_assemble_stack", g.pos, g.nrm, g.w, B, up["ao"], up["a"], up["fo"], up["f"],
              up["pts"], up["pn"], up["pw"], P, up["so"], st, int(nB.max()), int((nF + P + 1).max()), s)
         A = (st.data_ptr() + 8 * so[:-1]).astype(np.int64)
-        pre = rows > nB
-        call("skb_geqrf_batched", int(pre.sum()), np.ascontiguousarray(rows[pre]),
-             np.ascontiguousarray(nB[pre]), np.ascontiguousarray(rows[pre]), np.ascontiguousarray(A[pre]), s)
+        pre = rows > 2 * nB                      # dense.py:56
+        if pre.any():
+            call("skb_geqrf_batched", int(pre.sum()), np.ascontiguousarray(rows[pre]),
+                 np.ascontiguousarray(nB[pre]), np.ascontiguousarray(rows[pre]),
+                 np.ascontiguousarray(A[pre]), s)
         mq = np.where(pre, nB, rows).astype(np.int64)
         perm = torch.empty(len(act), dtype=torch.int32, device="cuda")
         diag = torch.empty(len(act), dtype=torch.float64, device="cuda")
@@ -260,11 +261,45 @@ def test_id_replay_skeletons(golden, name, builder):
             r = ref[t.key(i)]
             S = pm[act_off[bi]:act_off[bi] + kk[bi]]
             if kk[bi] != r["k"] or not np.array_equal(S, r["S"]):
-                mism.append((t.key(i), int(kk[bi]), r["k"], float(gp[bi])))
+                margin = np.inf
+                d = r.get("diag")
+                if d is not None and len(d) and d[0] > 0:
+                    thr = wl.tol * abs(d[0])
+                    near = [abs(abs(d[j]) / thr - 1.0) for j in (r["k"] - 1, r["k"]) if 0 <= j < len(d)]
+                    margin = min(near) if near else np.inf
+                mism.append((t.key(i), int(kk[bi]), r["k"], float(gp[bi]), float(margin)))
+    return mism
+
+
+@pytest.mark.parametrize("name,builder", [("cfg1_", configs.cfg1), ("mini_", configs.mini_holes)])
+def test_id_replay_skeletons(golden, name, builder):
+    """(b) Replay every box on the reference's exact active sets: GPU stack ->
+    Householder -> QRCP must select the reference's skeleton (same order)."""
+    mism = _replay_ids(builder(), _golden_boxes(golden, name))
     # a mismatch is acceptable only as a pivot tie within rounding (SURVEY.md §8(c)1)
     untied = [m for m in mism if m[3] > 1e-12]
     assert not untied, untied
-    assert not mism, mism      # these fixtures were chosen tie-free
+    assert not mism, mism      # these fixtures are tie-free
+
+
+def test_id_replay_tie_rich_cfg2(golden):
+    """Tie-rich fixture (unphased cfg2: equispaced circles centred on quadtree
+    axes give exact pivot ties): per-level replay of every box on the
+    reference's active sets.  Every skeleton that differs from the reference's
+    must be a tie within rounding -- GPU minimum relative pivot gap <= 1e-12 --
+    or a rank decided within rounding of the threshold (|R_kk| within 1e-10 of
+    tol |R_00|); SURVEY.md §8(c) item 1."""
+    wl = configs.cfg2(phases=False)
+    keys = [tuple(k) for k in golden["cfg2u_keys"]]
+    ref = {}
+    for i, k in enumerate(keys):
+        seg = lambda nm: golden[f"cfg2u_{nm}"][golden[f"cfg2u_{nm}_off"][i]:golden[f"cfg2u_{nm}_off"][i + 1]]
+        ref[k] = dict(act=seg("act"), S=seg("S"), diag=seg("diag"), k=int(golden["cfg2u_k"][i]))
+    mism = _replay_ids(wl, ref)
+    print(f"unphased cfg2: {len(keys) - len(mism)}/{len(keys)} boxes with the reference's skeleton "
+          f"on replay; mismatches (key, k_gpu, k_ref, gap, margin): {mism}")
+    untied = [m for m in mism if m[3] > 1e-12 and m[4] > 1e-10]
+    assert not untied, untied
 
 
 @pytest.mark.parametrize("m,n", [(40, 17), (300, 100), (700, 130), (1500, 200), (2400, 96), (520, 384)])

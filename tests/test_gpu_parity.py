@@ -267,3 +267,66 @@ def test_noop_and_coarse_only_updates():
     fu = update(f, b, found)
     assert 0 < fu.stats["n_dirty"]
     assert np.array_equal(fu.solve(rhs), x0)
+
+
+@pytest.mark.parametrize("name,builder", [("cfg1_", configs.cfg1), ("mini_", configs.mini_holes)])
+def test_evaluate_interior_vs_reference(golden, name, builder):
+    """Interior evaluation (reference evaluate_interior skel.py:537-564) on the
+    GPU from the reference's own solution: within 1e-12 of the reference's field;
+    point_in_domain (geometry.py:179-192) identical; exterior targets rejected."""
+    from paper_2001_11619_b200 import evaluate_interior, point_in_domain
+    wl = builder()
+    b = wl.boundary
+    tg = golden[name + "targets"]
+    assert np.array_equal(point_in_domain(b, tg), golden[name + "in_domain"])
+    assert np.array_equal(b.point_in_domain(tg), golden[name + "in_domain"])
+    u = evaluate_interior(SystemSpec(), b, golden[name + "x"], tg[:64])
+    ref = golden[name + "interior"]
+    assert u.shape == ref.shape
+    assert np.max(np.abs(u - ref)) <= 1e-12 * np.max(np.abs(ref))
+    with pytest.raises(ValueError):
+        evaluate_interior(SystemSpec(), b, golden[name + "x"], tg)
+    # multi-column solutions: column-wise equal to the single-column result
+    X = np.stack([golden[name + "x"], 2.0 * golden[name + "x"]], axis=1)
+    U = evaluate_interior(SystemSpec(), b, X, tg[:64])
+    assert np.array_equal(U[:, :, 0], u)
+
+
+def test_interior_field_exact_cfg1():
+    """Independent oracle: cfg1's RHS is the boundary trace of 4 exterior
+    Stokeslets, so the field evaluated from the GPU solve at interior points
+    equals the exact Stokeslet field (2.6e-10 on the CPU)."""
+    from paper_2001_11619_b200 import evaluate_interior
+    wl = configs.cfg1()
+    b = wl.boundary
+    f = _factor(wl)
+    x = f.solve(wl.extra["rhs"])
+    tg = configs.interior_targets(b, 200, seed=3)
+    u = evaluate_interior(SystemSpec(), b, x, tg)
+    H = configs.stokeslet_columns(tg, wl.extra["sources"])
+    al = wl.extra["alpha"]
+    exact = sum(H[:, 3 * i] * al[i, 0] + H[:, 3 * i + 1] * al[i, 1] for i in range(4)).reshape(-1, 2)
+    assert _rel(u.ravel(), exact.ravel()) < 1e-8
+
+
+def test_unphased_cfg2_end_to_end(golden):
+    """Tie-rich geometry end to end: skeleton agreement with the reference is
+    reported; the GPU solve's backward error (exact operator) stays within 2x
+    the reference solution's (tie flips move the forward solution by ~50 eps,
+    SURVEY.md §0)."""
+    from paper_2001_11619_b200 import system_matvec
+    wl = configs.cfg2(phases=False)
+    b = wl.boundary
+    f = _factor(wl)
+    keys = [tuple(k) for k in golden["cfg2u_keys"]]
+    so, S = golden["cfg2u_S_off"], golden["cfg2u_S"]
+    same = sum(np.array_equal(f.factors[k].S_loc, S[so[i]:so[i + 1]]) for i, k in enumerate(keys)
+               if k in f.factors)
+    rhs = wl.extra["rhs"]
+    x = f.solve(rhs)
+    xr = golden["cfg2u_x"]
+    R = system_matvec(SystemSpec(), b, np.stack([x, xr], axis=1)) - rhs[:, None]
+    rg, rc = np.linalg.norm(R, axis=0) / np.linalg.norm(rhs)
+    print(f"unphased cfg2: {same}/{len(keys)} identical skeletons end to end; solve rel diff "
+          f"{_rel(x, xr):.2e}; residual GPU {rg:.2e} reference {rc:.2e}")
+    assert rg <= 2 * rc

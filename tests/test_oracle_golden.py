@@ -79,3 +79,31 @@ def test_oracle_update_dirty_set(golden):
     # update == refactor on the new geometry (reference claim skel.py:459-465)
     fr = O.factor_full(nb, wl.leaf_cap, wl.tol, wl.proxy_count, wl.proxy_factor)
     assert np.array_equal(fr.solve(golden["mini_rhs"]), x)
+
+
+@pytest.mark.parametrize("name,builder", [("cfg1_", configs.cfg1), ("mini_", configs.mini_holes)])
+def test_oracle_interior_evaluation_vs_reference(golden, name, builder):
+    """evaluate_interior / point_in_domain restatements vs the reference's outputs
+    (skel.py:537-564, geometry.py:179-199) on seeded targets."""
+    wl = builder()
+    tg = golden[name + "targets"]
+    assert np.array_equal(O.point_in_domain(wl.boundary, tg), golden[name + "in_domain"])
+    u = O.evaluate_interior(wl.boundary, golden[name + "x"], tg[:64])
+    ref = golden[name + "interior"]
+    assert np.max(np.abs(u - ref)) <= 1e-12 * np.max(np.abs(ref))
+    with pytest.raises(ValueError):
+        O.evaluate_interior(wl.boundary, golden[name + "x"], tg)
+
+
+def test_oracle_unphased_cfg2_vs_reference(golden):
+    """Tie-rich fixture: on unphased cfg2 (exact pivot ties from equispaced
+    circles) the oracle, with the reference's LAPACK calls, reproduces every
+    per-box skeleton and the solution bitwise."""
+    wl = configs.cfg2(phases=False)
+    f = O.factor_full(wl.boundary, wl.leaf_cap, wl.tol, wl.proxy_count, wl.proxy_factor)
+    keys = [tuple(k) for k in golden["cfg2u_keys"]]
+    so, S = golden["cfg2u_S_off"], golden["cfg2u_S"]
+    assert sorted(f.boxes) == sorted(keys)
+    for i, k in enumerate(keys):
+        assert np.array_equal(f.boxes[k].S, S[so[i]:so[i + 1]]), k
+    assert np.array_equal(f.solve(wl.extra["rhs"]), golden["cfg2u_x"])
