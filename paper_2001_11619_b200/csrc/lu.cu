@@ -6,10 +6,14 @@
 // algorithm, panel width 64: the panel (getf2) is one CTA per matrix, the
 // U12 triangular solve is batched over (matrix, column chunk), the trailing
 // update goes to the grouped DMMA GEMM.
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <vector>
 
 #include "common.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace skb {
 
@@ -183,6 +187,130 @@ __global__ void __launch_bounds__(NT) k_getf2_panel(const LuPanel* __restrict__ 
     if (t < 2 * jb) {
       d = t < jb ? t : s_piv[t - jb];
       if ((t >= jb && d < jb) || perm[d] == d) d = -1;   // listed already / unmoved
+      else sr = perm[d];
+    }
+    D.swp[t] = d;
+    D.swp[2 * LB + t] = sr;
+  }
+}
+
+
+// dgetf2 of one LB-wide panel on a thread-block cluster (large matrices: the
+// tall panel does not fit one CTA's shared memory at LB columns).  Panel row r
+// lives in CTA r % C (row-major, odd stride LB + 1).  Per column: local |max|
+// search, cluster barrier, every CTA merges the C candidates (lowest row among
+// equal maxima, as idamax) and pulls the pivot row (the owner of the pivot
+// also pulls row c) through DSMEM, cluster barrier, then the owners write the
+// interchange and every CTA scales / updates its rows (8 threads per row).
+// Same per-row arithmetic as k_getf2_panel (l = a_rc * (1/piv),
+// a_rk -= l u_k): results do not depend on which panel kernel ran.  Writes
+// the moved-row lists for k_laswp like k_getf2_panel.  (A one-barrier variant
+// publishing candidate rows in double-buffered slots measured 10-20 % slower:
+// the column cost is instruction latency, not the second barrier.)
+__global__ void __launch_bounds__(256) k_getf2_cl(const LuPanel* __restrict__ descs) {
+  constexpr int NT = 256, NW = NT / 32, pld = LB + 1;
+  extern __shared__ __align__(16) double P[];
+  __shared__ double red_v[NW];
+  __shared__ int red_i[NW];
+  __shared__ double s_cand_v;
+  __shared__ int s_cand_i;
+  __shared__ double s_u[LB], s_rc[LB];
+  __shared__ int s_piv[LB];
+  cg::cluster_group cl = cg::this_cluster();
+  const int C = (int)cl.num_blocks(), me = (int)cl.block_rank();
+  const LuPanel D = descs[blockIdx.x / C];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int rows = (int)(D.n - D.j0), jb = (int)D.jb;
+  const int nloc = rows > me ? (rows - me + C - 1) / C : 0;     // my rows: me, me + C, ...
+  for (int e = threadIdx.x; e < nloc * jb; e += NT) {
+    const int lr = e / jb, k = e - lr * jb;
+    P[lr * pld + k] = D.A[(D.j0 + (int64_t)lr * C + me) * D.ld + D.j0 + k];
+  }
+  __syncthreads();
+  int info = -1;
+  for (int c = 0; c < jb; ++c) {
+    // local rows with global index >= c: lr >= ceil((c - me) / C)
+    const int lr0 = c > me ? (c - me + C - 1) / C : 0;
+    double bv = -1.0;
+    int bi = INT_MAX;
+    for (int lr = lr0 + threadIdx.x; lr < nloc; lr += NT) {
+      const double v = fabs(P[lr * pld + c]);
+      if (v > bv) { bv = v; bi = lr * C + me; }
+    }
+    warp_absmax(bv, bi);
+    if (lane == 0) { red_v[warp] = bv; red_i[warp] = bi; }
+    __syncthreads();
+    if (warp == 0) {
+      double gv = lane < NW ? red_v[lane] : -1.0;
+      int gi = lane < NW ? red_i[lane] : INT_MAX;
+      warp_absmax(gv, gi);
+      if (lane == 0) { s_cand_v = gv; s_cand_i = gi; }
+    }
+    cl.sync();                                             // candidates published
+    double gv = -1.0;
+    int gi = INT_MAX;
+    if (lane < C) {
+      gv = *cl.map_shared_rank(&s_cand_v, lane);
+      gi = *cl.map_shared_rank(&s_cand_i, lane);
+    }
+    warp_absmax(gv, gi);                                   // every warp: the same merge
+    const int p = gi == INT_MAX ? c : gi;
+    const bool zero = !(gv > 0.0);
+    if (me == 0 && threadIdx.x == 0) D.ipiv[D.j0 + c] = (int32_t)(D.j0 + p);
+    if (threadIdx.x == 0) s_piv[c] = p;
+    if (!zero && threadIdx.x < jb) {
+      const int k = threadIdx.x;
+      s_u[k] = cl.map_shared_rank(P, p % C)[(p / C) * pld + k];
+      if (me == p % C && p != c) s_rc[k] = cl.map_shared_rank(P, c % C)[(c / C) * pld + k];
+    }
+    cl.sync();                                             // remote rows read
+    if (zero) {
+      if (info < 0) info = (int)(D.j0 + c);
+      continue;
+    }
+    if (threadIdx.x < jb) {
+      const int k = threadIdx.x;
+      if (me == c % C) P[(c / C) * pld + k] = s_u[k];
+      if (me == p % C && p != c) P[(p / C) * pld + k] = s_rc[k];
+    }
+    __syncthreads();
+    const double rinv = 1.0 / s_u[c];
+    const int lr1 = c + 1 > me ? (c + 1 - me + C - 1) / C : 0;   // rows > c
+    for (int e = threadIdx.x; e < (nloc - lr1) * 8; e += NT) {
+      // (row, 8-column group) work items, groups of one row on consecutive threads
+      const int lr = lr1 + e / 8, g = e & 7;
+      double* pr = P + lr * pld;
+      const double l = pr[c] * rinv;
+      for (int k = c + 1 + g; k < jb; k += 8) pr[k] = pr[k] - l * s_u[k];
+    }
+    __syncthreads();
+    for (int lr = lr1 + threadIdx.x; lr < nloc; lr += NT) P[lr * pld + c] *= rinv;
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < nloc * jb; e += NT) {
+    const int lr = e / jb, k = e - lr * jb;
+    D.A[(D.j0 + (int64_t)lr * C + me) * D.ld + D.j0 + k] = P[lr * pld + k];
+  }
+  if (me == 0 && threadIdx.x == 0 && info >= 0 && *D.info < 0) *D.info = info;
+  cl.sync();
+  if (me != 0) return;
+  // moved-row lists for k_laswp (rank 0), as k_getf2_panel
+  __syncthreads();
+  int* perm = reinterpret_cast<int*>(P);
+  for (int i = threadIdx.x; i < rows; i += NT) perm[i] = i;
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int c = 0; c < jb; ++c) {
+      const int q = s_piv[c];
+      const int t = perm[c]; perm[c] = perm[q]; perm[q] = t;
+    }
+  __syncthreads();
+  if (threadIdx.x < 2 * LB) {
+    const int t = threadIdx.x;
+    int d = -1, sr = 0;
+    if (t < 2 * jb) {
+      d = t < jb ? t : s_piv[t - jb];
+      if ((t >= jb && d < jb) || perm[d] == d) d = -1;
       else sr = perm[d];
     }
     D.swp[t] = d;
@@ -507,11 +635,19 @@ int getrf_batched(int64_t nbox, const SkbMat* a, const int64_t* ipiv, int32_t* i
   // panel width: a function of each matrix's own order only (so results do not
   // depend on the batch composition): as wide as shared memory allows (<= 64)
   // (rows are stored with an odd stride PB + 1)
+  // Panels taller than one CTA's shared memory at LB columns run on a
+  // thread-block cluster (k_getf2_cl, identical per-row arithmetic); its size
+  // is a function of n only.
   constexpr size_t kPanelSmem = 224 * 1024;
+  auto one_cta = [&](int64_t n) { return (size_t)n * (LB / 2 + 1) * sizeof(double) <= kPanelSmem; };
   auto pbw = [&](int64_t n) {
-    int64_t PB = LB;
-    while (PB > 8 && (size_t)n * (PB + 1) * sizeof(double) > kPanelSmem) PB /= 2;
-    return PB;
+    if (!one_cta(n)) return (int64_t)LB;
+    return (size_t)n * (LB + 1) * sizeof(double) <= kPanelSmem ? (int64_t)LB : (int64_t)LB / 2;
+  };
+  auto csize = [&](int64_t n) {       // <= 100 KB of panel rows per CTA
+    int64_t C = 2;
+    while (C < 16 && (size_t)((n + C - 1) / C) * (LB + 1) * sizeof(double) > 100 * 1024) C *= 2;
+    return C;
   };
   int64_t rounds = 0;
   for (int64_t b = 0; b < nbox; ++b)
@@ -519,6 +655,8 @@ int getrf_batched(int64_t nbox, const SkbMat* a, const int64_t* ipiv, int32_t* i
   int32_t* swp = nullptr;   // moved-row lists of one round's panels (k_laswp)
   if (rounds > 0) {
     SKB_RET(smem_optin((const void*)k_getf2_panel<SKB_PANEL_NT>));
+    SKB_RET(smem_optin((const void*)k_getf2_cl));
+    SKB_RET(cudaFuncSetAttribute((const void*)k_getf2_cl, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
     int64_t nbig = 0;
     for (int64_t b = 0; b < nbox; ++b) nbig += a[b].rows > kSmallLU;
     SKB_RET(cudaMallocAsync(reinterpret_cast<void**>(&swp), sizeof(int32_t) * 4 * LB * nbig, s));
@@ -536,15 +674,32 @@ int getrf_batched(int64_t nbox, const SkbMat* a, const int64_t* ipiv, int32_t* i
     pd.clear(); td.clear(); gd.clear(); tdr.clear(); gdr.clear();
     size_t smem = 0;
     int64_t maxcol = 0;
-    for (int64_t b = 0; b < nbox; ++b) {
+    // panels: one-CTA ones first, then cluster ones grouped by cluster size
+    std::vector<int64_t> order;
+    for (int pass = 0; pass < 5; ++pass)
+      for (int64_t b = 0; b < nbox; ++b) {
+        const int64_t n = a[b].rows;
+        if (n <= kSmallLU || rd_ * pbw(n) >= n) continue;
+        const int grp = one_cta(n) ? 0 : (int)__builtin_ctzll((unsigned long long)csize(n));  // 1..4
+        if (grp == pass) order.push_back(b);
+      }
+    int64_t ngrp[5] = {0, 0, 0, 0, 0};
+    size_t csm[5] = {0, 0, 0, 0, 0};
+    for (int64_t b : order) {
       const int64_t n = a[b].rows;
-      if (n <= kSmallLU) continue;
       const int64_t PB = pbw(n);
       const int64_t j0 = rd_ * PB;
-      if (j0 >= n) continue;
       const int64_t jb = std::min<int64_t>(PB, n - j0), n2 = n - j0 - jb;
-      smem = std::max(smem, sizeof(double) * (size_t)(n - j0) * (size_t)(PB + 1));
-      smem = std::max(smem, sizeof(int) * (size_t)(n - j0));   // composed permutation
+      const int grp = one_cta(n) ? 0 : (int)__builtin_ctzll((unsigned long long)csize(n));
+      ngrp[grp]++;
+      if (grp == 0) {
+        smem = std::max(smem, sizeof(double) * (size_t)(n - j0) * (size_t)(PB + 1));
+        smem = std::max(smem, sizeof(int) * (size_t)(n - j0));   // composed permutation
+      } else {
+        const int64_t C = csize(n);
+        csm[grp] = std::max(csm[grp], sizeof(double) * (size_t)((n - j0 + C - 1) / C) * (LB + 1));
+        csm[grp] = std::max(csm[grp], sizeof(int) * (size_t)(n - j0));
+      }
       double* A = a[b].ptr;
       const int64_t ld = a[b].ld;
       pd.push_back(LuPanel{A, n, ld, j0, jb, reinterpret_cast<int32_t*>(ipiv[b]), info_out + b,
@@ -574,8 +729,27 @@ int getrf_batched(int64_t nbox, const SkbMat* a, const int64_t* ipiv, int32_t* i
     if ((rc = upload(pd.data(), (int64_t)pd.size(), s, &dp))) return rc;
     {
       ProfScope ps(F_GETRF, s);
-      k_getf2_panel<SKB_PANEL_NT><<<(unsigned)pd.size(), SKB_PANEL_NT, smem, s>>>(dp);
+      if (ngrp[0]) k_getf2_panel<SKB_PANEL_NT><<<(unsigned)ngrp[0], SKB_PANEL_NT, smem, s>>>(dp);
       SKB_LAUNCH_CHECK();
+      int64_t off = ngrp[0];
+      for (int g = 1; g < 5; ++g) {
+        if (!ngrp[g]) continue;
+        const int C = 1 << g;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(ngrp[g] * C));
+        cfg.blockDim = dim3(256);
+        cfg.dynamicSmemBytes = csm[g];
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = C;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        SKB_RET(cudaLaunchKernelEx(&cfg, k_getf2_cl, (const LuPanel*)(dp + off)));
+        off += ngrp[g];
+      }
       // the interchanges touch the columns the side stream is still updating
       if (pending_rest) { SKB_RET((cudaError_t)(-join_n(s, 1))); pending_rest = false; }
       if (maxcol > 0) k_laswp<<<dim3((unsigned)((maxcol + 31) / 32), (unsigned)pd.size()), 256, 0, s>>>(dp);

@@ -406,22 +406,6 @@ def _gemm(rows):
     call("skb_gemm_grouped", g, n, _stream())
 
 
-def _gemm_tn_splitk(A, B, M, N, K, lda, ldb, C, alpha, D, chunk=4096):
-    """D = C + alpha * A^T B with A: (K x M), B: (K x N) row-major and K large:
-    split K into chunks (one grouped GEMM), then a fixed-order sum of partials."""
-    nch = max(1, (K + chunk - 1) // chunk)
-    parts = torch.empty(max(nch * M * N, 1), dtype=torch.float64, device=_dev())
-    k0 = np.arange(nch) * chunk
-    kk = np.minimum(chunk, K - k0)
-    pa = _addr(parts)
-    _gemm([dict(A=(A + 8 * k0 * lda).astype(np.uint64), B=(B + 8 * k0 * ldb).astype(np.uint64),
-                D=(pa + 8 * np.arange(nch) * M * N).astype(np.uint64), m=np.full(nch, M),
-                n=np.full(nch, N), k=kk, lda=np.full(nch, lda), ldb=np.full(nch, ldb),
-                ldd=np.full(nch, N), alpha=np.ones(nch), beta=np.zeros(nch), transA=np.ones(nch))])
-    call("skb_sum_partials", M * N, nch, parts, M * N, C, alpha, D, _stream())
-    return parts
-
-
 def _mats(ptrs, rows, cols, ld):
     m = np.zeros(len(ptrs), MAT_DT)
     m["ptr"], m["rows"], m["cols"], m["ld"] = ptrs, rows, cols, ld
@@ -1496,10 +1480,14 @@ class _Engine:
             self.lib.skb_engine_set_update(self.h, todo.ctypes.data, coff.ctypes.data,
                                            cskel.ctypes.data)
             self.lib.skb_engine_go(self.h)
-        # Run-ahead of the engine over the enqueued Schur stages: unbounded by
-        # default (SKB_ENGINE_LEAD=n >= 0 limits it to n levels).  Levels
-        # without boxes to compress count as acknowledged (engine.cu).
-        lead = int(os.environ.get("SKB_ENGINE_LEAD", "-1"))
+        # Run-ahead of the engine over the enqueued Schur stages: the engine
+        # starts level L once level L+1's Schur stage is enqueued (lead 0).
+        # Deeper run-ahead (SKB_ENGINE_LEAD=n, -1 unbounded) is ~5 % faster in
+        # the median on cfg3 but lets the compression chain's cluster kernels
+        # stall behind two levels of Schur / sweep work: 0.3-1 s steps in ~1 of
+        # 40 factorizations (scripts/outliers.py).  Levels without boxes to
+        # compress count as acknowledged (engine.cu).
+        lead = int(os.environ.get("SKB_ENGINE_LEAD", "0"))
         if lead >= 0:
             self.lib.skb_engine_set_lead(self.h, lead)
         self.sizes = np.zeros(8, np.int64)

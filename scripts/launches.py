@@ -7,11 +7,12 @@ rows = list(csv.reader(open(sys.argv[1])))
 hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
 h = rows[hi]
 ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+mi = h.index("Metric Name") if "Metric Name" in h else None
 agg = collections.defaultdict(lambda: [0, 0.0, 0.0])
 tot = 0.0
 seq = []
 for r in rows[hi + 1:]:
-    if len(r) <= vi:
+    if len(r) <= vi or (mi is not None and r[mi] != "gpu__time_duration.sum"):
         continue
     v = float(r[vi].replace(",", ""))
     v *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(r[ui], 1.0)

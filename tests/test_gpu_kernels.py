@@ -319,3 +319,34 @@ def test_geqrf_batched_R(m, n):
         Rref = sla.qr(a, mode="r")[0][:n]
         assert np.allclose(np.abs(np.diag(R)), np.abs(np.diag(Rref)), rtol=1e-9, atol=1e-14 * np.abs(Rref).max())
         assert np.allclose(np.abs(R), np.abs(Rref), rtol=1e-9, atol=1e-12 * np.abs(Rref).max())
+
+
+def test_gemm_bits_independent_of_tile_and_n():
+    """Each output element is one thread's fixed-K-order DMMA chain: the 64x64
+    and 128x128 tile variants and any column subset give identical bits (the
+    update path's incremental sweep relies on it)."""
+    import subprocess, sys, os
+    code = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, %r)
+from paper_2001_11619_b200 import skel
+rng = np.random.default_rng(1)
+m, n, k = 300, 200, 250
+A, B, C = (torch.from_numpy(rng.standard_normal(s)).cuda() for s in ((m, k), (k, n), (m, n)))
+outs = []
+for cols in (n, 37):
+    D = torch.empty((m, n), dtype=torch.float64, device="cuda")
+    skel._gemm([dict(A=np.array([A.data_ptr()], np.uint64), B=np.array([B.data_ptr()], np.uint64),
+                     C=np.array([C.data_ptr()], np.uint64), D=np.array([D.data_ptr()], np.uint64),
+                     m=[m], n=[cols], k=[k], lda=[k], ldb=[n], ldc=[n], ldd=[n], alpha=[-1.0], beta=[1.0])])
+    outs.append(D[:, :37].cpu().numpy())
+np.save(sys.argv[1], np.stack(outs))
+""" % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = []
+    for tile in ("64", "128"):
+        out = f"/tmp/skb_gemm_{tile}.npy"
+        env = dict(os.environ, SKB_GEMM_TILE=tile)
+        subprocess.run([sys.executable, "-c", code, out], check=True, env=env)
+        res.append(np.load(out))
+    assert np.array_equal(res[0][0], res[0][1])       # n = 200 vs n = 37
+    assert np.array_equal(res[0], res[1])             # 64x64 vs 128x128 tiles
