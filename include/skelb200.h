@@ -280,10 +280,46 @@ int skb_level_schur(int64_t nbox, const int64_t* nB, const int64_t* k,
 int skb_level_aug(int64_t nbox, const int64_t* k, const int64_t* r, int64_t q,
                   const int64_t* cols_off, const int64_t* cols, const int64_t* sd_off,
                   const int64_t* sd, const int64_t* rd_off, const int64_t* rd,
-                  const int64_t* c_off, const int64_t* c, const uint64_t* T,
-                  const uint64_t* LU, const uint64_t* Xsr, const uint64_t* Xrsdiv,
-                  const uint64_t* ipiv, double* UH, double* PsiV, double* UH_div,
-                  double* schur, void* stream);
+                  const int64_t* c_off, const int64_t* c, const uint64_t* T, const uint64_t* LU,
+                  const uint64_t* Xsr, const uint64_t* Xrsdiv, const uint64_t* ipiv, double* UH,
+                  double* PsiV, double* UH_div, double* schur, double* stash, const int64_t* st_us,
+                  const int64_t* st_ps, const int64_t* st_sp, int32_t acc, void* stream);
+/* Accumulate one level's stored Schur parts (stash + st_sp) into schur, in
+ * skb_level_aug's order (skel.py:396).                                       */
+int skb_level_schur_acc(int64_t nbox, const int64_t* cols_off, const int64_t* cols, int64_t q,
+                        const double* stash, const int64_t* st_sp, double* schur, void* stream);
+/* update(): incremental _finish_top.  The sweep of a
+ * level restricted to the changed augmentation columns qc (host list) for
+ * boxes whose factors were reused; updates UH / UH_div rows, the stored
+ * outgoing UH_S and Schur parts at those columns.                            */
+int skb_level_aug_narrow(int64_t nbox, const int64_t* k, const int64_t* r, int64_t q, int64_t nqc,
+                         const int64_t* qc, const int64_t* cols_off, const int64_t* sd_off,
+                         const int64_t* sd, const int64_t* rd_off, const int64_t* rd,
+                         const int64_t* c_off, const int64_t* c, const uint64_t* T,
+                         const uint64_t* LU, const uint64_t* Xsr, const uint64_t* ipiv, double* UH,
+                         const double* PsiV, double* UH_div, double* stash, const int64_t* st_us,
+                         const int64_t* st_sp, void* stream);
+/* Stored outgoing skeleton rows of reused boxes (us: k x q, ps: k x nc per
+ * box, device addresses) back into UH (columns with qmask 0) and PsiV.       */
+int skb_restore_rows(int64_t nbox, const int64_t* sd_off, const int64_t* sd, int64_t max_k,
+                     const int64_t* c_off, const int64_t* c, const uint64_t* us, const uint64_t* ps,
+                     const uint8_t* qmask_dev, int64_t q, double* UH, double* PsiV, void* stream);
+/* One level of update()'s incremental sweep (reused boxes: copy + narrow +
+ * restore under a dirty parent; dirty boxes: full; then accumulation), all
+ * descriptor arrays on the host.                                             */
+int skb_level_aug_update(int64_t nbox, const int64_t* k, const int64_t* r, int64_t q,
+                         const int64_t* cols_off, const int64_t* cols, const int64_t* sd_off,
+                         const int64_t* sd, const int64_t* rd_off, const int64_t* rd,
+                         const uint8_t* dirty, const uint8_t* parent_dirty, const uint64_t* T,
+                         const uint64_t* LU, const uint64_t* Xsr, const uint64_t* Xrsdiv,
+                         const uint64_t* ipiv, const uint64_t* old_us, const uint64_t* old_ps,
+                         const uint64_t* old_sp, int64_t nqc, const int64_t* qc,
+                         const uint8_t* qmask_dev, double* UH, double* PsiV, double* UH_div,
+                         double* schur, double* stash, const int64_t* st_us, const int64_t* st_ps,
+                         const int64_t* st_sp, void* stream);
+/* dst rows idx (n) and columns qc (nqc) <- src, both nrows x ncols row-major. */
+int skb_copy_rows_cols(int64_t n, const int64_t* idx_dev, int64_t nqc, const int64_t* qc_dev,
+                       int64_t nrows, int64_t ncols, const double* src, double* dst, void* stream);
 
 /* ---- native level engine (csrc/engine.cu) ----------------------------------
  * The compression chain of factor() (skel.py:443-449 over compress_box

@@ -63,8 +63,12 @@ SIGNATURES = {
     "skb_point_in_domain": [_vp, _vp, _i64, _vp, _i64, _vp, _vp],
     "skb_level_schur": [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                         _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
-    "skb_level_aug": [_i64, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
-                      _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+    "skb_level_aug": [_i64, _vp, _vp, _i64] + [_vp] * 17 + [_vp, _vp, _vp, _vp, _i32, _vp],
+    "skb_level_schur_acc": [_i64, _vp, _vp, _i64, _vp, _vp, _vp, _vp],
+    "skb_level_aug_narrow": [_i64, _vp, _vp, _i64, _i64] + [_vp] * 16 + [_vp, _vp, _vp],
+    "skb_restore_rows": [_i64, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp],
+    "skb_level_aug_update": [_i64, _vp, _vp, _i64] + [_vp] * 16 + [_i64] + [_vp] * 11,
+    "skb_copy_rows_cols": [_i64, _vp, _i64, _vp, _i64, _i64, _vp, _vp, _vp],
     "skb_engine_start": [_vp, _i64, _vp, _f64, _vp, _i64, _vp, _i64, _f64, _vp, _i64, _i64, _vp],
     "skb_engine_wait": [_i64, _i64, _vp, _vp],
     "skb_engine_stream_wait": [_i64, _i64, _vp],

@@ -382,7 +382,8 @@ def _upload(**arrays):
     out = {}
     for k, a, o in items:
         tdt = {np.dtype(np.int64): torch.int64, np.dtype(np.float64): torch.float64,
-               np.dtype(np.int32): torch.int32, np.dtype(np.uint64): torch.int64}[a.dtype]
+               np.dtype(np.int32): torch.int32, np.dtype(np.uint64): torch.int64,
+               np.dtype(np.uint8): torch.uint8}[a.dtype]
         out[k] = d[o:o + a.nbytes].view(tdt)
     out["_keep"] = (None, d)
     return out
@@ -1078,9 +1079,13 @@ class Factorization:
             call("skb_scatter_rows", 1, ptr(up["ro"]), ptr(rd["r"]), None, None, nr,
                  _addr(top_rhs), ptr(up["o"]), ptr(up["ld"]), ptr(x), nr, 0, 1.0, ns, nr, s)
             x[nd:].copy_(top_rhs[ns:])
-            # x[:nd] -= UH_div lam (UH_div rows of root DOFs are exactly zero): one
-            # plain (2N x q) x (q x nrhs) product, the largest GEMM of the solve -> cuBLAS
-            x[:nd].addmm_(self.UH_div, top_rhs[ns:], alpha=-1.0)
+            # x[:nd] -= UH_div lam (UH_div rows of root DOFs are exactly zero; skel.py:188):
+            # the solve's largest product, (2N x q)(q x nrhs), on the DMMA GEMM
+            _gemm([dict(A=np.array([_addr(self.UH_div)], np.uint64),
+                        B=np.array([_addr(top_rhs) + 8 * ns * nr], np.uint64),
+                        C=np.array([_addr(x)], np.uint64), D=np.array([_addr(x)], np.uint64),
+                        m=[nd], n=[nr], k=[q], lda=[q], ldb=[nr], ldc=[nr], ldd=[nr],
+                        alpha=[-1.0], beta=[1.0])])
             keep += [top_rhs]
         else:
             top_rhs = torch.empty((ns, nr), dtype=torch.float64, device=dev)
@@ -1189,7 +1194,11 @@ class Factorization:
         self._solve_graphed(x)
         if is_t:
             return x.reshape(-1) if vec else x
-        out = x.cpu().numpy()
+        # device -> pinned host (the returned array views the pinned block)
+        hp = torch.empty(x.shape, dtype=torch.float64, pin_memory=True)
+        hp.copy_(x, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        out = hp.numpy()
         return out.reshape(-1) if vec else out
 
     def apply(self, x, workers: int = 1):
@@ -1326,7 +1335,9 @@ def _hole_columns(t: Tree, b, idx, pairs=None):
 class _AugPipe:
     """U sweep on H / V^T sweep on Psi (reference _finish_top, skel.py:379-396),
     run per level on a side stream as soon as the level's factors are final, so
-    it overlaps the factorisation of the levels above."""
+    it overlaps the factorisation of the levels above.  Every box's outgoing
+    skeleton rows and Schur part are kept per level (LevelFactors.stash) for
+    the incremental sweep of a later update()."""
 
     def __init__(self, ctx: _Ctx):
         b = ctx.b
@@ -1345,16 +1356,20 @@ class _AugPipe:
         self.stream = _aug_stream()
         self.src = ctx.sstream
 
-    def submit(self, L: "LevelFactors"):
-        if not self.q:
-            return
+    def _wait_inputs(self):
         # the level's Schur work (level stream) and its descriptor uploads /
         # H, Psi assembly (current stream) must both precede the sweep
         for st in (self.src, torch.cuda.current_stream()):
             ev = torch.cuda.Event()
             ev.record(st)
             self.stream.wait_event(ev)
+
+    def submit(self, L: "LevelFactors"):
+        if not self.q:
+            return
+        self._wait_inputs()
         with torch.cuda.stream(self.stream):
+            _stash_alloc(L, self.q)
             _aug_level(L, self.UH, self.PsiV, self.UH_div, self.schur, self.q)
 
     def join(self):
@@ -1362,6 +1377,131 @@ class _AugPipe:
             ev = torch.cuda.Event()
             ev.record(self.stream)
             torch.cuda.current_stream().wait_event(ev)
+
+
+_INC_SWEEP = os.environ.get("SKB_INC_SWEEP", "1") != "0"
+
+
+def _make_pipe(ctx: "_Ctx"):
+    upd = getattr(ctx, "upd_old", None) if _INC_SWEEP else None
+    return _AugPipeUpdate(ctx, *upd) if upd is not None else _AugPipe(ctx)
+
+
+def _stash_alloc(L: "LevelFactors", q: int):
+    """Per-box storage of a level's sweep results: outgoing UH_S (k x q),
+    PsiV_S (k x nc), Schur part (nc x q); element offsets per box."""
+    k, nc = L.k, L.ncols
+    us = k * q
+    ps = k * nc
+    sp = nc * q
+    st_us = np.zeros(len(k), np.int64)
+    np.cumsum(us[:-1], out=st_us[1:])
+    base_ps = int(us.sum())
+    st_ps = np.full(len(k), base_ps, np.int64)
+    np.cumsum(ps[:-1], out=st_ps[1:])
+    st_ps[1:] += base_ps
+    base_sp = base_ps + int(ps.sum())
+    st_sp = np.full(len(k), base_sp, np.int64)
+    np.cumsum(sp[:-1], out=st_sp[1:])
+    st_sp[1:] += base_sp
+    L.stash = torch.empty(max(base_sp + int(sp.sum()), 1), dtype=torch.float64, device=_dev())
+    L.st_us, L.st_ps, L.st_sp = st_us, st_ps, st_sp
+
+
+class _AugPipeUpdate(_AugPipe):
+    """Incremental _finish_top for update() (the
+    reference recomputes it all, skel.py:510).  The sweep is linear in (H, Psi)
+    and a box's step touches only its own active rows, so:
+
+    * boxes whose factors were reused (clean) redo only the columns of the
+      moved holes (their H columns change everywhere) -- skb_level_aug_narrow;
+      their other columns, final UH / PsiV / UH_div rows and Schur parts are
+      the previous factorization's (copied);
+    * recompressed (dirty) boxes redo every column -- skb_level_aug -- starting
+      from fresh H / Psi rows for dirty leaves and, above a clean child, from
+      that child's stored outgoing skeleton rows (skb_restore_rows);
+    * the corner's Schur block is re-accumulated from the stored per-box parts
+      level by level in the refactor's order.
+
+    Every kernel gives the same bits restricted to a column subset as on all
+    columns (fixed-K-order DMMA GEMM, per-column triangular solves), so the
+    result equals the full sweep bitwise (tests/test_gpu_parity.py)."""
+
+    def __init__(self, ctx: _Ctx, old: "Factorization", dmask):
+        b = ctx.b
+        self.q = 3 * b.n_holes if ctx.spec.augmented(b) else 0
+        if not self.q or old.UH is None:
+            if self.q:
+                _AugPipe.__init__(self, ctx)
+            self.inc = False
+            return
+        self.inc = True
+        dev = _dev()
+        nd, q = 2 * b.n_nodes, self.q
+        t = ctx.t
+        s = _stream()
+        self.UH = old.UH.clone()
+        self.PsiV = old.PsiV.clone()
+        self.UH_div = old.UH_div.clone()
+        self.schur = torch.zeros((q, q), dtype=torch.float64, device=dev)
+        H0 = torch.empty((nd, q), dtype=torch.float64, device=dev)
+        P0 = torch.empty((nd, q), dtype=torch.float64, device=dev)
+        self._hc = torch.from_numpy(np.ascontiguousarray(b.hole_centers, np.float64)).to(dev)
+        call("skb_assemble_aug", ptr(ctx.g.pos), ptr(ctx.g.w), b.n_nodes, ptr(self._hc), b.n_holes,
+             np.ascontiguousarray(b.offsets, np.int64), ptr(H0), ptr(P0), s)
+        # columns of holes whose centre moved; rows of every dirty leaf
+        moved = np.flatnonzero(np.any(old.boundary.hole_centers != b.hole_centers, axis=1))
+        self.qc = (3 * moved[:, None] + np.arange(3)[None, :]).ravel().astype(np.int64)
+        qmask = np.zeros(q, np.uint8)
+        qmask[self.qc] = 1
+        leaves = np.flatnonzero(t.is_leaf & dmask)
+        nodes = [t.nodes_of(i) for i in leaves]
+        nodes = np.concatenate(nodes) if nodes else np.zeros(0, np.int64)
+        rows = np.sort((2 * nodes[:, None] + np.arange(2)[None, :]).ravel()).astype(np.int64)
+        up = _upload(rows=rows if len(rows) else np.zeros(1, np.int64),
+                     qc=self.qc if len(self.qc) else np.zeros(1, np.int64), qmask=qmask)
+        for src, dst in ((H0, self.UH), (P0, self.PsiV)):
+            call("skb_copy_rows_cols", len(rows), up["rows"], len(self.qc), up["qc"], nd, q, src, dst, s)
+        self._keep = (up, H0, P0)
+        self.qmask_d = up["qmask"]
+        self.dmask = dmask
+        self.tree = t
+        self.stream = _aug_stream()
+        self.src = ctx.sstream
+
+    def submit(self, L: "LevelFactors"):
+        if not self.q:
+            return
+        if not self.inc:
+            return _AugPipe.submit(self, L)
+        self._wait_inputs()
+        with torch.cuda.stream(self.stream):
+            self._submit(L)
+
+    def _submit(self, L):
+        q = self.q
+        _stash_alloc(L, q)
+        B = len(L.idx)
+        dirty = self.dmask[L.idx]
+        par = self.tree.parent[L.idx]
+        pdirty = ((par >= 0) & self.dmask[np.maximum(par, 0)]).astype(np.uint8)
+        old_us = np.zeros(B, np.uint64)
+        old_ps = np.zeros(B, np.uint64)
+        old_sp = np.zeros(B, np.uint64)
+        cl = np.flatnonzero(~dirty)
+        if len(cl):
+            Lo, pos = L.batch.clean_old
+            base = _addr(Lo.stash)
+            old_us[cl] = base + 8 * Lo.st_us[pos]
+            old_ps[cl] = base + 8 * Lo.st_ps[pos]
+            old_sp[cl] = base + 8 * Lo.st_sp[pos]
+        z = np.zeros(1, np.int64)
+        call("skb_level_aug_update", B, L.k, L.r, q, L.cols_off, L.cols if len(L.cols) else z,
+             L.sd_off, L.sd if len(L.sd) else z, L.rd_off, L.rd if len(L.rd) else z,
+             dirty.astype(np.uint8), pdirty, L.P["T"], L.P["LU"], L.P["Xsr"], L.P["Xrsdiv"], L.ipiv,
+             old_us, old_ps, old_sp, len(self.qc), self.qc if len(self.qc) else z, ptr(self.qmask_d),
+             ptr(self.UH), ptr(self.PsiV), ptr(self.UH_div), ptr(self.schur), ptr(L.stash), L.st_us,
+             L.st_ps, L.st_sp, _stream())
 
 
 def _finish_top(ctx: _Ctx, levels, store, pipe: "_AugPipe"):
@@ -1389,6 +1529,10 @@ def _finish_top(ctx: _Ctx, levels, store, pipe: "_AugPipe"):
         pipe.join()                                  # sweeps were issued level by level
         _Prof.tick("d_aug_sweep")
         UH, PsiV, UH_div, schur = pipe.UH, pipe.PsiV, pipe.UH_div, pipe.schur
+        if getattr(pipe, "inc", False) and ns:
+            # UH_div rows of root DOFs are never written by the sweep (zero in a
+            # refactor); the incremental sweep started from the previous UH_div
+            call("skb_fill_rows", ns, ptr(up["a"]), ptr(UH_div), q, None, q, 0.0, s)
         n = ns + q
         top = torch.empty((n, n), dtype=torch.float64, device=dev)
         call("skb_copy2d_batched", 1, _mats([_addr(top)], [ns], [ns], [n]),
@@ -1428,7 +1572,8 @@ def _aug_level(L: LevelFactors, UH, PsiV, UH_div, schur, q):
     call("skb_level_aug", len(L.k), L.k, L.r, q, L.cols_off,
          L.cols if len(L.cols) else np.zeros(1, np.int64), ptr(d["sd_off"]), ptr(d["sd"]),
          ptr(d["rd_off"]), ptr(d["rd"]), ptr(d["c_off"]), ptr(d["c"]), L.P["T"], L.P["LU"],
-         L.P["Xsr"], L.P["Xrsdiv"], L.ipiv, ptr(UH), ptr(PsiV), ptr(UH_div), ptr(schur), _stream())
+         L.P["Xsr"], L.P["Xrsdiv"], L.ipiv, ptr(UH), ptr(PsiV), ptr(UH_div), ptr(schur),
+         ptr(L.stash), L.st_us, L.st_ps, L.st_sp, 1, _stream())
 
 
 # The native level engine (csrc/engine.cu) drives factor() unless SKB_ENGINE=0
@@ -1487,7 +1632,10 @@ class _Engine:
         # stall behind two levels of Schur / sweep work: 0.3-1 s steps in ~1 of
         # 40 factorizations (scripts/outliers.py).  Levels without boxes to
         # compress count as acknowledged (engine.cu).
-        lead = int(os.environ.get("SKB_ENGINE_LEAD", "0"))
+        # Updates recompress a few boxes per level: no heavy Schur work to
+        # starve behind, so they run ahead unbounded (the Python level loop is
+        # their critical path).
+        lead = int(os.environ.get("SKB_ENGINE_LEAD", "0" if update is None else "-1"))
         if lead >= 0:
             self.lib.skb_engine_set_lead(self.h, lead)
         self.sizes = np.zeros(8, np.int64)
@@ -1622,7 +1770,7 @@ def _run_levels_engine_update(ctx: _Ctx, old: dict, dmask):
 def _engine_loop(ctx, eng, store, reuse=None, dirty=None):
         t = ctx.t
         pairs = t.hole_pairs(np.asarray(ctx.b.offsets, np.int64)) if ctx.b.n_holes else None
-        pipe = _AugPipe(ctx)
+        pipe = _make_pipe(ctx)
         ctx.pipe = pipe
         levels = []
         prev = None
@@ -1721,7 +1869,7 @@ def _run_levels(ctx: _Ctx, reuse=None, dirty=None):
     p_cur = pre(lev) if lev >= 1 else None
     cur = go(p_cur) if lev >= 1 else None            # first compression in flight first
     pairs = t.hole_pairs(np.asarray(ctx.b.offsets, np.int64)) if ctx.b.n_holes else None
-    pipe = _AugPipe(ctx)
+    pipe = _make_pipe(ctx)
     ctx.pipe = pipe
     p_nxt = pre(lev - 1) if lev > 1 else None
     while lev >= 1:
@@ -1798,6 +1946,7 @@ def _merge_level(ctx, idx, store, todo, bt_new, old_levels):
         if not np.array_equal(a_new, a_old):
             raise RuntimeError("clean box changed its active set")
         bt.take(clean, ob, pos)
+        bt.clean_old = (L, pos)                # the incremental sweep copies their stored rows
     return bt
 
 
@@ -1866,6 +2015,7 @@ def update(fct: Factorization, b_new, report, workers: int = 1) -> Factorization
         raise NotImplementedError("only DOF-preserving edits (hole moves) are supported")
     old = {L.lev: L for L in fct.levels}
     ctx = _Ctx(fct.spec, b_new, t_new, fct.tol, fct.proxy_count, fct.proxy_factor)
+    ctx.upd_old = (fct, dmask)
     torch.cuda.current_stream().synchronize()
     with torch.cuda.stream(_compress_stream()):
         levels = None
@@ -1875,6 +2025,7 @@ def update(fct: Factorization, b_new, report, workers: int = 1) -> Factorization
             except _EngineAbort:
                 _drain(ctx)
                 ctx = _Ctx(fct.spec, b_new, t_new, fct.tol, fct.proxy_count, fct.proxy_factor)
+                ctx.upd_old = (fct, dmask)
                 levels = None
         if levels is None:
             levels, store, n_recomp = _run_levels(ctx, reuse=old, dirty=dmask)

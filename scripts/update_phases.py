@@ -15,6 +15,8 @@ for i, (h, d, nb, rp) in enumerate(seq):
     torch.cuda.synchronize()
     if i == 2:
         skel._HostTimer.acc.clear()
+        from paper_2001_11619_b200 import _lib
+        _lib.CALL_TIMES = {}
     t0 = time.perf_counter()
     f = update(f, nb, rp)
     torch.cuda.synchronize()
@@ -24,3 +26,8 @@ n = len(ts)
 print("update ms median %.2f" % np.median(ts))
 for k, v in sorted(skel._HostTimer.acc.items(), key=lambda x: -x[1]):
     print("  %-14s %8.3f ms/update" % (k, v * 1e3 / n))
+
+from paper_2001_11619_b200 import _lib
+print("native entry points (host ms/update, calls/update):")
+for k, (c, t) in sorted(_lib.CALL_TIMES.items(), key=lambda x: -x[1][1])[:14]:
+    print("  %-26s %7.3f ms %6.1f" % (k, t * 1e3 / n, c / n))
