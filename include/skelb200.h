@@ -116,6 +116,21 @@ int skb_assemble_self(const double* pos, const double* nrm, const double* w, con
                       double* E, const int64_t* E_off, const int64_t* E_ld,
                       int64_t max_n, void* stream);
 
+/* Laplace-Neumann variants (SystemSpec(LAPLACE): one DOF per node): ID stack
+ * of rows 2 nF + 2 P + 2 (kernels.py:161-168, 322-325, 347-352, 368-370;
+ * pnrm unused) and self blocks of the adjoint double layer with the +1
+ * completion and the kappa / (4 pi) same-node limit (kernels.py:119-125).    */
+int skb_assemble_stack_lap(const double* pos, const double* nrm, const double* w, int64_t nbox,
+                           const int64_t* act_off, const int64_t* act, const int64_t* far_off,
+                           const int64_t* far, const double* ppts, const double* pnrm,
+                           const double* pw, int32_t P, const int64_t* stack_off, double* stack,
+                           int64_t max_cols, int64_t max_items, void* stream);
+int skb_assemble_self_lap(const double* pos, const double* nrm, const double* w,
+                          const double* kappa, int64_t nbox, const int64_t* act_off,
+                          const int64_t* act, const int64_t* perm_off, const int32_t* perm,
+                          const int64_t* child_off, const int64_t* child_xss, double* E,
+                          const int64_t* E_off, const int64_t* E_ld, int64_t max_n, void* stream);
+
 /* (d) Stokeslet/rotlet columns H (nd x 3p) and weighted rigid-body functionals
  * Psi (nd x 3p) -- kernels.stokeslet_rotlet_columns (kernels.py:201-223) and
  * build_augmentation (kernels.py:226-246).  curve_off: (p+2,) node offsets.  */
@@ -236,6 +251,14 @@ int skb_system_matvec(const double* pos, const double* nrm, const double* w, con
 /* Field at interior targets from a solve() output, out (2m x nrhs) row-major:
  * u = D mu + H lam (reference evaluate_interior skel.py:537-564,
  * eval_forward_block kernels.py:171-198).  x: (2N + 3p) x nrhs row-major.    */
+/* Laplace-Neumann exact operator y = (-1/2 I + K' + 1 w^T) mu (kernels.py:
+ * 119-125 summed over all nodes) and interior field u = -S mu (kernels.py:
+ * 193-194); x: N x nrhs, y: N x nrhs, out: m x nrhs (row-major).            */
+int skb_system_matvec_lap(const double* pos, const double* nrm, const double* w,
+                          const double* kappa, int64_t n_nodes, const double* x, int64_t nrhs,
+                          double* y, void* stream);
+int skb_eval_interior_lap(const double* pos, const double* w, int64_t n_nodes, const double* x,
+                          int64_t nrhs, const double* targets, int64_t m, double* out, void* stream);
 int skb_eval_interior(const double* pos, const double* nrm, const double* w, int64_t n_nodes,
                       const double* hole_centers, int64_t n_holes, const double* x, int64_t nrhs,
                       const double* targets, int64_t m, double* out, void* stream);
@@ -269,7 +292,7 @@ int skb_level_schur(int64_t nbox, const int64_t* nB, const int64_t* k,
                     const uint64_t* child_xss, const uint64_t* T, const uint64_t* Xrr,
                     const uint64_t* LU, const uint64_t* Xsr, const uint64_t* Xrsdiv,
                     const uint64_t* Xss, const uint64_t* ipiv, int32_t* info_dev,
-                    double* ratio_dev, void* stream);
+                    double* ratio_dev, int32_t pde, void* stream);   /* pde 0 Stokes, 1 Laplace */
 
 /* (d) augmentation sweep of one level (_finish_top, skel.py:384-396): on the
  * (2N x q) UH / PsiV / UH_div, UH_R -= T^T UH_S; w = X_rr^-1 UH_R;
@@ -334,7 +357,7 @@ int skb_copy_rows_cols(int64_t n, const int64_t* idx_dev, int64_t nqc, const int
 int skb_engine_start(const void* const* tree, int64_t depth, const double* root, double factor,
                      int64_t* const* store, int64_t cap, const double* const* geo, int64_t P,
                      double tol, void* stream, int64_t lev_lo, int64_t max_level_ints,
-                     int64_t* handle);
+                     int32_t pde, int64_t* handle);   /* pde 0 Stokes, 1 Laplace */
 /* Block until level L is done: sizes = {rc, B, na, box0, o_int, o_act, h2d bytes,
  * d2h bytes}; ptrs =
  * {act_off, act, rows, A, m_q, perm, k, steps, gap (host), stack, dbuf, dup
@@ -385,7 +408,7 @@ int skb_host_far_lists(int64_t nb, const int64_t* idx, const double* center, con
                        int64_t depth, const double* root, double factor, const int64_t* big,
                        const int64_t* a_start, const int64_t* a_len, const double* px,
                        const double* py, int64_t* far_off, int64_t* far, int64_t cap,
-                       int64_t* need);
+                       int64_t* need, int32_t dof_shift);   /* node = dof >> dof_shift */
 
 /* Proxy rings (kernels.py:263-273): pts = centre + r_p (cos, sin)(2 pi j / P),
  * radial normals about the ring centroid (kernels.py:340-342), weights

@@ -165,17 +165,115 @@ def nullspace_rows(g, cols):
     return ((g.weights[nc] * g.normals[nc, cc])[None, :], g.normals[nc, cc][None, :])
 
 
-def id_stack(g, box_dofs, far, center, radius, count):
+# ---------------------------------------------------------------------------
+# Laplace-Neumann branches (kernels.py:119-125, 161-168, 322-325, 347-352,
+# 368-370; dof_per_node 1: a DOF is a node)
+# ---------------------------------------------------------------------------
+STOKES = "stokes_dirichlet"       # kernels.py:36
+LAPLACE = "laplace_neumann"       # kernels.py:35
+
+
+def lap_self_block(g, rows, cols):
+    """kernels.py:89-130, Laplace branch (119-125): adjoint double layer,
+    same-node limit kappa_row / (4 pi), + 1 completion, x w_col, jump."""
+    nr = np.asarray(rows, np.int64)
+    nc = np.asarray(cols, np.int64)
+    pr, pc = g.positions[nr], g.positions[nc]
+    rx = pr[:, None, 0] - pc[None, :, 0]
+    ry = pr[:, None, 1] - pc[None, :, 1]
+    r2 = rx * rx + ry * ry
+    same = nr[:, None] == nc[None, :]
+    r2s = np.where(same, 1.0, r2)
+    nrt = g.normals[nr]
+    rdn = rx * nrt[:, None, 0] + ry * nrt[:, None, 1]
+    kern = rdn / (2 * np.pi * r2s)
+    lim = np.broadcast_to(g.curvatures[nr][:, None] / (4 * np.pi), kern.shape)
+    kern = np.where(same, lim, kern)
+    kern = kern + 1.0
+    out = kern * g.weights[nc][None, :]
+    out += np.where(nr[:, None] == nc[None, :], JUMP, 0.0)
+    return out
+
+
+def lap_pair_blocks(g, far, box):
+    """(K[far, box], K[box, far]^T), kernels.py:161-168."""
+    nf = np.asarray(far, np.int64)
+    nb = np.asarray(box, np.int64)
+    pf, pb = g.positions[nf], g.positions[nb]
+    rx = pf[:, None, 0] - pb[None, :, 0]
+    ry = pf[:, None, 1] - pb[None, :, 1]
+    r2 = rx * rx + ry * ry
+    wf = g.weights[nf][:, None]
+    wb = g.weights[nb][None, :]
+    nfv, nbv = g.normals[nf], g.normals[nb]
+    rdn_f = rx * nfv[:, None, 0] + ry * nfv[:, None, 1]
+    rdn_b = rx * nbv[None, :, 0] + ry * nbv[None, :, 1]
+    ir2 = 1.0 / (2 * np.pi * r2)
+    return (rdn_f * ir2 + 1.0) * wb, (-rdn_b * ir2 + 1.0) * wf
+
+
+def lap_proxy_incoming(g, pts, cols):
+    """kernels.py:322-325: log potential of the box sources on the proxy ring."""
+    nc = np.asarray(cols, np.int64)
+    rx = pts[:, None, 0] - g.positions[nc][None, :, 0]
+    ry = pts[:, None, 1] - g.positions[nc][None, :, 1]
+    r2 = rx * rx + ry * ry
+    return -0.25 * np.log(r2) / np.pi * g.weights[nc][None, :]
+
+
+def lap_proxy_outgoing(g, rows, pts, pw):
+    """kernels.py:347-352: target-normal dipole at proxy sources, transposed."""
+    nr = np.asarray(rows, np.int64)
+    pos = g.positions[nr]
+    nrt = g.normals[nr]
+    rx = pos[:, None, 0] - pts[None, :, 0]
+    ry = pos[:, None, 1] - pts[None, :, 1]
+    r2 = rx * rx + ry * ry
+    blk = (rx * nrt[:, None, 0] + ry * nrt[:, None, 1]) / (2 * np.pi * r2)
+    return (blk * pw[None, :]).T
+
+
+def lap_nullspace_rows(g, cols):
+    """kernels.py:368-370."""
+    nc = np.asarray(cols, np.int64)
+    return g.weights[nc][None, :], np.ones((1, len(nc)))
+
+
+def lap_forward_block(g, targets, cols):
+    """Interior rows, kernels.py:171-198 Laplace branch: u = -S mu."""
+    targets = np.atleast_2d(np.asarray(targets, float))
+    nc = np.asarray(cols, np.int64)
+    pc = g.positions[nc]
+    rx = targets[:, None, 0] - pc[None, :, 0]
+    ry = targets[:, None, 1] - pc[None, :, 1]
+    r2 = rx * rx + ry * ry
+    return 0.5 * np.log(r2) / (2 * np.pi) * g.weights[nc][None, :]
+
+
+def block(g, rows, cols, pde=STOKES):
+    return self_block(g, rows, cols) if pde == STOKES else lap_self_block(g, rows, cols)
+
+
+def dpn(pde):
+    """SystemSpec.dof_per_node, kernels.py:52-54."""
+    return 2 if pde == STOKES else 1
+
+
+def id_stack(g, box_dofs, far, center, radius, count, pde=STOKES):
     """The stacked ID matrix of one box, skel.py:297-314."""
     nB = len(box_dofs)
     pts, pw = proxy_ring(center, radius, count)
-    e_in, e_out = nullspace_rows(g, box_dofs)
+    if pde == STOKES:
+        pair, pin, pout, null = pair_blocks, proxy_incoming, proxy_outgoing, nullspace_rows
+    else:
+        pair, pin, pout, null = lap_pair_blocks, lap_proxy_incoming, lap_proxy_outgoing, lap_nullspace_rows
+    e_in, e_out = null(g, box_dofs)
     if len(far):
-        k_in, k_out = pair_blocks(g, far, box_dofs)
+        k_in, k_out = pair(g, far, box_dofs)
     else:
         k_in = k_out = np.zeros((0, nB))
-    return np.vstack([k_in, proxy_incoming(g, pts, box_dofs), e_in,
-                      k_out, proxy_outgoing(g, box_dofs, pts, pw), e_out])
+    return np.vstack([k_in, pin(g, pts, box_dofs), e_in,
+                      k_out, pout(g, box_dofs, pts, pw), e_out])
 
 
 def aug_columns(points, centers, workers=1):
@@ -266,12 +364,20 @@ def forward_block(g, targets, cols):
     return out
 
 
-def evaluate_interior(g, solution, targets, chunk=256):
-    """u = D mu + H lam at interior targets, skel.py:537-564 (Stokes)."""
+def evaluate_interior(g, solution, targets, chunk=256, pde=STOKES):
+    """u = D mu + H lam (Stokes, (m, 2)) or u = -S mu (Laplace, (m,)) at
+    interior targets, skel.py:537-564."""
     targets = np.atleast_2d(np.asarray(targets, float))
     if not np.all(point_in_domain(g, targets)):
         raise ValueError("targets must lie strictly inside the domain")
     sol = np.asarray(solution, float)
+    if pde == LAPLACE:
+        nd = len(g.positions)
+        mu = sol[:nd]
+        out = np.empty(len(targets))
+        for s in range(0, len(targets), chunk):
+            out[s:s + chunk] = lap_forward_block(g, targets[s:s + chunk], np.arange(nd)) @ mu
+        return out
     nd = 2 * len(g.positions)
     mu, lam = sol[:nd], sol[nd:]
     dofs = np.arange(nd)
@@ -285,11 +391,11 @@ def evaluate_interior(g, solution, targets, chunk=256):
     return out
 
 
-def dense_system(g):
-    """Full augmented matrix, kernels.py:377-390."""
-    nd = 2 * len(g.positions)
-    A = self_block(g, np.arange(nd), np.arange(nd))
-    q = 3 * g.n_holes
+def dense_system(g, pde=STOKES):
+    """Full (augmented) matrix, kernels.py:377-390."""
+    nd = dpn(pde) * len(g.positions)
+    A = block(g, np.arange(nd), np.arange(nd), pde)
+    q = 3 * g.n_holes if pde == STOKES else 0
     if q == 0:
         return A
     M = np.zeros((nd + q, nd + q))
@@ -300,16 +406,16 @@ def dense_system(g):
     return M
 
 
-def exact_matvec(g, x, chunk=1024):
+def exact_matvec(g, x, chunk=1024, pde=STOKES):
     """Uncompressed system product, kernels.py:393-414."""
-    nd = 2 * len(g.positions)
-    q = 3 * g.n_holes
+    nd = dpn(pde) * len(g.positions)
+    q = 3 * g.n_holes if pde == STOKES else 0
     x = np.asarray(x, float)
     out = np.empty(nd + q)
     allc = np.arange(nd)
     for s in range(0, nd, chunk):
         r = allc[s:s + chunk]
-        out[s:s + len(r)] = self_block(g, r, allc) @ x[:nd]
+        out[s:s + len(r)] = block(g, r, allc, pde) @ x[:nd]
     if q:
         out[:nd] += aug_columns(g.positions, g.hole_centers) @ x[nd:]
         out[nd:] = aug_functionals(g).T @ x[:nd] - x[nd:]
@@ -498,7 +604,8 @@ class OracleFactorization:
         self.root_dofs, self.E_root, self.top = root_dofs, E_root, top
         self.UH, self.PsiV, self.UH_div, self.nonroot = UH, PsiV, UH_div, nonroot
         self.stats = stats
-        self.nd = 2 * len(g.positions)
+        self.pde = stats.get("pde", STOKES)
+        self.nd = dpn(self.pde) * len(g.positions)
         self.q = 0 if UH is None else UH.shape[1]
 
     @property
@@ -579,15 +686,18 @@ class OracleFactorization:
 class _Pass:
     """State of one factor pass (skel.py:227-361)."""
 
-    def __init__(self, g, tree, tol, count, factor):
+    def __init__(self, g, tree, tol, count, factor, pde=STOKES):
         self.g, self.tree, self.tol, self.count, self.factor = g, tree, tol, count, factor
-        self.dof_xy = np.repeat(g.positions, 2, axis=0)
+        self.pde = pde
+        self.dpn = dpn(pde)
+        self.dof_xy = np.repeat(g.positions, self.dpn, axis=0)        # skel.py:233
         self.active = {}
         self.out = {}
         self.record = None   # optional dict key -> per-box debug data
 
     def leaf_dofs(self, bx):
-        return (2 * bx.nodes[:, None] + np.arange(2)[None, :]).ravel()
+        """dofs_of_nodes, skel.py:243-244."""
+        return (self.dpn * bx.nodes[:, None] + np.arange(self.dpn)[None, :]).ravel()
 
     def far(self, bx):
         """skel.py:258-280 (first tuple element)."""
@@ -602,7 +712,7 @@ class _Pass:
 
     def block_E(self, bx):
         """skel.py:282-291."""
-        E = self_block(self.g, self.active[bx.key], self.active[bx.key])
+        E = block(self.g, self.active[bx.key], self.active[bx.key], self.pde)
         off = 0
         for ck in bx.kids:
             c = self.out[ck]
@@ -617,7 +727,7 @@ class _Pass:
         B = self.active[key]
         nB = len(B)
         F = self.far(bx)
-        A = id_stack(self.g, B, F, bx.center, proxy_radius(bx.hw, self.factor), self.count)
+        A = id_stack(self.g, B, F, bx.center, proxy_radius(bx.hw, self.factor), self.count, self.pde)
         qr = QRID(A)
         k = qr.rank(self.tol)
         E = self.block_E(bx)
@@ -692,8 +802,8 @@ class _Pass:
             rd = np.concatenate([self.out[c].skel for c in root.kids])
         self.active[ROOT] = rd
         E_root = self.block_E(root)
-        nd = 2 * len(g.positions)
-        q = 3 * g.n_holes
+        nd = self.dpn * len(g.positions)
+        q = 3 * g.n_holes if self.pde == STOKES else 0        # SystemSpec.augmented, kernels.py:59-60
         UH = PsiV = UH_div = None
         nonroot = np.ones(nd, dtype=bool)
         nonroot[rd] = False
@@ -726,14 +836,14 @@ class _Pass:
         kpl = {lev: max((len(self.out[k].S) for k in keys), default=0) for lev, keys in sweep}
         return OracleFactorization(g, t, self.tol, dict(self.out), sweep, rd, E_root, top,
                                    UH, PsiV, UH_div, nonroot,
-                                   {"k_per_level": kpl, "root_size": len(rd)})
+                                   {"k_per_level": kpl, "root_size": len(rd), "pde": self.pde})
 
 
-def factor(g, tree, tol, proxy_count=64, proxy_factor=1.5, workers=1, record=None):
+def factor(g, tree, tol, proxy_count=64, proxy_factor=1.5, workers=1, record=None, pde=STOKES):
     """skel.py:428-453."""
     t0 = time.perf_counter()
     with threadpool_limits(limits=1):          # skel.py:441
-        p = _Pass(g, tree, tol, proxy_count, proxy_factor)
+        p = _Pass(g, tree, tol, proxy_count, proxy_factor, pde)
         p.record = record
         sweep = p.run(workers)
         f = p.top(sweep, workers)
@@ -831,7 +941,7 @@ def update(fct, b_new, report, workers=1):
                   fct.tree.max_depth)
     dirty = dirty_set(fct.tree, t_new, b_new, report, fct.proxy_factor)
     with threadpool_limits(limits=1):          # skel.py:469
-        p = _Pass(b_new, t_new, fct.tol, fct.proxy_count, fct.proxy_factor)
+        p = _Pass(b_new, t_new, fct.tol, fct.proxy_count, fct.proxy_factor, fct.pde)
         sweep = p.run(workers, reuse=fct.boxes, dirty=dirty)
         f = p.top(sweep, workers)
     f.proxy_count, f.proxy_factor = fct.proxy_count, fct.proxy_factor
@@ -841,8 +951,8 @@ def update(fct, b_new, report, workers=1):
     return f
 
 
-def factor_full(g, leaf_cap, tol, proxy_count, proxy_factor, workers=1, record=None):
+def factor_full(g, leaf_cap, tol, proxy_count, proxy_factor, workers=1, record=None, pde=STOKES):
     t = QTree(g.positions, leaf_cap)
-    f = factor(g, t, tol, proxy_count, proxy_factor, workers, record)
+    f = factor(g, t, tol, proxy_count, proxy_factor, workers, record, pde)
     f.proxy_count, f.proxy_factor = proxy_count, proxy_factor
     return f

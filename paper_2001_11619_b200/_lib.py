@@ -41,6 +41,12 @@ SIGNATURES = {
                            _vp, _i64, _i64, _vp],
     "skb_assemble_self": [_vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
                           _i64, _vp],
+    "skb_assemble_stack_lap": [_vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp,
+                               _vp, _i64, _i64, _vp],
+    "skb_assemble_self_lap": [_vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                              _i64, _vp],
+    "skb_system_matvec_lap": [_vp, _vp, _vp, _vp, _i64, _vp, _i64, _vp, _vp],
+    "skb_eval_interior_lap": [_vp, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _vp],
     "skb_assemble_aug": [_vp, _vp, _i64, _vp, _i64, _vp, _vp, _vp, _vp],
     "skb_geqrf_batched": [_i64, _vp, _vp, _vp, _vp, _vp],
     "skb_qrcp_id_batched": [_i64, _vp, _vp, _vp, _vp, _vp, _f64, _vp, _vp, _vp, _vp, _vp, _vp,
@@ -62,14 +68,14 @@ SIGNATURES = {
     "skb_eval_interior": [_vp, _vp, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _vp],
     "skb_point_in_domain": [_vp, _vp, _i64, _vp, _i64, _vp, _vp],
     "skb_level_schur": [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
-                        _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
+                        _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i32, _vp],
     "skb_level_aug": [_i64, _vp, _vp, _i64] + [_vp] * 17 + [_vp, _vp, _vp, _vp, _i32, _vp],
     "skb_level_schur_acc": [_i64, _vp, _vp, _i64, _vp, _vp, _vp, _vp],
     "skb_level_aug_narrow": [_i64, _vp, _vp, _i64, _i64] + [_vp] * 16 + [_vp, _vp, _vp],
     "skb_restore_rows": [_i64, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _vp],
     "skb_level_aug_update": [_i64, _vp, _vp, _i64] + [_vp] * 16 + [_i64] + [_vp] * 11,
     "skb_copy_rows_cols": [_i64, _vp, _i64, _vp, _i64, _i64, _vp, _vp, _vp],
-    "skb_engine_start": [_vp, _i64, _vp, _f64, _vp, _i64, _vp, _i64, _f64, _vp, _i64, _i64, _vp],
+    "skb_engine_start": [_vp, _i64, _vp, _f64, _vp, _i64, _vp, _i64, _f64, _vp, _i64, _i64, _i32, _vp],
     "skb_engine_wait": [_i64, _i64, _vp, _vp],
     "skb_engine_stream_wait": [_i64, _i64, _vp],
     "skb_engine_release": [_i64, _i64, _vp],
@@ -82,7 +88,7 @@ SIGNATURES = {
     "skb_debug_snap": [_i32, _vp, _i64],
     # native host runtime (host arrays only, no device)
     "skb_host_far_lists": [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _f64,
-                           _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp],
+                           _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _i32],
     "skb_host_proxies": [_i64, _vp, _vp, _vp, _f64, _i64, _vp, _vp, _vp, _vp],
     "skb_host_init": [],
     "skb_tree_build": [_vp, _i64, _i64, _i64, _vp, _vp],

@@ -73,6 +73,7 @@ struct Engine {
   const double *px, *py, *pos, *nrm, *w, *cs;
   int64_t P;
   double tol;
+  int32_t pde = 0;               // 0 Stokes (2 DOFs per node), 1 Laplace (1)
   cudaStream_t s;
   int dev;
   int64_t lev_lo;
@@ -325,14 +326,17 @@ int run_level(Engine& E, int64_t L, LevelOut& R) {
       poff[p].resize(nb + 1);
       pfar[p].resize(4096);
       int64_t need = 0;
+      const int32_t shift = E.pde == 1 ? 0 : 1;
       int r = skb_host_far_lists(nb, idx.data() + lo, E.center, E.hw, E.nbr, E.lev, E.ix, E.iy, E.leaf,
                                  E.level_start, E.depth, E.root, E.factor, E.big, E.a_start, E.a_len,
-                                 E.px, E.py, poff[p].data(), pfar[p].data(), (int64_t)pfar[p].size(), &need);
+                                 E.px, E.py, poff[p].data(), pfar[p].data(), (int64_t)pfar[p].size(), &need,
+                                 shift);
       if (r == 1) {
         pfar[p].resize(need + 1);
         r = skb_host_far_lists(nb, idx.data() + lo, E.center, E.hw, E.nbr, E.lev, E.ix, E.iy, E.leaf,
                                E.level_start, E.depth, E.root, E.factor, E.big, E.a_start, E.a_len,
-                               E.px, E.py, poff[p].data(), pfar[p].data(), (int64_t)pfar[p].size(), &need);
+                               E.px, E.py, poff[p].data(), pfar[p].data(), (int64_t)pfar[p].size(), &need,
+                               shift);
       }
       prc[p] = r;
       skb_host_proxies(nb, idx.data() + lo, E.center, E.hw, E.factor, P, E.cs, pts + lo * P * 2,
@@ -369,7 +373,7 @@ int run_level(Engine& E, int64_t L, LevelOut& R) {
   for (int64_t b = 0; b < B; ++b) {
     nB[b] = R.act_off[b + 1] - R.act_off[b];
     const int64_t nF = far_off[b + 1] - far_off[b];
-    R.rows[b] = 2 * nF + 6 * P + 2;
+    R.rows[b] = E.pde == 1 ? 2 * nF + 2 * P + 2 : 2 * nF + 6 * P + 2;   // skel.py:306-314
     stack_off[b] = so;
     so += R.rows[b] * nB[b];
     maxnB = std::max(maxnB, nB[b]);
@@ -383,7 +387,8 @@ int run_level(Engine& E, int64_t L, LevelOut& R) {
   SKB_RET(cudaMemcpyAsync(R.dup, pk, sizeof(int64_t) * npk, cudaMemcpyHostToDevice, s));
   tm.tick("upload");
   R.h2d += 8 * npk;
-  if ((rc = skb_assemble_stack(E.pos, E.nrm, E.w, B, R.dup + o_ao, R.dup + R.o_act, R.dup + o_fo,
+  if ((rc = (E.pde == 1 ? skb_assemble_stack_lap : skb_assemble_stack)(
+           E.pos, E.nrm, E.w, B, R.dup + o_ao, R.dup + R.o_act, R.dup + o_fo,
                                R.dup + o_f, (const double*)(R.dup + o_pt),
                                (const double*)(R.dup + o_pn), (const double*)(R.dup + o_pw),
                                (int32_t)P, R.dup + o_so, R.stack, maxnB, maxitems, s)))
@@ -514,8 +519,9 @@ extern "C" {
 int skb_engine_start(const void* const* tree, int64_t depth, const double* root, double factor,
                      int64_t* const* store, int64_t cap, const double* const* geo, int64_t P,
                      double tol, void* stream, int64_t lev_lo, int64_t max_level_ints,
-                     int64_t* handle) {
+                     int32_t pde, int64_t* handle) {
   Engine* E = new Engine();
+  E->pde = pde;
   E->center = (const double*)tree[0];
   E->hw = (const double*)tree[1];
   E->nbr = (const int64_t*)tree[2];

@@ -101,7 +101,7 @@ int skb_host_far_lists(int64_t nb, const int64_t* idx, const double* center, con
                        int64_t depth, const double* root, double factor, const int64_t* big,
                        const int64_t* a_start, const int64_t* a_len, const double* px,
                        const double* py, int64_t* far_off, int64_t* far, int64_t cap,
-                       int64_t* need) {
+                       int64_t* need, int32_t dof_shift) {
   TreeView t{center, hw, nbr, lev, ix, iy, is_leaf, level_start, depth, root[0], root[1], root[2]};
   const double s2 = sqrt(2.0);
   std::vector<int64_t> src;
@@ -119,7 +119,7 @@ int skb_host_far_lists(int64_t nb, const int64_t* idx, const double* center, con
     for (int64_t j : src) {
       const int64_t* a = big + a_start[j];
       for (int64_t q = 0; q < a_len[j]; ++q) {
-        const int64_t node = a[q] >> 1;
+        const int64_t node = a[q] >> dof_shift;     // dof -> node (dpn 2: >> 1, dpn 1: id)
         const double dx = px[node] - cx, dy = py[node] - cy;
         if (dx * dx + dy * dy < r2) {               // skel.py:279 strict distance filter
           if (o < cap) far[o] = a[q];

@@ -60,7 +60,7 @@ extern "C" int skb_level_schur(int64_t nbox, const int64_t* nB, const int64_t* k
                                const uint64_t* child_xss, const uint64_t* T, const uint64_t* Xrr,
                                const uint64_t* LU, const uint64_t* Xsr, const uint64_t* Xrsdiv,
                                const uint64_t* Xss, const uint64_t* ipiv, int32_t* info_dev,
-                               double* ratio_dev, void* stream) {
+                               double* ratio_dev, int32_t pde, void* stream) {
   if (nbox <= 0) return 0;
   cudaStream_t s = (cudaStream_t)stream;
   const int64_t B = nbox;
@@ -89,9 +89,9 @@ extern "C" int skb_level_schur(int64_t nbox, const int64_t* nB, const int64_t* k
   pk.add(ldE.data(), B);
   int64_t* dpk = nullptr;
   if ((rc = upload(pk.host.data(), (int64_t)pk.host.size(), s, &dpk))) return rc;
-  if ((rc = skb_assemble_self(pos, nrm, w, kappa, B, act_off_dev, act_dev, act_off_dev, perm_dev,
-                              dpk + pk.at[0], dpk + pk.at[1], Ebuf, dpk + pk.at[2], dpk + pk.at[3],
-                              maxn, s)))
+  if ((rc = (pde == 1 ? skb_assemble_self_lap : skb_assemble_self)(
+           pos, nrm, w, kappa, B, act_off_dev, act_dev, act_off_dev, perm_dev, dpk + pk.at[0],
+           dpk + pk.at[1], Ebuf, dpk + pk.at[2], dpk + pk.at[3], maxn, s)))
     return rc;
   // X_sr = E_SR - E_SS T ; X_rs = E_RS - T^T E_SS ; X_rr = E_RR - E_RS T (skel.py:321-332)
   // problem order as in the Python restatement: [all X_sr | all X_rs | all X_rr]

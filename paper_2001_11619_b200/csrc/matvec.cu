@@ -254,6 +254,111 @@ __global__ void k_point_in_domain(const double2* __restrict__ pos, const int64_t
   if (lane == 0) inside[t] = (ok && sqrt(dmin2) > 1e-12) ? 1 : 0;
 }
 
+
+// ---- Laplace-Neumann (one DOF per node) -----------------------------------
+// s = sum_j w_j mu_j (the +1 completion of kernels.py:125), per RHS
+__global__ void k_mv_wdot(const double* __restrict__ w, int64_t n, const double* __restrict__ x,
+                          int64_t nr, int64_t r0, int rc, double* __restrict__ out) {
+  __shared__ double red[MV_R][MV_T];
+  double acc[MV_R] = {0, 0, 0, 0};
+  for (int64_t j = blockIdx.x * (int64_t)MV_T + threadIdx.x; j < n; j += (int64_t)gridDim.x * MV_T)
+    for (int q = 0; q < rc; ++q) acc[q] += w[j] * x[j * nr + r0 + q];
+  for (int q = 0; q < MV_R; ++q) red[q][threadIdx.x] = acc[q];
+  __syncthreads();
+  for (int o = MV_T / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o)
+      for (int q = 0; q < MV_R; ++q) red[q][threadIdx.x] += red[q][threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0)
+    for (int q = 0; q < rc; ++q) out[blockIdx.x * MV_R + q] = red[q][0];
+}
+
+// y_a = -1/2 mu_a + sum_b K'_ab w_b mu_b + sum_b w_b mu_b, K'_ab = (x_a - x_b).n_a / (2 pi r^2),
+// K'_aa = kappa_a / (4 pi)  (kernels.py:119-125)
+__global__ void __launch_bounds__(MV_T)
+k_mv_direct_lap(const double2* __restrict__ pos, const double2* __restrict__ nrm,
+                const double* __restrict__ w, const double* __restrict__ kappa, int64_t n,
+                const double* __restrict__ x, int64_t nr, int64_t r0, int rc,
+                const double* __restrict__ parts, int nparts, double* __restrict__ y) {
+  __shared__ double2 sp[MV_T];
+  __shared__ double swx[MV_T][MV_R];
+  __shared__ double s_w[MV_R];
+  const int64_t i = blockIdx.x * (int64_t)MV_T + threadIdx.x;
+  if (threadIdx.x < MV_R) {
+    double sm = 0.0;
+    for (int b = 0; b < nparts; ++b) sm += parts[b * MV_R + threadIdx.x];
+    s_w[threadIdx.x] = sm;
+  }
+  const bool act = i < n;
+  const double2 pi = act ? pos[i] : make_double2(0, 0);
+  const double2 ni = act ? nrm[i] : make_double2(0, 0);
+  double a[MV_R] = {0, 0, 0, 0};
+  for (int64_t j0 = 0; j0 < n; j0 += MV_T) {
+    __syncthreads();
+    const int64_t j = j0 + threadIdx.x;
+    if (j < n) {
+      sp[threadIdx.x] = pos[j];
+      for (int q = 0; q < rc; ++q) swx[threadIdx.x][q] = w[j] * x[j * nr + r0 + q];
+    }
+    __syncthreads();
+    const int jn = (int)((n - j0) < MV_T ? (n - j0) : MV_T);
+    if (!act) continue;
+    for (int jj = 0; jj < jn; ++jj) {
+      const int64_t jg = j0 + jj;
+      double k;
+      if (jg == i) {
+        k = kappa[i] / (4.0 * MV_PI);
+      } else {
+        const double2 pj = sp[jj];
+        const double rx = pi.x - pj.x, ry = pi.y - pj.y;
+        k = (rx * ni.x + ry * ni.y) / ((2.0 * MV_PI) * (rx * rx + ry * ry));
+      }
+      for (int q = 0; q < MV_R; ++q) {
+        if (q >= rc) break;
+        a[q] += k * swx[jj][q];
+      }
+    }
+  }
+  if (!act) return;
+  for (int q = 0; q < rc; ++q) y[i * nr + r0 + q] = a[q] + s_w[q] - 0.5 * x[i * nr + r0 + q];
+}
+
+// u(t) = sum_j (1/2 log r^2 / (2 pi)) w_j mu_j  (kernels.py:193-194; u = -S mu)
+__global__ void __launch_bounds__(MV_T)
+k_eval_interior_lap(const double2* __restrict__ pos, const double* __restrict__ w, int64_t n,
+                    const double* __restrict__ x, int64_t nr, int64_t r0, int rc,
+                    const double2* __restrict__ tgt, int64_t m, double* __restrict__ out) {
+  __shared__ double2 sp[MV_T];
+  __shared__ double swx[MV_T][MV_R];
+  const int64_t i = blockIdx.x * (int64_t)MV_T + threadIdx.x;
+  const bool act = i < m;
+  const double2 ti = act ? tgt[i] : make_double2(0, 0);
+  double a[MV_R] = {0, 0, 0, 0};
+  for (int64_t j0 = 0; j0 < n; j0 += MV_T) {
+    __syncthreads();
+    const int64_t j = j0 + threadIdx.x;
+    if (j < n) {
+      sp[threadIdx.x] = pos[j];
+      for (int q = 0; q < rc; ++q) swx[threadIdx.x][q] = w[j] * x[j * nr + r0 + q];
+    }
+    __syncthreads();
+    const int jn = (int)((n - j0) < MV_T ? (n - j0) : MV_T);
+    if (!act) continue;
+    for (int jj = 0; jj < jn; ++jj) {
+      const double2 pj = sp[jj];
+      const double rx = ti.x - pj.x, ry = ti.y - pj.y;
+      const double g = (0.5 * log(rx * rx + ry * ry)) / (2.0 * MV_PI);
+      for (int q = 0; q < MV_R; ++q) {
+        if (q >= rc) break;
+        a[q] += g * swx[jj][q];
+      }
+    }
+  }
+  if (!act) return;
+  for (int q = 0; q < rc; ++q) out[i * nr + r0 + q] = a[q];
+}
+
 }  // namespace skb
 
 using namespace skb;
@@ -304,6 +409,39 @@ extern "C" int skb_point_in_domain(const double* pos, const int64_t* curve_off_d
   cudaStream_t s = (cudaStream_t)stream;
   k_point_in_domain<<<(unsigned)((m * 32 + 255) / 256), 256, 0, s>>>(
       (const double2*)pos, curve_off_dev, ncurves, (const double2*)targets, m, inside);
+  SKB_LAUNCH_CHECK();
+  return 0;
+}
+
+extern "C" int skb_system_matvec_lap(const double* pos, const double* nrm, const double* w,
+                                     const double* kappa, int64_t n_nodes, const double* x,
+                                     int64_t nrhs, double* y, void* stream) {
+  if (n_nodes <= 0 || nrhs <= 0) return 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int nparts = 148;
+  double* parts = nullptr;
+  SKB_RET(malloc_async((void**)&parts, sizeof(double) * nparts * MV_R, s));
+  for (int64_t r0 = 0; r0 < nrhs; r0 += MV_R) {
+    const int rc = (int)((nrhs - r0) < MV_R ? (nrhs - r0) : MV_R);
+    k_mv_wdot<<<nparts, MV_T, 0, s>>>(w, n_nodes, x, nrhs, r0, rc, parts);
+    k_mv_direct_lap<<<(unsigned)((n_nodes + MV_T - 1) / MV_T), MV_T, 0, s>>>(
+        (const double2*)pos, (const double2*)nrm, w, kappa, n_nodes, x, nrhs, r0, rc, parts, nparts, y);
+  }
+  cudaError_t e = cudaGetLastError();
+  cudaFreeAsync(parts, s);
+  return e == cudaSuccess ? 0 : -(int)e;
+}
+
+extern "C" int skb_eval_interior_lap(const double* pos, const double* w, int64_t n_nodes,
+                                     const double* x, int64_t nrhs, const double* targets, int64_t m,
+                                     double* out, void* stream) {
+  if (m <= 0 || nrhs <= 0) return 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  for (int64_t r0 = 0; r0 < nrhs; r0 += MV_R) {
+    const int rc = (int)((nrhs - r0) < MV_R ? (nrhs - r0) : MV_R);
+    k_eval_interior_lap<<<(unsigned)((m + MV_T - 1) / MV_T), MV_T, 0, s>>>(
+        (const double2*)pos, w, n_nodes, x, nrhs, r0, rc, (const double2*)targets, m, out);
+  }
   SKB_LAUNCH_CHECK();
   return 0;
 }

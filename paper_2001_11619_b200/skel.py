@@ -40,6 +40,7 @@ PIVOT_RATIO_FLOOR = 1e-12          # skel.py:46
 DEFAULT_PROXY_COUNT = 64           # skel.py:47
 DEFAULT_PROXY_FACTOR = 1.5         # skel.py:48
 STOKES = "stokes_dirichlet"        # kernels.py:36
+LAPLACE = "laplace_neumann"        # kernels.py:35
 
 
 class SingularPivotError(RuntimeError):
@@ -56,23 +57,34 @@ class RootBoxExceededError(RuntimeError):
 
 @dataclass(frozen=True)
 class SystemSpec:
-    """PDE selection (reference kernels.py:41-63); Stokes only on this path."""
+    """PDE / kernel selection (reference kernels.py:41-63): the Stokes
+    double layer with the multiply-connected augmentation, or the
+    Laplace-Neumann adjoint double layer (one DOF per node, never augmented)."""
 
     pde: str = STOKES
 
     def __post_init__(self):
-        if self.pde != STOKES:
-            raise ValueError("only the Stokes double-layer system is on the B200 path")
+        if self.pde not in (LAPLACE, STOKES):
+            raise ValueError(f"unknown pde {self.pde!r}")
 
     @property
     def dof_per_node(self) -> int:
-        return 2
+        return 2 if self.pde == STOKES else 1
+
+    @property
+    def jump_coefficient(self) -> float:
+        return -0.5                 # kernels.py:38
+
+    @property
+    def code(self) -> int:
+        """C-ABI pde code: 0 Stokes, 1 Laplace."""
+        return 0 if self.pde == STOKES else 1
 
     def augmented(self, b) -> bool:
-        return b.n_holes >= 1
+        return self.pde == STOKES and b.n_holes >= 1
 
     def n_dofs(self, b) -> int:
-        return 2 * b.n_nodes
+        return self.dof_per_node * b.n_nodes
 
 
 # ---------------------------------------------------------------------------
@@ -213,7 +225,7 @@ class ActStore:
     array (vectorised replacement of the reference's per-box ``bx.active`` /
     ``bx.skel`` arrays, skel.py:243-256)."""
 
-    def __init__(self, t: Tree, engine: bool = False):
+    def __init__(self, t: Tree, engine: bool = False, dpn: int = 2):
         nbox = len(t.lev)
         cap = 2 * t.n_nodes * (t.depth + 3) + 16
         if engine:
@@ -225,7 +237,7 @@ class ActStore:
         self.s_start = np.zeros(nbox, np.int64)
         self.s_len = np.zeros(nbox, np.int64)
         self.xss = np.zeros(nbox, np.uint64)
-        init = getattr(t, "_store_init", None)     # leaf actives depend on the tree only
+        init = getattr(t, f"_store_init{dpn}", None)    # leaf actives depend on the tree only
         if init is not None:
             fill, a_start, a_len, prefix = init
             self.big[:fill] = prefix
@@ -241,15 +253,16 @@ class ActStore:
             if len(li) == 0:
                 continue
             off, nodes = _seg_gather(t.level_nodes[l], t.node_start[li], t.node_cnt[li])
-            dofs = (2 * nodes[:, None] + np.arange(2)[None, :]).ravel()
-            self.a_start[li] = self._append(dofs) + 2 * off[:-1]
-            self.a_len[li] = 2 * t.node_cnt[li]
-        t._store_init = (self.fill, self.a_start.copy(), self.a_len.copy(), self.big[:self.fill].copy())
+            dofs = (dpn * nodes[:, None] + np.arange(dpn)[None, :]).ravel()   # skel.py:243-244
+            self.a_start[li] = self._append(dofs) + dpn * off[:-1]
+            self.a_len[li] = dpn * t.node_cnt[li]
+        setattr(t, f"_store_init{dpn}",
+                (self.fill, self.a_start.copy(), self.a_len.copy(), self.big[:self.fill].copy()))
 
     @classmethod
-    def replay(cls, t: Tree, act_of: dict) -> "ActStore":
+    def replay(cls, t: Tree, act_of: dict, dpn: int = 2) -> "ActStore":
         """Store with given active sets (per-level replay of recorded inputs)."""
-        st = cls(t)
+        st = cls(t, dpn=dpn)
         for i, a in act_of.items():
             st.a_start[i] = st._append(np.asarray(a, np.int64))
             st.a_len[i] = len(a)
@@ -337,7 +350,7 @@ def _native_far_lists(ctx, idx, store):
             nv["iy"].ctypes.data, nv["leaf"].ctypes.data, nv["ls"].ctypes.data, ctx.t.depth,
             nv["root"].ctypes.data, ctx.factor, store.big.ctypes.data, store.a_start.ctypes.data,
             store.a_len.ctypes.data, ctx.px.ctypes.data, ctx.py.ctypes.data, off.ctypes.data,
-            far.ctypes.data, cap, need.ctypes.data)
+            far.ctypes.data, cap, need.ctypes.data, 1 if ctx.dpn == 2 else 0)
         if rc == 0:
             ctx._far_cap = cap
             return off, far[:int(need[0])]
@@ -548,6 +561,7 @@ class LevelFactors:
 class _Ctx:
     def __init__(self, spec, b, t: Tree, tol, proxy_count, proxy_factor):
         self.spec, self.b, self.t = spec, b, t
+        self.dpn, self.pde = spec.dof_per_node, spec.code
         self.tol, self.P, self.factor = float(tol), int(proxy_count), float(proxy_factor)
         if self.P < 8:
             raise ValueError("need at least 8 proxy nodes")
@@ -604,7 +618,7 @@ class _Ctx:
         _, flat = _seg_gather(store.big, store.a_start[ps], lens)
         owner = np.repeat(pb, lens)
         # ((dof_pos - c)**2).sum(axis=1) of skel.py:279, same rounding: dx*dx + dy*dy
-        node = flat >> 1
+        node = flat >> (1 if self.dpn == 2 else 0)
         dx = self.px[node] - t.center[idx, 0][owner]
         dy = self.py[node] - t.center[idx, 1][owner]
         d2 = dx * dx + dy * dy
@@ -675,7 +689,7 @@ class _Ctx:
             far_off, far = self.far_lists(idx, store, prep["pairs"])
         nF = np.diff(far_off)
         pts, pn, pw = prep["proxies"]
-        rows = 2 * nF + 6 * P + 2
+        rows = 2 * nF + (6 if self.dpn == 2 else 2) * P + 2       # stack rows, skel.py:306-314
         sizes = rows * nB
         stack_off = np.zeros(B + 1, np.int64)
         np.cumsum(sizes, out=stack_off[1:])
@@ -688,7 +702,8 @@ class _Ctx:
                      far_off=far_off, far=far if len(far) else np.zeros(1, np.int64),
                      pts=pts.reshape(-1), pn=pn.reshape(-1), pw=pw, stack_off=stack_off[:-1])
         s = _stream()
-        call("skb_assemble_stack", ptr(self.g.pos), ptr(self.g.nrm), ptr(self.g.w), B,
+        call("skb_assemble_stack" if self.dpn == 2 else "skb_assemble_stack_lap",
+             ptr(self.g.pos), ptr(self.g.nrm), ptr(self.g.w), B,
              ptr(up["act_off"]), ptr(up["act"]), ptr(up["far_off"]), ptr(up["far"]),
              ptr(up["pts"]), ptr(up["pn"]), ptr(up["pw"]), P, ptr(up["stack_off"]), ptr(stack),
              int(nB.max(initial=0)), int((nF + P + 1).max(initial=0)), s)
@@ -826,7 +841,7 @@ class _Ctx:
              ptr(self.g.pos), ptr(self.g.nrm), ptr(self.g.w), ptr(self.g.kap), act_off_d,
              act_d, perm_d, A, lda, np.ascontiguousarray(co.reshape(-1)),
              np.ascontiguousarray(cx.reshape(-1)), bt.ptr["T"], bt.ptr["Xrr"], bt.ptr["LU"],
-             bt.ptr["Xsr"], bt.ptr["Xrsdiv"], bt.ptr["Xss"], bt.ipiv, info_d, ratio_d,
+             bt.ptr["Xsr"], bt.ptr["Xrsdiv"], bt.ptr["Xss"], bt.ipiv, info_d, ratio_d, self.pde,
              _stream())
         _Prof.tick("c_schur")
         # X_RR pivot info for the migration rule: copied asynchronously, checked
@@ -965,7 +980,7 @@ class Factorization:
 
     @property
     def n_dofs(self) -> int:
-        return 2 * self.boundary.n_nodes
+        return self.spec.dof_per_node * self.boundary.n_nodes
 
     def _psi_lists(self, with_root: bool):
         """Per augmentation column, the DOF rows where PsiV can be nonzero (rows
@@ -1513,14 +1528,15 @@ def _finish_top(ctx: _Ctx, levels, store, pipe: "_AugPipe"):
     store.set_internal(t, np.array([root]))
     rd = store.act(root).copy()
     ns = len(rd)
-    nd = 2 * b.n_nodes
+    nd = ctx.dpn * b.n_nodes
     q = 3 * b.n_holes if ctx.spec.augmented(b) else 0
     co, cx = ctx.child_desc(np.array([root]), store)
     E_root = torch.empty((max(ns, 1), max(ns, 1)), dtype=torch.float64, device=dev)
     up = _upload(ao=np.array([0, ns], np.int64), a=rd if ns else np.zeros(1, np.int64),
                  co=co.reshape(-1), cx=cx.reshape(-1), eo=np.zeros(1, np.int64),
                  eld=np.array([ns], np.int64))
-    call("skb_assemble_self", ptr(ctx.g.pos), ptr(ctx.g.nrm), ptr(ctx.g.w), ptr(ctx.g.kap), 1,
+    call("skb_assemble_self" if ctx.dpn == 2 else "skb_assemble_self_lap",
+         ptr(ctx.g.pos), ptr(ctx.g.nrm), ptr(ctx.g.w), ptr(ctx.g.kap), 1,
          ptr(up["ao"]), ptr(up["a"]), None, None, ptr(up["co"]), ptr(up["cx"]), ptr(E_root),
          ptr(up["eo"]), ptr(up["eld"]), ns, s)
     UH = PsiV = UH_div = None
@@ -1615,7 +1631,8 @@ class _Engine:
             rc = self.lib.skb_engine_start(tree, t.depth, nv["root"].ctypes.data, ctx.factor, st,
                                            len(store.big), geo, ctx.P, ctx.tol, _stream(),
                                            0 if update is not None else 1,
-                                           2 * t.n_nodes + 3 * len(t.lev) + 16, ctypes.byref(self.h))
+                                           2 * t.n_nodes + 3 * len(t.lev) + 16, ctx.pde,
+                                           ctypes.byref(self.h))
         if rc:
             raise _lib.SkbError(f"skb_engine_start returned {rc}")
         self.h = self.h.value
@@ -1698,7 +1715,7 @@ def _run_levels_engine(ctx: _Ctx):
     migration check, augmentation sweep, level descriptors)."""
     t = ctx.t
     with _ht("E.store"):
-        store = ActStore(t, engine=True)
+        store = ActStore(t, engine=True, dpn=ctx.dpn)
     ctx.store = store
     with _ht("E.start"):
         eng = _Engine(ctx, store)
@@ -1754,7 +1771,7 @@ def _run_levels_engine_update(ctx: _Ctx, old: dict, dmask):
     with _ht("U.clean"):
         coff, cskel = _clean_skeletons(t, old, dmask)
     with _ht("U.store"):
-        store = ActStore(t, engine=True)
+        store = ActStore(t, engine=True, dpn=ctx.dpn)
     ctx.store = store
     with _ht("U.engine"):
         eng = _Engine(ctx, store, update=(np.ascontiguousarray(dmask, np.uint8), coff, cskel))
@@ -1829,7 +1846,7 @@ def _run_levels(ctx: _Ctx, reuse=None, dirty=None):
     stream, so the host bookkeeping and the Schur work overlap the critical
     QRCP -> host -> QRCP chain."""
     t = ctx.t
-    store = ActStore(t)
+    store = ActStore(t, dpn=ctx.dpn)
     ctx.store = store
     levels = []
     n_recomp = 0
@@ -2047,19 +2064,22 @@ def system_matvec(spec, b, x):
     kernels.py:393-414), direct O(N^2) summation; x: (dim,) or (dim, nrhs)."""
     is_t = isinstance(x, torch.Tensor)
     xa = x if is_t else np.asarray(x, float)
-    nd, q = 2 * b.n_nodes, 3 * b.n_holes if spec.augmented(b) else 0
+    nd, q = spec.dof_per_node * b.n_nodes, 3 * b.n_holes if spec.augmented(b) else 0
     if xa.shape[0] != nd + q:
         raise ValueError("dimension mismatch")
     dev = _dev()
     X = (xa.to(device=dev, dtype=torch.float64) if is_t
          else torch.from_numpy(np.ascontiguousarray(xa)).to(dev)).reshape(nd + q, -1).contiguous()
     g = getattr(b, "_skb_device", None) or DeviceBoundary(b)
-    up = _upload(hc=np.ascontiguousarray(b.hole_centers, np.float64).reshape(-1)
-                 if b.n_holes else np.zeros(2),
-                 co=np.ascontiguousarray(b.offsets, np.int64))
     Y = torch.empty_like(X)
-    call("skb_system_matvec", g.pos, g.nrm, g.w, g.kap, b.n_nodes, up["hc"], q // 3, up["co"], X,
-         X.shape[1], Y, _stream())
+    if spec.pde == LAPLACE:
+        call("skb_system_matvec_lap", g.pos, g.nrm, g.w, g.kap, b.n_nodes, X, X.shape[1], Y, _stream())
+    else:
+        up = _upload(hc=np.ascontiguousarray(b.hole_centers, np.float64).reshape(-1)
+                     if b.n_holes else np.zeros(2),
+                     co=np.ascontiguousarray(b.offsets, np.int64))
+        call("skb_system_matvec", g.pos, g.nrm, g.w, g.kap, b.n_nodes, up["hc"], q // 3, up["co"], X,
+             X.shape[1], Y, _stream())
     if is_t:
         return Y.reshape(x.shape)
     out = Y.cpu().numpy()
@@ -2084,17 +2104,19 @@ def point_in_domain(b, points) -> np.ndarray:
 
 def evaluate_interior(spec, b, solution, targets, chunk: int = 256):
     """Field at interior targets from a solve() output (reference
-    evaluate_interior, skel.py:537-564): u = D mu + H lam by direct summation
-    on the GPU (eval_forward_block kernels.py:171-198 + the Stokeslet/rotlet
-    columns kernels.py:201-223).  Returns (m, 2); ``solution`` may also be a
-    (dim, nrhs) matrix (then (m, 2, nrhs)).  Exterior targets are rejected.
-    ``chunk`` is accepted for signature parity (all targets run in one launch)."""
+    evaluate_interior, skel.py:537-564) by direct summation on the GPU:
+    Stokes u = D mu + H lam (eval_forward_block kernels.py:171-198 + the
+    Stokeslet/rotlet columns kernels.py:201-223), shape (m, 2); Laplace
+    u = -S mu (kernels.py:193-194), shape (m,).  A (dim, nrhs) solution gives
+    (m, 2, nrhs) / (m, nrhs).  Exterior targets are rejected.  ``chunk`` is
+    accepted for signature parity (all targets run in one launch)."""
     tg = np.ascontiguousarray(np.atleast_2d(np.asarray(targets, float)), np.float64)
     if not np.all(point_in_domain(b, tg)):
         raise ValueError("targets must lie strictly inside the domain")
     is_t = isinstance(solution, torch.Tensor)
     sol = solution if is_t else np.asarray(solution, float)
-    nd, q = 2 * b.n_nodes, 3 * b.n_holes if spec.augmented(b) else 0
+    dpn = spec.dof_per_node
+    nd, q = dpn * b.n_nodes, 3 * b.n_holes if spec.augmented(b) else 0
     if sol.shape[0] != nd + q:
         raise ValueError("dimension mismatch")
     vec = sol.ndim == 1
@@ -2103,13 +2125,18 @@ def evaluate_interior(spec, b, solution, targets, chunk: int = 256):
          else torch.from_numpy(np.ascontiguousarray(sol)).to(dev)).reshape(nd + q, -1).contiguous()
     nr = X.shape[1]
     g = getattr(b, "_skb_device", None) or DeviceBoundary(b)
-    up = _upload(hc=np.ascontiguousarray(b.hole_centers, np.float64).reshape(-1)
-                 if b.n_holes else np.zeros(2), tg=tg.reshape(-1))
     m = len(tg)
-    Y = torch.empty((2 * m, nr), dtype=torch.float64, device=dev)
-    call("skb_eval_interior", g.pos, g.nrm, g.w, b.n_nodes, up["hc"], q // 3, X, nr, up["tg"], m, Y,
-         _stream())
-    Y = Y.reshape(m, 2, nr)
-    if vec:
-        Y = Y[:, :, 0]
+    Y = torch.empty((dpn * m, nr), dtype=torch.float64, device=dev)
+    if spec.pde == LAPLACE:
+        up = _upload(tg=tg.reshape(-1))
+        call("skb_eval_interior_lap", g.pos, g.w, b.n_nodes, X, nr, up["tg"], m, Y, _stream())
+        Y = Y[:, 0] if vec else Y
+    else:
+        up = _upload(hc=np.ascontiguousarray(b.hole_centers, np.float64).reshape(-1)
+                     if b.n_holes else np.zeros(2), tg=tg.reshape(-1))
+        call("skb_eval_interior", g.pos, g.nrm, g.w, b.n_nodes, up["hc"], q // 3, X, nr, up["tg"], m, Y,
+             _stream())
+        Y = Y.reshape(m, 2, nr)
+        if vec:
+            Y = Y[:, :, 0]
     return Y if is_t else Y.cpu().numpy()

@@ -59,11 +59,11 @@ def to_ref_boundary(s, b):
     return rb
 
 
-def record_factor(s, wl, stack_boxes=2, t_boxes=6):
+def record_factor(s, wl, stack_boxes=2, t_boxes=6, pde=None):
     """Run the reference factor with a recorder on compress_box / PivotedQR."""
     from skelsolve import skel as sk
     b = to_ref_boundary(s, wl.boundary)
-    spec = s.SystemSpec(s.STOKES)
+    spec = s.SystemSpec(pde or s.STOKES)
     tree = s.build_tree(b.positions, leaf_cap=wl.leaf_cap)
     rec = {}
     orig_cb = sk._Compressor.compress_box
@@ -206,6 +206,36 @@ def main():
     out["mini_upd_dirty"] = np.array(sorted(dirty_seen["d"]), dtype=np.int64)
     out["mini_upd_x"] = fu.solve(rhs)
     print("mini boxes", len(rec), "k/level", fct.stats["k_per_level"], "n_dirty", fu.stats["n_dirty"])
+
+    # ---- Laplace-Neumann branch (kernels.py:119-125,161-168,322-325,347-352,368-370)
+    # on the cfg1 star: RHS = normal derivative of the harmonic log|x - c|, c outside
+    wl = configs.cfg1()
+    b, spec, tree, fct, rec = record_factor(s, wl, pde=s.LAPLACE)
+    leaf_keys = [k for k in sorted(rec) if k[0] == tree.depth]
+    out.update(pack(rec, fct, "lap_", [leaf_keys[0]], [leaf_keys[0]]))
+    c0 = np.array([1.7, 0.4])
+    d = wl.boundary.positions - c0[None, :]
+    f = (d * wl.boundary.normals).sum(axis=1) / (d * d).sum(axis=1)
+    out["lap_rhs"] = f
+    out["lap_x"] = fct.solve(f)
+    v = np.random.default_rng(13).standard_normal(fct.dim)
+    out["lap_apply_in"] = v
+    out["lap_apply_out"] = fct.apply(v)
+    tg = configs.interior_targets(wl.boundary, 32, seed=4)
+    out["lap_targets"] = tg
+    out["lap_interior"] = s.evaluate_interior(spec, b, out["lap_x"], tg)
+    print("laplace boxes", len(rec), "k/level", fct.stats["k_per_level"], "root", fct.stats["root_size"])
+    # Laplace on the 3-hole geometry + a hole move (update path, no augmentation)
+    wl = configs.mini_holes()
+    b, spec, tree, fct, rec = record_factor(s, wl, pde=s.LAPLACE)
+    out.update(pack(rec, fct, "lapm_", [], []))
+    rhs = np.random.default_rng(14).standard_normal(fct.dim)
+    out["lapm_rhs"] = rhs
+    out["lapm_x"] = fct.solve(rhs)
+    b_new, rep = s.apply_perturbation(b, [s.MoveHole(1, translation=(-0.08, 0.06))])
+    fu = s.update(fct, b_new, rep)
+    out["lapm_upd_x"] = fu.solve(rhs)
+    out["lapm_upd_ndirty"] = np.array(fu.stats["n_dirty"])
 
     # ---- unphased cfg2: equispaced circles centred on box axes -> exact pivot
     # ties; per-box active sets, skeletons and |R_jj| for the tie-classified replay

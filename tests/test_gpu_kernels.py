@@ -350,3 +350,54 @@ np.save(sys.argv[1], np.stack(outs))
         res.append(np.load(out))
     assert np.array_equal(res[0][0], res[0][1])       # n = 200 vs n = 37
     assert np.array_equal(res[0], res[1])             # 64x64 vs 128x128 tiles
+
+
+def test_laplace_stack_and_self_block_bitwise(golden):
+    """Laplace-Neumann branch: the GPU ID stack of a leaf box equals the
+    reference's np.vstack(blocks) bitwise except the log() proxy rows
+    (<= 4 ulp); self blocks equal the oracle's Laplace eval_block bitwise."""
+    wl = configs.cfg1()
+    spec = skel.SystemSpec(skel.LAPLACE)
+    t = build_tree(wl.boundary.positions, wl.leaf_cap)
+    ctx = skel._Ctx(spec, wl.boundary, t, wl.tol, wl.proxy_count, wl.proxy_factor)
+    ref = _golden_boxes(golden, "lap_")
+    key = tuple(golden["lap_stack0_key"])
+    S_ref = golden["lap_stack0"]
+    bi = t.index(key)
+    act_of = {j: ref[t.key(j)]["act"] for j in range(len(t.lev)) if t.key(j) in ref}
+    idx = np.array([bi])
+    act_off, act = skel._csr([act_of[bi]])
+    far_off, far = ctx.far_lists(idx, skel.ActStore.replay(t, act_of, dpn=1))
+    assert np.array_equal(far, ref[key]["far"])
+    pts, pn, pw = ctx.proxies(idx)
+    nB, nF, P = len(act), len(far), wl.proxy_count
+    rows = 2 * nF + 2 * P + 2
+    st = torch.empty(rows * nB, dtype=torch.float64, device="cuda")
+    up = skel._upload(ao=act_off, a=act, fo=far_off, f=far if nF else np.zeros(1, np.int64),
+                      pts=pts.reshape(-1), pn=pn.reshape(-1), pw=pw, so=np.zeros(1, np.int64))
+    g = ctx.g
+    call("skb_assemble_stack_lap", g.pos, g.nrm, g.w, 1, up["ao"], up["a"], up["fo"], up["f"],
+         up["pts"], up["pn"], up["pw"], P, up["so"], st, nB, nF + P + 1, skel._stream())
+    got = st.cpu().numpy().reshape(nB, rows).T
+    assert got.shape == S_ref.shape
+    ul = _ulp_diff(got, S_ref)
+    log_rows = np.zeros(rows, bool)
+    log_rows[nF:nF + P] = True
+    assert ul[~log_rows].max() == 0
+    assert ul[log_rows].max() <= 4
+    # self blocks of 4 leaf boxes
+    idx = t.level_indices(t.depth)[:4]
+    lists = [t.nodes_of(i).astype(np.int64) for i in idx]
+    ao, a = skel._csr(lists)
+    nBs = np.diff(ao)
+    eo = np.concatenate([[0], np.cumsum(nBs * nBs)])
+    E = torch.empty(int(eo[-1]), dtype=torch.float64, device="cuda")
+    co = np.full((len(idx), 5), -1, np.int64)
+    cx = np.zeros((len(idx), 4), np.uint64)
+    up = skel._upload(ao=ao, a=a, co=co.reshape(-1), cx=cx.reshape(-1), eo=eo[:-1], eld=nBs)
+    call("skb_assemble_self_lap", g.pos, g.nrm, g.w, g.kap, len(idx), up["ao"], up["a"], None, None,
+         up["co"], up["cx"], E, up["eo"], up["eld"], int(nBs.max()), skel._stream())
+    En = E.cpu().numpy()
+    for bi_, lst in enumerate(lists):
+        refE = O.lap_self_block(wl.boundary, lst, lst)
+        assert np.array_equal(En[eo[bi_]:eo[bi_ + 1]].reshape(nBs[bi_], nBs[bi_]), refE)

@@ -330,3 +330,58 @@ def test_unphased_cfg2_end_to_end(golden):
     print(f"unphased cfg2: {same}/{len(keys)} identical skeletons end to end; solve rel diff "
           f"{_rel(x, xr):.2e}; residual GPU {rg:.2e} reference {rc:.2e}")
     assert rg <= 2 * rc
+
+
+@pytest.mark.parametrize("name,builder", [("lap_", configs.cfg1), ("lapm_", configs.mini_holes)])
+def test_laplace_factor_solve_vs_reference(golden, name, builder):
+    """Laplace-Neumann variant (kernels.py:119-125,
+    161-168, 322-325, 347-352, 368-370): identical skeletons per box and root
+    DOFs, solve / apply within 10 eps of the reference, residual against the
+    exact operator, and the interior field u = -S mu."""
+    from paper_2001_11619_b200 import LAPLACE, evaluate_interior, system_matvec
+    wl = builder()
+    b = wl.boundary
+    spec = SystemSpec(LAPLACE)
+    t = build_tree(b.positions, wl.leaf_cap)
+    f = factor(spec, b, t, wl.tol, proxy_count=wl.proxy_count, proxy_factor=wl.proxy_factor)
+    assert f.dim == b.n_nodes
+    keys = [tuple(k) for k in golden[name + "keys"]]
+    so, S = golden[name + "S_off"], golden[name + "S"]
+    bad = [k for i, k in enumerate(keys) if not np.array_equal(f.factors[k].S_loc, S[so[i]:so[i + 1]])]
+    assert not bad, bad
+    assert np.array_equal(f.root_dofs, golden[name + "root_dofs"])
+    kpl = {int(l): int(v) for l, v in golden[name + "k_per_level"]}
+    assert f.stats["k_per_level"] == kpl
+    rhs = golden[name + "rhs"]
+    x = f.solve(rhs)
+    assert _rel(x, golden[name + "x"]) <= 10 * wl.tol
+    r = system_matvec(spec, b, x) - rhs
+    assert np.linalg.norm(r) / np.linalg.norm(rhs) < 1e-8
+    if name + "apply_in" in golden.files:
+        y = f.apply(golden[name + "apply_in"])
+        assert _rel(y, golden[name + "apply_out"]) <= 10 * wl.tol
+    if name + "interior" in golden.files:
+        u = evaluate_interior(spec, b, golden[name + "x"], golden[name + "targets"])
+        ref = golden[name + "interior"]
+        assert u.shape == ref.shape
+        assert np.max(np.abs(u - ref)) <= 1e-12 * np.max(np.abs(ref))
+
+
+def test_laplace_update_equals_refactor(golden):
+    """Laplace hole-move update on the 3-hole geometry: equals the reference's
+    update within 10 eps and the GPU refactor bitwise."""
+    from paper_2001_11619_b200 import LAPLACE
+    wl = configs.mini_holes()
+    b = wl.boundary
+    spec = SystemSpec(LAPLACE)
+    f = factor(spec, b, build_tree(b.positions, wl.leaf_cap), wl.tol, proxy_count=wl.proxy_count,
+               proxy_factor=wl.proxy_factor)
+    nb, rep = apply_perturbation(b, [MoveHole(1, translation=(-0.08, 0.06))])
+    fu = update(f, nb, rep)
+    assert fu.stats["n_dirty"] == int(golden["lapm_upd_ndirty"])
+    rhs = golden["lapm_rhs"]
+    xu = fu.solve(rhs)
+    assert _rel(xu, golden["lapm_upd_x"]) <= 10 * wl.tol
+    t2 = build_tree(nb.positions, wl.leaf_cap, root_box=(f.tree.root_center, f.tree.root_half_width))
+    fr = factor(spec, nb, t2, wl.tol, proxy_count=wl.proxy_count, proxy_factor=wl.proxy_factor)
+    assert np.array_equal(fr.solve(rhs), xu)

@@ -31,11 +31,15 @@ def test_kat_id(golden):
     assert np.array_equal(T, golden["kat_cluster_T"])
 
 
-@pytest.mark.parametrize("name,builder", [("cfg1_", configs.cfg1), ("mini_", configs.mini_holes)])
-def test_oracle_matches_reference(golden, name, builder):
+@pytest.mark.parametrize("name,builder,pde", [("cfg1_", configs.cfg1, O.STOKES),
+                                              ("mini_", configs.mini_holes, O.STOKES),
+                                              ("lap_", configs.cfg1, O.LAPLACE),
+                                              ("lapm_", configs.mini_holes, O.LAPLACE)])
+def test_oracle_matches_reference(golden, name, builder, pde):
     wl = builder()
     rec = {}
-    f = O.factor_full(wl.boundary, wl.leaf_cap, wl.tol, wl.proxy_count, wl.proxy_factor, record=rec)
+    f = O.factor_full(wl.boundary, wl.leaf_cap, wl.tol, wl.proxy_count, wl.proxy_factor, record=rec,
+                      pde=pde)
     ref = _boxes(golden, name)
     assert set(ref) == set(f.boxes)
     for k, r in ref.items():
@@ -60,9 +64,27 @@ def test_oracle_matches_reference(golden, name, builder):
     x = f.solve(golden[name + "rhs"])
     xr = golden[name + "x"]
     assert np.linalg.norm(x - xr) / np.linalg.norm(xr) < 1e-13
-    y = f.apply(golden[name + "apply_in"])
-    yr = golden[name + "apply_out"]
-    assert np.linalg.norm(y - yr) / np.linalg.norm(yr) < 1e-13
+    if name + "apply_in" in golden.files:
+        y = f.apply(golden[name + "apply_in"])
+        yr = golden[name + "apply_out"]
+        assert np.linalg.norm(y - yr) / np.linalg.norm(yr) < 1e-13
+
+
+def test_oracle_laplace_update_and_interior(golden):
+    """Laplace-Neumann: hole-move update on the 3-hole geometry and interior
+    evaluation u = -S mu against the reference (kernels.py:171-198)."""
+    from paper_2001_11619_b200.geometry import MoveHole, apply_perturbation
+    wl = configs.mini_holes()
+    f = O.factor_full(wl.boundary, wl.leaf_cap, wl.tol, wl.proxy_count, wl.proxy_factor, pde=O.LAPLACE)
+    nb, rep = apply_perturbation(wl.boundary, [MoveHole(1, translation=(-0.08, 0.06))])
+    fu = O.update(f, nb, rep)
+    assert fu.stats["n_dirty"] == int(golden["lapm_upd_ndirty"])
+    x = fu.solve(golden["lapm_rhs"])
+    assert np.linalg.norm(x - golden["lapm_upd_x"]) / np.linalg.norm(golden["lapm_upd_x"]) < 1e-13
+    wl = configs.cfg1()
+    u = O.evaluate_interior(wl.boundary, golden["lap_x"], golden["lap_targets"], pde=O.LAPLACE)
+    ref = golden["lap_interior"]
+    assert np.max(np.abs(u - ref)) <= 1e-12 * np.max(np.abs(ref))
 
 
 def test_oracle_update_dirty_set(golden):
