@@ -381,6 +381,12 @@ int skb_engine_set_lead(int64_t handle, int64_t lead);
 /* stop after the current level and join the engine thread */
 int skb_engine_stop(int64_t handle);
 int skb_engine_free(int64_t handle, void* stream);
+/* Factor storage from a process-wide stream-ordered pool (no implicit device
+ * synchronisation when it grows); freed stream-ordered.                      */
+int skb_dev_alloc(int64_t bytes, void* stream, uint64_t* out);
+int skb_dev_free(uint64_t ptr, void* stream);
+/* Synchronous device -> host copy of raw bytes (factor inspection). */
+int skb_d2h(void* host, const void* dev, int64_t bytes);
 /* Debug (SKB_ENGINE_SNAP=<level>): host copy of the snapshot `which` of that
  * level's ID stacks (0 after assembly, 1 after pre-reduction, 2 after QRCP);
  * returns the element count, -1 when no snapshot was taken.                  */

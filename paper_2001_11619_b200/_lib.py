@@ -86,6 +86,9 @@ SIGNATURES = {
     "skb_engine_set_lead": [_i64, _i64],
     "skb_engine_free": [_i64, _vp],
     "skb_debug_snap": [_i32, _vp, _i64],
+    "skb_d2h": [_vp, _vp, _i64],
+    "skb_dev_alloc": [_i64, _vp, _vp],
+    "skb_dev_free": [ctypes.c_uint64, _vp],
     # native host runtime (host arrays only, no device)
     "skb_host_far_lists": [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _f64,
                            _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _i32],

@@ -289,6 +289,51 @@ static std::vector<std::vector<void*>> g_sessions;
 
 extern "C" int skb_version(void) { return 1; }
 
+// Factor storage (per-level factor slabs, sweep stashes): a process-wide
+// stream-ordered pool that never shrinks.  Torch's caching allocator falls
+// back to cudaMalloc -- which waits for the device -- whenever an update's
+// slab sizes do not fit its cached blocks (10-25 ms stalls in update chains).
+static cudaMemPool_t factor_pool() {
+  static cudaMemPool_t pool = nullptr;
+  static std::mutex m;
+  std::lock_guard<std::mutex> lk(m);
+  if (!pool) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) return nullptr;
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  return pool;
+}
+
+extern "C" int skb_dev_alloc(int64_t bytes, void* stream, uint64_t* out) {
+  cudaMemPool_t pool = factor_pool();
+  if (!pool) return 11;
+  void* p = nullptr;
+  SKB_RET(cudaMallocFromPoolAsync(&p, (size_t)(bytes > 0 ? bytes : 8), pool, (cudaStream_t)stream));
+  *out = (uint64_t)p;
+  return 0;
+}
+
+extern "C" int skb_dev_free(uint64_t ptr, void* stream) {
+  if (!ptr) return 0;
+  SKB_RET(cudaFreeAsync((void*)ptr, (cudaStream_t)stream));
+  return 0;
+}
+
+// Synchronous device -> host copy of raw bytes (factor inspection: BoxFactors.lu pivots).
+extern "C" int skb_d2h(void* host, const void* dev, int64_t bytes) {
+  if (bytes <= 0) return 0;
+  SKB_RET(cudaMemcpy(host, dev, (size_t)bytes, cudaMemcpyDeviceToHost));
+  return 0;
+}
+
 extern "C" int skb_capture_begin(int64_t arena_bytes) {
   auto& C = skb::capture();
   C.pinned.clear();

@@ -357,6 +357,40 @@ def _native_far_lists(ctx, idx, store):
         cap = int(need[0]) + 1024
 
 
+class _DevSlab:
+    """Device storage from the library's factor pool (skb_dev_alloc: stream
+    ordered, never a synchronising cudaMalloc).  Frees are deferred to the
+    next factor / update / solve entry (never inside a graph capture) and
+    ordered after the level, sweep and current streams."""
+    _pending = []
+
+    def __init__(self, nbytes: int, stream):
+        out = np.zeros(1, np.uint64)
+        call("skb_dev_alloc", int(max(nbytes, 8)), stream.cuda_stream, out)
+        self.ptr = int(out[0])
+        self.nbytes = int(nbytes)
+
+    def data_ptr(self) -> int:
+        return self.ptr
+
+    def __del__(self):
+        if self.ptr:
+            pend = _DevSlab._pending if _DevSlab is not None else None
+            if pend is not None:            # (module teardown at exit: the pool goes with the process)
+                pend.append(self.ptr)
+            self.ptr = 0
+
+    @classmethod
+    def flush(cls):
+        if not cls._pending:
+            return
+        cur = torch.cuda.current_stream()
+        for st in _LEVEL_STREAM:
+            cur.wait_stream(st)
+        while cls._pending:
+            call("skb_dev_free", ctypes.c_uint64(cls._pending.pop()), cur.cuda_stream)
+
+
 class _CaptureArena:
     """Owns a library capture session (the pinned descriptor arena a captured
     graph replays from).  Released lazily, outside any capture: a destructor
@@ -367,7 +401,8 @@ class _CaptureArena:
         self.sess = int(sess)
 
     def __del__(self):
-        _CaptureArena._pending.append(self.sess)
+        if _CaptureArena is not None:
+            _CaptureArena._pending.append(self.sess)
 
     @classmethod
     def flush(cls):
@@ -468,7 +503,8 @@ class BoxBatch:
         self.info = np.full(n, -1, np.int64)
         self.ptr = {f: np.zeros(n, np.uint64) for f in self.FIELDS}
         self.ipiv = np.zeros(n, np.uint64)
-        self.slabs = []
+        self.slabs = []                        # device allocations holding the boxes' factors
+        self.slab_of = np.full(n, -1, np.int64)   # index into slabs per box
 
     @property
     def r(self):
@@ -521,8 +557,19 @@ class BoxBatch:
         if getattr(self, "_deferred", None) is None:
             self._deferred = []
         self._deferred.append((sel, other, osel))
-        have = {id(x) for x in self.slabs}
-        self.slabs.extend(x for x in other.slabs if id(x) not in have)
+        # keep only the slabs that hold a box of this batch (an update chain must not
+        # keep every superseded slab of the level alive)
+        pos = {id(x): i for i, x in enumerate(self.slabs)}
+        so = other.slab_of[osel]
+        lut = np.full(max(len(other.slabs), 1), -1, np.int64)
+        for u in np.unique(so[so >= 0]):
+            sl = other.slabs[u]
+            i = pos.get(id(sl))
+            if i is None:
+                i = pos[id(sl)] = len(self.slabs)
+                self.slabs.append(sl)
+            lut[u] = i
+        self.slab_of[sel] = np.where(so >= 0, lut[np.maximum(so, 0)], -1)
 
 
 class LevelFactors:
@@ -784,17 +831,17 @@ class _Ctx:
                 i_ = np.arange(st, dtype=float)
                 fq += 2.0 * mm * nn + float((4.0 * (mm - i_) * (nn - i_ - 1)).sum())
             _lib.prof_add("qrcp", fq, 8.0 * float((h["m_q"] * nB).sum()))
-        # factor storage (one slab), allocated for the level stream that fills it
-        dev = _dev()
-        with torch.cuda.stream(self.sstream):
-            sz = np.stack([k * r, r * r, r * r, k * r, r * k, k * k], axis=1)
-            tot = sz.sum(axis=1)
-            boff = np.zeros(B + 1, np.int64)
-            np.cumsum(tot, out=boff[1:])
-            # factors (f64) followed by the LU pivots (i32) in ONE allocation
-            nf = max(int(boff[-1]), 1)
-            slab = torch.empty(8 * nf + 4 * max(int(r.sum()), 1), dtype=torch.uint8, device=dev)
+        # factor storage (one slab from the factor pool), ordered on the level
+        # stream that fills it
+        sz = np.stack([k * r, r * r, r * r, k * r, r * k, k * k], axis=1)
+        tot = sz.sum(axis=1)
+        boff = np.zeros(B + 1, np.int64)
+        np.cumsum(tot, out=boff[1:])
+        # factors (f64) followed by the LU pivots (i32) in ONE allocation
+        nf = max(int(boff[-1]), 1)
+        slab = _DevSlab(8 * nf + 4 * max(int(r.sum()), 1), self.sstream)
         bt.slabs.append(slab)
+        bt.slab_of[:] = len(bt.slabs) - 1
         sb = _addr(slab)
         fo = boff[:-1].copy()
         for fi, f in enumerate(BoxBatch.FIELDS):
@@ -913,6 +960,34 @@ def _fetch(addr, rows, cols):
     return t.cpu().numpy()
 
 
+def _fetch_i32(addr, n):
+    out = np.empty(max(int(n), 1), np.int32)
+    if n:
+        call("skb_d2h", out, ctypes.c_void_p(int(addr)), 4 * int(n))
+    return out[:int(n)]
+
+
+class LUView:
+    """Host copy of a box's X_RR LU factors (reference BoxFactors.lu, a PLU of
+    dense.py:106-135): ``lu`` (unit-lower L and U packed, row-major), 0-based
+    LAPACK pivots ``piv`` and ``pivot_ratio`` = min |u_ii| / max |u_ii|."""
+
+    def __init__(self, lu, piv):
+        self.lu, self.piv = lu, piv
+        d = np.abs(np.diag(lu))
+        self.pivot_ratio = float(d.min() / d.max()) if len(d) and d.max() > 0 else 1.0
+
+    @property
+    def n(self):
+        return self.lu.shape[0]
+
+    def solve(self, B):
+        """X_RR^-1 B on the host copies (inspection only; the factorization's
+        own solves run on the device)."""
+        import scipy.linalg as sla
+        return sla.lu_solve((self.lu, self.piv), np.asarray(B, float))
+
+
 class _FactorsView:
     """Lazy mapping key -> BoxFactors (reference Factorization.factors)."""
 
@@ -956,6 +1031,7 @@ class _FactorsView:
             "X_sr": lambda: _fetch(P["Xsr"][bi], k, r),
             "X_rs_div": lambda: _fetch(P["Xrsdiv"][bi], r, k),
             "Xss_mod": lambda: _fetch(P["Xss"][bi], k, k),
+            "lu": lambda: LUView(_fetch(P["LU"][bi], r, r), _fetch_i32(L.ipiv[bi], r)),
         }
         return BoxFactors(tuple(key), dofs, perm[:k], perm[k:], mats)
 
@@ -1200,6 +1276,7 @@ class Factorization:
         r = rhs if is_t else np.asarray(rhs, float)
         if r.shape[0] != self.dim:
             raise ValueError(f"dimension mismatch: got {r.shape[0]}, need {self.dim}")
+        _DevSlab.flush()
         vec = r.ndim == 1
         if is_t:
             x = r.to(device=_dev(), dtype=torch.float64).reshape(self.dim, -1).clone()
@@ -1419,7 +1496,7 @@ def _stash_alloc(L: "LevelFactors", q: int):
     st_sp = np.full(len(k), base_sp, np.int64)
     np.cumsum(sp[:-1], out=st_sp[1:])
     st_sp[1:] += base_sp
-    L.stash = torch.empty(max(base_sp + int(sp.sum()), 1), dtype=torch.float64, device=_dev())
+    L.stash = _DevSlab(8 * max(base_sp + int(sp.sum()), 1), torch.cuda.current_stream())
     L.st_us, L.st_ps, L.st_sp = st_us, st_ps, st_sp
 
 
@@ -1505,7 +1582,7 @@ class _AugPipeUpdate(_AugPipe):
         old_sp = np.zeros(B, np.uint64)
         cl = np.flatnonzero(~dirty)
         if len(cl):
-            Lo, pos = L.batch.clean_old
+            Lo, pos = L.batch.__dict__.pop("clean_old")     # drop the link to the old level
             base = _addr(Lo.stash)
             old_us[cl] = base + 8 * Lo.st_us[pos]
             old_ps[cl] = base + 8 * Lo.st_ps[pos]
@@ -1989,6 +2066,7 @@ def factor(spec, b, t: Tree, tol: float, workers: int = 1,
     if propagate_zeros:
         raise NotImplementedError("propagate_zeros is a sequential CPU validation mode")
     torch.cuda.synchronize()
+    _DevSlab.flush()
     t0 = time.perf_counter()
     with _ht("ctx"):
         ctx = _Ctx(spec, b, t, tol, proxy_count, proxy_factor)
@@ -2020,6 +2098,7 @@ def factor(spec, b, t: Tree, tol: float, workers: int = 1,
 def update(fct: Factorization, b_new, report, workers: int = 1) -> Factorization:
     """Refactor only what a local perturbation invalidated (reference skel.py:456-514)."""
     torch.cuda.synchronize()
+    _DevSlab.flush()
     t0 = time.perf_counter()
     try:
         with _ht("U.refit"):
@@ -2048,6 +2127,10 @@ def update(fct: Factorization, b_new, report, workers: int = 1) -> Factorization
             levels, store, n_recomp = _run_levels(ctx, reuse=old, dirty=dmask)
         rd, E_root, top, ipiv, UH, PsiV, UH_div, q, ratio = _finish_top(ctx, levels, store, ctx.pipe)
     torch.cuda.synchronize()
+    ctx.upd_old = None                                  # no chain of old factorizations
+    ctx.pipe = None
+    for L in levels:
+        L.batch.__dict__.pop("clean_old", None)
     stats = {"k_per_level": {L.lev: int(L.k.max(initial=0)) for L in levels},
              "root_size": len(rd), "top_pivot_ratio": ratio}
     nf = Factorization(fct.spec, b_new, t_new, fct.tol, fct.proxy_count, fct.proxy_factor, levels,

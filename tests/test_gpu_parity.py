@@ -385,3 +385,17 @@ def test_laplace_update_equals_refactor(golden):
     t2 = build_tree(nb.positions, wl.leaf_cap, root_box=(f.tree.root_center, f.tree.root_half_width))
     fr = factor(spec, nb, t2, wl.tol, proxy_count=wl.proxy_count, proxy_factor=wl.proxy_factor)
     assert np.array_equal(fr.solve(rhs), xu)
+
+
+def test_box_factors_lu_view():
+    """BoxFactors.lu (reference skel.py:69): host copy of the X_RR LU factors
+    and pivots; lu.solve(X_RR) reproduces the identity."""
+    wl = configs.cfg1()
+    f = _factor(wl)
+    k = [k for k in f.factors if len(f.factors[k].R_loc) > 20][0]
+    bf = f.factors[k]
+    lu = bf.lu
+    X = bf.X_rr
+    assert lu.n == X.shape[0] and lu.piv.shape == (X.shape[0],)
+    assert np.abs(lu.solve(X) - np.eye(lu.n)).max() < 1e-10
+    assert 0 < lu.pivot_ratio <= 1
