@@ -644,9 +644,10 @@ int getrf_batched(int64_t nbox, const SkbMat* a, const int64_t* ipiv, int32_t* i
     if (!one_cta(n)) return (int64_t)LB;
     return (size_t)n * (LB + 1) * sizeof(double) <= kPanelSmem ? (int64_t)LB : (int64_t)LB / 2;
   };
-  auto csize = [&](int64_t n) {       // <= 100 KB of panel rows per CTA
+  static const int64_t lcmax = getenv("SKB_LU_CMAX") ? atoll(getenv("SKB_LU_CMAX")) : 16;
+  auto csize = [&](int64_t n) {       // <= 100 KB of panel rows per CTA (200 KB at the cap)
     int64_t C = 2;
-    while (C < 16 && (size_t)((n + C - 1) / C) * (LB + 1) * sizeof(double) > 100 * 1024) C *= 2;
+    while (C < lcmax && (size_t)((n + C - 1) / C) * (LB + 1) * sizeof(double) > 100 * 1024) C *= 2;
     return C;
   };
   int64_t rounds = 0;

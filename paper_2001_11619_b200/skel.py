@@ -90,8 +90,15 @@ class SystemSpec:
 # ---------------------------------------------------------------------------
 # small helpers
 # ---------------------------------------------------------------------------
+_DEV_INDEX = []
+
+
 def _stream():
-    return torch.cuda.current_stream().cuda_stream
+    """Raw handle of the current stream (torch's Python-level current_stream()
+    costs ~20 us per call; the level loops ask for it hundreds of times)."""
+    if not _DEV_INDEX:
+        _DEV_INDEX.append(torch.cuda.current_device())
+    return torch._C._cuda_getCurrentRawStream(_DEV_INDEX[0])
 
 
 _LEVEL_STREAM = []
@@ -1719,17 +1726,17 @@ class _Engine:
             self.lib.skb_engine_set_update(self.h, todo.ctypes.data, coff.ctypes.data,
                                            cskel.ctypes.data)
             self.lib.skb_engine_go(self.h)
-        # Run-ahead of the engine over the enqueued Schur stages: the engine
-        # starts level L once level L+1's Schur stage is enqueued (lead 0).
-        # Deeper run-ahead (SKB_ENGINE_LEAD=n, -1 unbounded) is ~5 % faster in
-        # the median on cfg3 but lets the compression chain's cluster kernels
-        # stall behind two levels of Schur / sweep work: 0.3-1 s steps in ~1 of
-        # 40 factorizations (scripts/outliers.py).  Levels without boxes to
-        # compress count as acknowledged (engine.cu).
-        # Updates recompress a few boxes per level: no heavy Schur work to
-        # starve behind, so they run ahead unbounded (the Python level loop is
-        # their critical path).
-        lead = int(os.environ.get("SKB_ENGINE_LEAD", "0" if update is None else "-1"))
+        # Run-ahead of the engine over the enqueued Schur stages.  On trees
+        # with heavy levels (> 512 boxes, cfg3) the engine starts level L only
+        # once level L+1's Schur stage is enqueued (lead 0): deeper run-ahead
+        # is ~5 % faster in the median but lets the compression chain's
+        # cluster kernels starve behind two levels of Schur / sweep work
+        # (0.3-1 s steps in ~1 of 40 factorizations, scripts/outliers.py).
+        # Lighter trees (cfg2: 26 vs 31 ms) and updates (a few boxes per level)
+        # run ahead unbounded.  SKB_ENGINE_LEAD=n overrides.  Levels without
+        # boxes to compress count as acknowledged (engine.cu).
+        heavy = update is None and int(np.diff(t.level_start).max(initial=0)) > 512
+        lead = int(os.environ.get("SKB_ENGINE_LEAD", "0" if heavy else "-1"))
         if lead >= 0:
             self.lib.skb_engine_set_lead(self.h, lead)
         self.sizes = np.zeros(8, np.int64)
@@ -1737,8 +1744,10 @@ class _Engine:
 
     @staticmethod
     def _arr(addr, n, dt):
-        return np.ctypeslib.as_array((ctypes.c_char * (n * np.dtype(dt).itemsize)).from_address(
-            int(addr))).view(dt).copy() if n else np.zeros(0, dt)
+        if not n:
+            return np.zeros(0, dt)
+        nb = n * np.dtype(dt).itemsize
+        return np.frombuffer((ctypes.c_char * nb).from_address(int(addr)), dtype=dt).copy()
 
     def wait(self, L) -> dict:
         with _ht("E.wait"):

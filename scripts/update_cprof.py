@@ -17,4 +17,4 @@ for h, d, nb, rp in seq[3:]:
 torch.cuda.synchronize()
 pr.disable()
 st = pstats.Stats(pr)
-st.sort_stats("tottime").print_stats(28)
+st.sort_stats("cumtime").print_stats(45)
