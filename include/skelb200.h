@@ -370,6 +370,35 @@ int skb_engine_wait(int64_t handle, int64_t L, int64_t* sizes, int64_t* ptrs);
 int skb_engine_set_update(int64_t handle, const uint8_t* todo, const int64_t* clean_off,
                           const int64_t* clean_skel);
 int skb_engine_go(int64_t handle);
+/* Update mode for the native level driver: the clean boxes' skeletons are read
+ * from the previous factorization's level table, int64 [levels][21], row =
+ * {B, code (ix * 2^level + iy, ascending), act_off, act, perm (int32), k,
+ * T, X_rr, LU, X_sr, X_rs_div, Xss (uint64 per box), ipiv, info, ratio, stash
+ * (device address), st_us, st_ps, st_sp, gap, steps}; host arrays of the caller. */
+int skb_engine_set_update_table(int64_t handle, const uint8_t* todo, const int64_t* old_table);
+/* Native level driver: the consumer side of the level loop (run_level
+ * skel.py:340-361, compress_box (c) skel.py:316-338, the _finish_top sweep
+ * skel.py:384-396) on the calling thread.  Per level: wait for the engine,
+ * X_RR pivot check of the level below (100 = a box must migrate, the caller
+ * re-runs on its Python path), merge with the clean boxes of the previous
+ * factorization (101 = no twin, 102 = active set changed), factor storage,
+ * skb_level_schur, acknowledge, augmentation sweep of the level below
+ * (skb_level_aug, or skb_level_aug_update when cfg[18]), level lists on the
+ * device.  cfg (int64 x 24) = {level stream, sweep stream, curvature (device),
+ * q, npairs, pair_box, pair_curve ((box, curve) membership, sorted by box),
+ * parent, UH, PsiV, UH_div, schur (device), update, dirty mask (uint8 per box),
+ * nqc, qc (host), qmask (device), previous level table, incremental sweep,
+ * xss (uint64 per box, host, filled)}.                                        */
+int skb_drv_run(int64_t engine, const int64_t* cfg, double pivot_ratio_floor, int64_t* handle);
+/* Arrays of one level (valid until skb_drv_free): sizes (int64 x 24) = {B, na,
+ * nnew, nsd, nrd, ncols, slab, slab bytes, stash, stash bytes, desc, desc bytes,
+ * offsets of {sd_off, sd, rd_off, rd, c_off, c} in desc (int64 units), total
+ * h2d bytes, total d2h bytes}; ptrs (int64 x 32) = {idx, code, act_off, act, perm
+ * (int32), k, steps, gap, info, ratio, clean_pos, T, X_rr, LU, X_sr, X_rs_div,
+ * Xss, ipiv, sd_off, sd, rd_off, rd, cols_off, cols, st_us, st_ps, st_sp,
+ * new_pos}.  The device allocations (skb_dev_alloc pool) become the caller's. */
+int skb_drv_level(int64_t handle, int64_t lev, int64_t* sizes, int64_t* ptrs);
+int skb_drv_free(int64_t handle);
 /* stream waits for level L's compression */
 int skb_engine_stream_wait(int64_t handle, int64_t L, void* stream);
 /* free level L's device buffers, stream-ordered on stream */

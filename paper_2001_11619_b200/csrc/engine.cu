@@ -96,7 +96,47 @@ struct Engine {
   const uint8_t* todo = nullptr;
   const int64_t* clean_off = nullptr;
   const int64_t* clean_skel = nullptr;
+  // ... or the previous factorization's level table (skb_engine_set_update_table)
+  const int64_t* old_table = nullptr;
 };
+
+// One level of the previous factorization (update): arrays owned by the
+// caller, addressed through a table of int64 [depth + 1][O_NF] (row = level,
+// all zero when the level did not exist).  code = ix * 2^level + iy, ascending.
+enum { O_B = 0, O_CODE, O_ACT_OFF, O_ACT, O_PERM, O_K, O_PTR0, O_IPIV = O_PTR0 + 6, O_INFO, O_RATIO,
+       O_STASH, O_ST_US, O_ST_PS, O_ST_SP, O_GAP, O_STEPS, O_NF };
+struct OldLevel {
+  int64_t B = 0;
+  const int64_t *code, *act_off, *act, *k, *info, *st_us, *st_ps, *st_sp, *steps;
+  const int32_t* perm;
+  const uint64_t* ptr[6];
+  const uint64_t* ipiv;
+  const double *ratio, *gap;
+  uint64_t stash;
+};
+inline OldLevel old_level(const int64_t* table, int64_t lev) {
+  const int64_t* t = table + lev * O_NF;
+  OldLevel O;
+  O.B = t[O_B];
+  O.code = (const int64_t*)t[O_CODE]; O.act_off = (const int64_t*)t[O_ACT_OFF];
+  O.act = (const int64_t*)t[O_ACT]; O.perm = (const int32_t*)t[O_PERM]; O.k = (const int64_t*)t[O_K];
+  for (int f = 0; f < 6; ++f) O.ptr[f] = (const uint64_t*)t[O_PTR0 + f];
+  O.ipiv = (const uint64_t*)t[O_IPIV]; O.info = (const int64_t*)t[O_INFO];
+  O.ratio = (const double*)t[O_RATIO]; O.stash = (uint64_t)t[O_STASH];
+  O.st_us = (const int64_t*)t[O_ST_US]; O.st_ps = (const int64_t*)t[O_ST_PS];
+  O.st_sp = (const int64_t*)t[O_ST_SP]; O.gap = (const double*)t[O_GAP];
+  O.steps = (const int64_t*)t[O_STEPS];
+  return O;
+}
+inline int64_t find_code(const OldLevel& O, int64_t code) {
+  int64_t lo = 0, hi = O.B;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (O.code[mid] < code) lo = mid + 1;
+    else hi = mid;
+  }
+  return (lo < O.B && O.code[lo] == code) ? lo : -1;
+}
 
 // Process-wide pinned staging buffer for the per-level upload (kept across
 // factorizations; one engine at a time, the others stage their own).
@@ -244,6 +284,14 @@ int snap_copy(int which, const double* src, int64_t n, cudaStream_t s) {
   return 0;
 }
 
+// Blocks until the engine may enqueue level L's kernels (run-ahead control,
+// skb_engine_ack / skb_engine_set_lead); false when the engine was stopped.
+bool launch_gate(Engine& E, int64_t L) {
+  std::unique_lock<std::mutex> lk(E.m);
+  E.cv.wait(lk, [&] { return E.stop.load() || E.lead < 0 || E.acked <= L + 1 + E.lead || L + 1 + E.lead > E.depth; });
+  return !E.stop.load();
+}
+
 int run_level(Engine& E, int64_t L, LevelOut& R) {
   ETimer tm;
   const int64_t b0 = E.level_start[L], nall = E.level_start[L + 1] - b0;
@@ -275,7 +323,23 @@ int run_level(Engine& E, int64_t L, LevelOut& R) {
   }
   tm.tick("internal");
   // clean boxes (update): skeletons carried over from the previous factorization
-  if (E.todo)
+  if (E.todo && E.old_table) {
+    const OldLevel O = old_level(E.old_table, L);
+    const int64_t side = (int64_t)1 << L;
+    std::vector<int64_t> sk;
+    for (int64_t i = b0; i < b0 + nall; ++i) {
+      if (E.todo[i]) continue;
+      const int64_t pos = O.B ? find_code(O, E.ix[i] * side + E.iy[i]) : -1;
+      if (pos < 0) return 20;               // clean box without a twin: the caller re-runs
+      const int64_t a0 = O.act_off[pos], nk = O.k[pos];
+      sk.resize(nk);
+      for (int64_t j = 0; j < nk; ++j) sk[j] = O.act[a0 + O.perm[a0 + j]];
+      const int64_t o = append(E, sk.data(), nk);
+      if (o < 0) return 7;
+      E.s_start[i] = o;
+      E.s_len[i] = nk;
+    }
+  } else if (E.todo) {
     for (int64_t i = b0; i < b0 + nall; ++i) {
       if (E.todo[i]) continue;
       const int64_t n0 = E.clean_off[i], nk = E.clean_off[i + 1] - n0;
@@ -284,6 +348,7 @@ int run_level(Engine& E, int64_t L, LevelOut& R) {
       E.s_start[i] = o;
       E.s_len[i] = nk;
     }
+  }
   if (B == 0) return 0;
   R.act_off.assign(B + 1, 0);
   for (int64_t b = 0; b < B; ++b) R.act_off[b + 1] = R.act_off[b] + E.a_len[idx[b]];
@@ -380,9 +445,13 @@ int run_level(Engine& E, int64_t L, LevelOut& R) {
     maxitems = std::max(maxitems, nF + P + 1);
   }
   cudaStream_t s = E.s;
-  SKB_RET(malloc_async((void**)&R.stack, sizeof(double) * std::max<int64_t>(so, 1), s));
   const int64_t npk = o_f + nfar;
   tm.tick("pack");
+  // the host side of the level (active sets, far lists, proxy rings, packing)
+  // is done; only the kernel launches wait for the run-ahead gate
+  if (!launch_gate(E, L)) return -1000;
+  tm.tick("gate");
+  SKB_RET(malloc_async((void**)&R.stack, sizeof(double) * std::max<int64_t>(so, 1), s));
   SKB_RET(malloc_async((void**)&R.dup, sizeof(int64_t) * npk, s));
   SKB_RET(cudaMemcpyAsync(R.dup, pk, sizeof(int64_t) * npk, cudaMemcpyHostToDevice, s));
   tm.tick("upload");
@@ -480,10 +549,6 @@ void engine_main(Engine* E) {
   }
   for (int64_t L = E->depth; L >= E->lev_lo; --L) {
     LevelOut& R = E->out[L];
-    if (E->lead >= 0) {
-      std::unique_lock<std::mutex> lk(E->m);
-      E->cv.wait(lk, [&] { return E->stop.load() || E->acked <= L + 1 + E->lead || L + 1 + E->lead > E->depth; });
-    }
     int rc = 0;
     if (E->stop.load()) rc = -1000;
     else rc = run_level(*E, L, R);
@@ -717,6 +782,551 @@ int skb_engine_free(int64_t handle, void* stream) {
     cudaFreeHost(E->pack);
   }
   delete E;
+  return 0;
+}
+
+}  // extern "C"
+
+// ===========================================================================
+// Native level driver: the consumer side of the level loop (reference
+// run_level / compress_box (c) / _finish_top sweep, skel.py:316-361, 384-396)
+// on the calling thread, one C call for all levels:
+//
+//   wait for the engine's level -> X_RR pivot check of the level below
+//   (migration rule skel.py:317-330: reported, the caller re-runs on its slow
+//   path) -> merge with the previous factorization's clean boxes (update,
+//   skel.py:342-353) -> factor storage layout -> Schur stage (skb_level_schur)
+//   -> acknowledge -> augmentation sweep of the level below -> skeleton /
+//   redundant / hole-column lists of the level on the device.
+//
+// The caller (skel.py) only wraps the resulting arrays afterwards.
+// ===========================================================================
+extern "C" int skb_level_schur(int64_t nbox, const int64_t* nB, const int64_t* k,
+                               const int64_t* act_off, const double* pos, const double* nrm,
+                               const double* w, const double* kappa, const int64_t* act_off_dev,
+                               const int64_t* act_dev, const int32_t* perm_dev, const int64_t* A,
+                               const int64_t* lda, const int64_t* child_off,
+                               const uint64_t* child_xss, const uint64_t* T, const uint64_t* Xrr,
+                               const uint64_t* LU, const uint64_t* Xsr, const uint64_t* Xrsdiv,
+                               const uint64_t* Xss, const uint64_t* ipiv, int32_t* info_dev,
+                               double* ratio_dev, int32_t pde, void* stream);
+extern "C" int skb_level_aug(int64_t nbox, const int64_t* k, const int64_t* r, int64_t q,
+                             const int64_t* cols_off, const int64_t* cols, const int64_t* sd_off,
+                             const int64_t* sd, const int64_t* rd_off, const int64_t* rd,
+                             const int64_t* c_off, const int64_t* c, const uint64_t* T,
+                             const uint64_t* LU, const uint64_t* Xsr, const uint64_t* Xrsdiv,
+                             const uint64_t* ipiv, double* UH, double* PsiV, double* UH_div,
+                             double* schur, double* stash, const int64_t* st_us,
+                             const int64_t* st_ps, const int64_t* st_sp, int32_t acc, void* stream);
+extern "C" int skb_level_aug_update(int64_t nbox, const int64_t* k, const int64_t* r, int64_t q,
+                                    const int64_t* cols_off, const int64_t* cols,
+                                    const int64_t* sd_off, const int64_t* sd, const int64_t* rd_off,
+                                    const int64_t* rd, const uint8_t* dirty, const uint8_t* parent_dirty,
+                                    const uint64_t* T, const uint64_t* LU, const uint64_t* Xsr,
+                                    const uint64_t* Xrsdiv, const uint64_t* ipiv, const uint64_t* old_us,
+                                    const uint64_t* old_ps, const uint64_t* old_sp, int64_t nqc,
+                                    const int64_t* qc, const uint8_t* qmask_dev, double* UH, double* PsiV,
+                                    double* UH_div, double* schur, double* stash, const int64_t* st_us,
+                                    const int64_t* st_ps, const int64_t* st_sp, void* stream);
+extern "C" int skb_dev_alloc(int64_t bytes, void* stream, uint64_t* out);
+extern "C" int skb_prof_add(int32_t fam, double flops, double bytes);
+
+namespace {
+
+struct DrvLevel {
+  int64_t lev = 0, B = 0, nnew = 0;
+  std::vector<int64_t> idx, code, act_off, act, k, steps, clean_pos, info, new_pos;
+  std::vector<int32_t> perm;
+  std::vector<double> gap, ratio;
+  std::vector<uint64_t> ptr[6], ipiv;
+  std::vector<int64_t> sd_off, sd, rd_off, rd, cols_off, cols, st_us, st_ps, st_sp;
+  uint64_t slab = 0, stash = 0, desc = 0;
+  int64_t slab_bytes = 0, stash_bytes = 0, desc_bytes = 0;
+  int64_t o_desc[6] = {0, 0, 0, 0, 0, 0};     // element offsets: sd_off | sd | rd_off | rd | c_off | c
+  cudaEvent_t ready = nullptr;                // level stream: factors and lists of the level final
+  cudaEvent_t pev = nullptr;                  // X_RR pivot info of the new boxes landed
+  char* pin = nullptr;                        // pinned: ratio (f64 x nnew) | info (i32 x nnew)
+  bool resolved = true, adopted = false, used = false;
+};
+
+struct DrvCfg {
+  cudaStream_t S, AS;
+  const double* kap;
+  int64_t q;
+  int64_t npairs;
+  const int64_t *pair_box, *pair_curve, *parent;
+  double *UH, *PsiV, *UH_div, *schur;
+  int64_t update;
+  const uint8_t* dmask;
+  int64_t nqc;
+  const int64_t* qc;
+  const uint8_t* qmask_dev;
+  const int64_t* old_table;
+  int64_t inc;
+  uint64_t* xss;
+  double floor;
+};
+
+struct Driver {
+  Engine* E = nullptr;
+  DrvCfg c;
+  std::vector<DrvLevel> lv;
+  DrvLevel* prev = nullptr;
+  char* pinned = nullptr;
+  size_t pinned_cap = 0, pinned_used = 0;
+  bool shared_pinned = false;
+  int64_t h2d = 0, d2h = 0;
+  int64_t fail_level = -1;
+};
+
+// process-wide pinned landing buffer of the pivot info (one driver at a time)
+struct DrvPinned {
+  char* p = nullptr;
+  size_t cap = 0;
+  bool busy = false;
+};
+DrvPinned& g_drv_pinned() {
+  static DrvPinned b;
+  return b;
+}
+
+// X_RR pivot info of a level's new boxes: wait for the copy, apply the
+// migration rule's trigger (skel.py:317-330).  100 = a box must migrate.
+int drv_resolve(Driver& D, DrvLevel& L) {
+  if (L.resolved) return 0;
+  SKB_RET(cudaEventSynchronize(L.pev));
+  const double* ratio = (const double*)L.pin;
+  const int32_t* info = (const int32_t*)(L.pin + 8 * L.nnew);
+  bool bad = false;
+  for (int64_t j = 0; j < L.nnew; ++j) {
+    const int64_t p = L.new_pos[j];
+    L.ratio[p] = ratio[j];
+    L.info[p] = info[j];
+    const int64_t nB = L.act_off[p + 1] - L.act_off[p];
+    if ((info[j] >= 0 || ratio[j] < D.c.floor) && L.k[p] < nB) bad = true;
+  }
+  L.resolved = true;
+  return bad ? 100 : 0;
+}
+
+int drv_sweep(Driver& D, DrvLevel& L) {
+  const DrvCfg& c = D.c;
+  const int64_t B = L.B, q = c.q;
+  if (q <= 0 || B <= 0) return 0;
+  SKB_RET(cudaStreamWaitEvent(c.AS, L.ready, 0));
+  // per-box storage of the sweep results (outgoing UH_S | PsiV_S | Schur part)
+  std::vector<int64_t> r(B);
+  L.st_us.assign(B, 0); L.st_ps.assign(B, 0); L.st_sp.assign(B, 0);
+  int64_t a = 0;
+  for (int64_t b = 0; b < B; ++b) { L.st_us[b] = a; a += L.k[b] * q; }
+  for (int64_t b = 0; b < B; ++b) { L.st_ps[b] = a; a += L.k[b] * (L.cols_off[b + 1] - L.cols_off[b]); }
+  for (int64_t b = 0; b < B; ++b) { L.st_sp[b] = a; a += (L.cols_off[b + 1] - L.cols_off[b]) * q; }
+  L.stash_bytes = 8 * std::max<int64_t>(a, 1);
+  int rc;
+  if ((rc = skb_dev_alloc(L.stash_bytes, c.AS, &L.stash))) return rc;
+  for (int64_t b = 0; b < B; ++b) r[b] = (L.act_off[b + 1] - L.act_off[b]) - L.k[b];
+  const int64_t zero = 0;
+  const int64_t* cols = L.cols.empty() ? &zero : L.cols.data();
+  const int64_t* dd = (const int64_t*)L.desc;
+  if (!c.inc)
+    return skb_level_aug(B, L.k.data(), r.data(), q, L.cols_off.data(), cols, dd + L.o_desc[0],
+                         dd + L.o_desc[1], dd + L.o_desc[2], dd + L.o_desc[3], dd + L.o_desc[4],
+                         dd + L.o_desc[5], L.ptr[0].data(), L.ptr[2].data(), L.ptr[3].data(),
+                         L.ptr[4].data(), L.ipiv.data(), c.UH, c.PsiV, c.UH_div, c.schur,
+                         (double*)L.stash, L.st_us.data(), L.st_ps.data(), L.st_sp.data(), 1, c.AS);
+  std::vector<uint8_t> dirty(B), pdirty(B);
+  std::vector<uint64_t> ous(B, 0), ops(B, 0), osp(B, 0);
+  const OldLevel O = old_level(c.old_table, L.lev);
+  for (int64_t b = 0; b < B; ++b) {
+    const int64_t i = L.idx[b], par = c.parent[i];
+    dirty[b] = c.dmask[i];
+    pdirty[b] = (par >= 0 && c.dmask[par]) ? 1 : 0;
+    if (!dirty[b]) {
+      const int64_t pos = L.clean_pos[b];
+      if (pos < 0 || !O.stash) return 103;
+      ous[b] = O.stash + 8 * (uint64_t)O.st_us[pos];
+      ops[b] = O.stash + 8 * (uint64_t)O.st_ps[pos];
+      osp[b] = O.stash + 8 * (uint64_t)O.st_sp[pos];
+    }
+  }
+  const int64_t* sd = L.sd.empty() ? &zero : L.sd.data();
+  const int64_t* rd = L.rd.empty() ? &zero : L.rd.data();
+  return skb_level_aug_update(B, L.k.data(), r.data(), q, L.cols_off.data(), cols, L.sd_off.data(), sd,
+                              L.rd_off.data(), rd, dirty.data(), pdirty.data(), L.ptr[0].data(),
+                              L.ptr[2].data(), L.ptr[3].data(), L.ptr[4].data(), L.ipiv.data(),
+                              ous.data(), ops.data(), osp.data(), c.nqc, c.nqc ? c.qc : &zero,
+                              c.qmask_dev, c.UH, c.PsiV, c.UH_div, c.schur, (double*)L.stash,
+                              L.st_us.data(), L.st_ps.data(), L.st_sp.data(), c.AS);
+}
+
+int drv_level(Driver& D, int64_t lev) {
+  Engine& E = *D.E;
+  const DrvCfg& c = D.c;
+  LevelOut& R = E.out[lev];
+  ETimer tm;
+  {
+    std::unique_lock<std::mutex> lk(E.m);
+    E.cv.wait(lk, [&] { return R.ready; });
+  }
+  tm.tick("WAIT");
+  if (R.rc) return R.rc == 20 ? 101 : 200 + std::abs(R.rc) % 100;
+  D.h2d += R.h2d;
+  D.d2h += R.d2h;
+  int rc;
+  if (D.prev && (rc = drv_resolve(D, *D.prev))) return rc;
+  tm.tick("resolve");
+  const int64_t b0 = E.level_start[lev], B = E.level_start[lev + 1] - b0;
+  DrvLevel& L = D.lv[lev];
+  L.lev = lev;
+  L.B = B;
+  L.used = true;
+  L.idx.resize(B); L.code.resize(B); L.act_off.assign(B + 1, 0);
+  const int64_t side = (int64_t)1 << lev;
+  for (int64_t b = 0; b < B; ++b) {
+    const int64_t i = b0 + b;
+    L.idx[b] = i;
+    L.code[b] = E.ix[i] * side + E.iy[i];
+    L.act_off[b + 1] = L.act_off[b] + E.a_len[i];
+  }
+  const int64_t na = L.act_off[B];
+  L.act.resize(na); L.perm.assign(na, 0);
+  for (int64_t b = 0; b < B; ++b)
+    if (E.a_len[b0 + b])
+      memcpy(L.act.data() + L.act_off[b], E.big + E.a_start[b0 + b], sizeof(int64_t) * E.a_len[b0 + b]);
+  L.k.assign(B, 0); L.steps.assign(B, 0); L.gap.assign(B, 1.0); L.ratio.assign(B, 1.0);
+  L.info.assign(B, -1); L.clean_pos.assign(B, -1);
+  for (auto& v : L.ptr) v.assign(B, 0);
+  L.ipiv.assign(B, 0);
+  // recompressed boxes: QRCP results of the engine
+  const int64_t Bn = R.B;
+  L.nnew = Bn;
+  L.new_pos.resize(Bn);
+  std::vector<uint8_t> is_new(B, 0);
+  std::vector<int64_t> nBn(Bn), kn(Bn);
+  for (int64_t j = 0; j < Bn; ++j) {
+    const int64_t p = R.idx[j] - b0;
+    if (p < 0 || p >= B) return 104;
+    L.new_pos[j] = p;
+    is_new[p] = 1;
+    const int64_t n = R.act_off[j + 1] - R.act_off[j];
+    if (n != L.act_off[p + 1] - L.act_off[p]) return 104;
+    memcpy(L.perm.data() + L.act_off[p], R.perm.data() + R.act_off[j], sizeof(int32_t) * n);
+    L.k[p] = R.k[j];
+    L.steps[p] = R.steps[j];
+    L.gap[p] = R.gap[j];
+    nBn[j] = n;
+    kn[j] = R.k[j];
+  }
+  // factor storage of the new boxes: T | X_rr | LU | X_sr | X_rs_div | Xss_mod per box (f64),
+  // then the LU pivots (i32), in ONE allocation ordered on the level stream
+  if (Bn > 0) {
+    int64_t tot = 0, rsum = 0;
+    for (int64_t j = 0; j < Bn; ++j) {
+      const int64_t kk = kn[j], rr = nBn[j] - kk;
+      tot += 3 * kk * rr + 2 * rr * rr + kk * kk;
+      rsum += rr;
+    }
+    const int64_t nf = std::max<int64_t>(tot, 1);
+    L.slab_bytes = 8 * nf + 4 * std::max<int64_t>(rsum, 1);
+    if ((rc = skb_dev_alloc(L.slab_bytes, c.S, &L.slab))) return rc;
+    int64_t fo = 0, io = 0;
+    for (int64_t j = 0; j < Bn; ++j) {
+      const int64_t p = L.new_pos[j], kk = kn[j], rr = nBn[j] - kk;
+      const int64_t sz[6] = {kk * rr, rr * rr, rr * rr, kk * rr, rr * kk, kk * kk};
+      // field-major inside the slab as in the Python layout: box-major blocks
+      int64_t o = fo;
+      for (int f = 0; f < 6; ++f) { L.ptr[f][p] = L.slab + 8 * (uint64_t)o; o += sz[f]; }
+      fo = o;
+      L.ipiv[p] = L.slab + 8 * (uint64_t)nf + 4 * (uint64_t)io;
+      io += rr;
+    }
+  }
+  // clean boxes share the previous factorization's memory (skel.py:342-353)
+  if (Bn < B) {
+    if (!c.update || !c.old_table) return 104;
+    const OldLevel O = old_level(c.old_table, lev);
+    if (!O.B) return 101;
+    for (int64_t p = 0; p < B; ++p) {
+      if (is_new[p]) continue;
+      const int64_t pos = find_code(O, L.code[p]);
+      if (pos < 0) return 101;
+      const int64_t a0 = O.act_off[pos], n = O.act_off[pos + 1] - a0;
+      if (n != L.act_off[p + 1] - L.act_off[p] ||
+          (n && memcmp(O.act + a0, L.act.data() + L.act_off[p], sizeof(int64_t) * n)))
+        return 102;                           // clean box changed its active set
+      memcpy(L.perm.data() + L.act_off[p], O.perm + a0, sizeof(int32_t) * n);
+      L.k[p] = O.k[pos]; L.steps[p] = O.steps[pos]; L.gap[p] = O.gap[pos];
+      L.info[p] = O.info[pos]; L.ratio[p] = O.ratio[pos];
+      for (int f = 0; f < 6; ++f) L.ptr[f][p] = O.ptr[f][pos];
+      L.ipiv[p] = O.ipiv[pos];
+      L.clean_pos[p] = pos;
+    }
+  }
+  tm.tick("merge");
+  if (Bn > 0) {
+    if (prof().on) {
+      // algorithmic work: stack + self-block bytes written,
+      // Householder 2 m n^2 - 2/3 n^3, QRCP 2mn + sum_i 4 (m-i)(n-i-1)
+      double ab = 0, gf = 0, gb = 0, qf = 0, qb = 0;
+      for (int64_t j = 0; j < Bn; ++j) {
+        const double m = (double)R.rows[j], n = (double)nBn[j], mq = (double)R.mq[j];
+        ab += m * n + n * n;
+        if (R.rows[j] > 2 * nBn[j]) { gf += 2 * m * n * n - 2.0 / 3.0 * n * n * n; gb += m * n; }
+        qf += 2.0 * mq * n;
+        for (int64_t i = 0; i < R.steps[j]; ++i) qf += 4.0 * (mq - i) * (n - i - 1);
+        qb += mq * n;
+      }
+      skb_prof_add(F_ASSEMBLE, 0.0, 8.0 * ab);
+      skb_prof_add(F_GEQRF, gf, 8.0 * gb);
+      skb_prof_add(F_QRCP, qf, 8.0 * qb);
+    }
+    // (c) Schur stage of the new boxes on the level stream
+    SKB_RET(cudaStreamWaitEvent(c.S, R.ev, 0));
+    std::vector<int64_t> co(5 * Bn);
+    std::vector<uint64_t> cx(4 * Bn), pT(Bn), pXrr(Bn), pLU(Bn), pXsr(Bn), pDiv(Bn), pXss(Bn), pIp(Bn);
+    for (int64_t j = 0; j < Bn; ++j) {
+      const int64_t i = R.idx[j], p = L.new_pos[j];
+      bool inner = false;
+      int64_t cum = 0;
+      for (int qd = 0; qd < 4; ++qd) {
+        const int64_t ch = E.children[4 * i + qd];
+        if (ch >= 0) {
+          inner = true;
+          cum += E.s_len[ch];
+          co[5 * j + 1 + qd] = cum;
+          cx[4 * j + qd] = c.xss[ch];
+        } else {
+          co[5 * j + 1 + qd] = -1;
+          cx[4 * j + qd] = 0;
+        }
+      }
+      co[5 * j] = inner ? 0 : -1;
+      pT[j] = L.ptr[0][p]; pXrr[j] = L.ptr[1][p]; pLU[j] = L.ptr[2][p]; pXsr[j] = L.ptr[3][p];
+      pDiv[j] = L.ptr[4][p]; pXss[j] = L.ptr[5][p]; pIp[j] = L.ipiv[p];
+    }
+    char* pbuf = nullptr;
+    SKB_RET(malloc_async((void**)&pbuf, (size_t)(12 * Bn), c.S));
+    if ((rc = skb_level_schur(Bn, nBn.data(), kn.data(), R.act_off.data(), E.pos, E.nrm, E.w, c.kap,
+                              R.dup, R.dup + R.o_act, (const int32_t*)(R.dbuf + R.o_int), R.A.data(),
+                              R.rows.data(), co.data(), cx.data(), pT.data(), pXrr.data(), pLU.data(),
+                              pXsr.data(), pDiv.data(), pXss.data(), pIp.data(),
+                              (int32_t*)(pbuf + 8 * Bn), (double*)pbuf, E.pde, c.S)))
+      return rc;
+    const size_t need = (size_t)(12 * Bn + 16);
+    if (D.pinned_used + need > D.pinned_cap) return 105;
+    L.pin = D.pinned + D.pinned_used;
+    D.pinned_used += (need + 15) & ~(size_t)15;
+    SKB_RET(cudaMemcpyAsync(L.pin, pbuf, (size_t)(12 * Bn), cudaMemcpyDeviceToHost, c.S));
+    SKB_RET(cudaEventRecord(L.pev, c.S));
+    L.resolved = false;
+    D.d2h += 12 * Bn;
+    cudaFreeAsync(pbuf, c.S);
+    // the engine's level buffers (stacks, permutations, descriptors) are read
+    // by the Schur stage only: released stream-ordered behind it
+    if (R.stack) { cudaFreeAsync(R.stack, c.S); R.stack = nullptr; }
+    if (R.dbuf) { cudaFreeAsync(R.dbuf, c.S); R.dbuf = nullptr; }
+    if (R.dup) { cudaFreeAsync(R.dup, c.S); R.dup = nullptr; }
+    {
+      std::lock_guard<std::mutex> lk(E.m);
+      if (lev < E.acked) E.acked = lev;
+    }
+    E.cv.notify_all();
+  }
+  tm.tick("schur");
+  for (int64_t p = 0; p < B; ++p) c.xss[b0 + p] = L.ptr[5][p];
+  // the level below is final now: its augmentation sweep goes to the sweep stream
+  if (D.prev && (rc = drv_sweep(D, *D.prev))) return rc;
+  tm.tick("sweep");
+  // skeleton / redundant DOF lists and hole columns of the level, one upload
+  L.sd_off.assign(B + 1, 0); L.rd_off.assign(B + 1, 0); L.cols_off.assign(B + 1, 0);
+  for (int64_t b = 0; b < B; ++b) {
+    const int64_t n = L.act_off[b + 1] - L.act_off[b];
+    L.sd_off[b + 1] = L.sd_off[b] + L.k[b];
+    L.rd_off[b + 1] = L.rd_off[b] + (n - L.k[b]);
+  }
+  L.sd.resize(L.sd_off[B]); L.rd.resize(L.rd_off[B]);
+  for (int64_t b = 0; b < B; ++b) {
+    const int64_t a0 = L.act_off[b], n = L.act_off[b + 1] - a0, kk = L.k[b];
+    const int64_t* act = L.act.data() + a0;
+    const int32_t* pm = L.perm.data() + a0;
+    int64_t* sd = L.sd.data() + L.sd_off[b];
+    int64_t* rd = L.rd.data() + L.rd_off[b];
+    for (int64_t j = 0; j < kk; ++j) sd[j] = act[pm[j]];
+    for (int64_t j = kk; j < n; ++j) rd[j - kk] = act[pm[j]];
+  }
+  L.cols.clear();
+  if (c.npairs > 0) {
+    for (int64_t b = 0; b < B; ++b) {
+      const int64_t i = L.idx[b];
+      const int64_t* lo = std::lower_bound(c.pair_box, c.pair_box + c.npairs, i);
+      for (; lo < c.pair_box + c.npairs && *lo == i; ++lo) {
+        const int64_t cur = c.pair_curve[lo - c.pair_box];
+        if (cur >= 1)
+          for (int e = 0; e < 3; ++e) L.cols.push_back(3 * (cur - 1) + e);
+      }
+      L.cols_off[b + 1] = (int64_t)L.cols.size();
+    }
+  }
+  {
+    auto al = [](int64_t o) { return (o + 1) & ~(int64_t)1; };
+    const int64_t nsd = std::max<int64_t>((int64_t)L.sd.size(), 1), nrd = std::max<int64_t>((int64_t)L.rd.size(), 1);
+    const int64_t ncl = std::max<int64_t>((int64_t)L.cols.size(), 1);
+    L.o_desc[0] = 0;
+    L.o_desc[1] = al(B + 1);
+    L.o_desc[2] = al(L.o_desc[1] + nsd);
+    L.o_desc[3] = al(L.o_desc[2] + B + 1);
+    L.o_desc[4] = al(L.o_desc[3] + nrd);
+    L.o_desc[5] = al(L.o_desc[4] + B + 1);
+    const int64_t tot = al(L.o_desc[5] + ncl);
+    std::vector<int64_t> h(tot, 0);
+    memcpy(h.data() + L.o_desc[0], L.sd_off.data(), sizeof(int64_t) * (B + 1));
+    if (!L.sd.empty()) memcpy(h.data() + L.o_desc[1], L.sd.data(), sizeof(int64_t) * L.sd.size());
+    memcpy(h.data() + L.o_desc[2], L.rd_off.data(), sizeof(int64_t) * (B + 1));
+    if (!L.rd.empty()) memcpy(h.data() + L.o_desc[3], L.rd.data(), sizeof(int64_t) * L.rd.size());
+    memcpy(h.data() + L.o_desc[4], L.cols_off.data(), sizeof(int64_t) * (B + 1));
+    if (!L.cols.empty()) memcpy(h.data() + L.o_desc[5], L.cols.data(), sizeof(int64_t) * L.cols.size());
+    L.desc_bytes = 8 * tot;
+    if ((rc = skb_dev_alloc(L.desc_bytes, c.S, &L.desc))) return rc;
+    if ((rc = ring_stage(h.data(), (size_t)L.desc_bytes, c.S, (void*)L.desc))) return rc;
+    D.h2d += L.desc_bytes;
+  }
+  SKB_RET(cudaEventRecord(L.ready, c.S));
+  D.prev = &L;
+  tm.tick("lists");
+  if (ETimer::on()) fprintf(stderr, "driver level %lld (%lld boxes, %lld new):%s us\n", (long long)lev, (long long)B, (long long)Bn, tm.buf);
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+// Update mode with the previous factorization's level table (see OldLevel):
+// clean boxes' skeletons are read from it by the engine itself.
+int skb_engine_set_update_table(int64_t handle, const uint8_t* todo, const int64_t* old_table) {
+  Engine* E = (Engine*)handle;
+  E->todo = todo;
+  E->old_table = old_table;
+  return 0;
+}
+
+// Run the consumer side of every level on the calling thread (see above).
+// cfg (int64 x 24): level stream, sweep stream, curvature (device), q, npairs,
+// pair_box, pair_curve, parent, UH, PsiV, UH_div, schur, update, dmask, nqc, qc,
+// qmask (device), old level table, incremental sweep, xss (uint64 per box).
+// Returns 0, 100 (a box must migrate), 101/102 (clean box missing / changed)
+// or a library error; the handle is valid either way (skb_drv_free).
+int skb_drv_run(int64_t engine, const int64_t* cfg, double pivot_floor, int64_t* handle) {
+  Engine* E = (Engine*)engine;
+  Driver* D = new Driver();
+  *handle = (int64_t)D;
+  D->E = E;
+  DrvCfg& c = D->c;
+  c.S = (cudaStream_t)cfg[0]; c.AS = (cudaStream_t)cfg[1];
+  c.kap = (const double*)cfg[2]; c.q = cfg[3]; c.npairs = cfg[4];
+  c.pair_box = (const int64_t*)cfg[5]; c.pair_curve = (const int64_t*)cfg[6];
+  c.parent = (const int64_t*)cfg[7];
+  c.UH = (double*)cfg[8]; c.PsiV = (double*)cfg[9]; c.UH_div = (double*)cfg[10]; c.schur = (double*)cfg[11];
+  c.update = cfg[12]; c.dmask = (const uint8_t*)cfg[13]; c.nqc = cfg[14]; c.qc = (const int64_t*)cfg[15];
+  c.qmask_dev = (const uint8_t*)cfg[16]; c.old_table = (const int64_t*)cfg[17]; c.inc = cfg[18];
+  c.xss = (uint64_t*)cfg[19];
+  c.floor = pivot_floor;
+  D->lv.resize(E->depth + 1);
+  const int64_t nbox = E->level_start[E->depth + 1];
+  {
+    std::lock_guard<std::recursive_mutex> lk(host_mutex());
+    DrvPinned& g = g_drv_pinned();
+    const size_t want = (size_t)(12 * nbox + 32 * (E->depth + 2) + 1024);
+    if (!g.busy) {
+      if (g.cap < want) {
+        if (g.p) cudaFreeHost(g.p);
+        g.p = nullptr; g.cap = 0;
+        SKB_RET(cudaHostAlloc((void**)&g.p, want + want / 2, cudaHostAllocDefault));
+        g.cap = want + want / 2;
+      }
+      g.busy = true;
+      D->pinned = g.p; D->pinned_cap = g.cap; D->shared_pinned = true;
+    } else {
+      SKB_RET(cudaHostAlloc((void**)&D->pinned, want, cudaHostAllocDefault));
+      D->pinned_cap = want;
+    }
+  }
+  for (int64_t L = 1; L <= E->depth; ++L) {
+    SKB_RET(cudaEventCreateWithFlags(&D->lv[L].ready, cudaEventDisableTiming));
+    SKB_RET(cudaEventCreateWithFlags(&D->lv[L].pev, cudaEventDisableTiming));
+  }
+  for (int64_t L = E->depth; L >= 1; --L) {
+    const int rc = drv_level(*D, L);
+    if (rc) { D->fail_level = L; return rc; }
+  }
+  if (D->prev) {
+    int rc = drv_resolve(*D, *D->prev);
+    if (rc) { D->fail_level = D->prev->lev; return rc; }
+    if ((rc = drv_sweep(*D, *D->prev))) { D->fail_level = D->prev->lev; return rc; }
+  }
+  return 0;
+}
+
+// Arrays of one level (valid until skb_drv_free).  sizes (int64 x 24): B, na, nnew, nsd,
+// nrd, ncols, slab, slab_bytes, stash, stash_bytes, desc, desc_bytes, o_desc[6],
+// total h2d, total d2h.  ptrs (int64 x 32): idx, code, act_off, act, perm(i32), k, steps,
+// gap, info, ratio, clean_pos, ptr[6], ipiv, sd_off, sd, rd_off, rd, cols_off, cols,
+// st_us, st_ps, st_sp, new_pos.  The device allocations become the caller's.
+int skb_drv_level(int64_t handle, int64_t lev, int64_t* sizes, int64_t* ptrs) {
+  Driver* D = (Driver*)handle;
+  if (lev < 1 || lev >= (int64_t)D->lv.size()) return 1;
+  DrvLevel& L = D->lv[lev];
+  if (!L.used) return 2;
+  L.adopted = true;
+  int64_t* s = sizes;
+  s[0] = L.B; s[1] = (int64_t)L.act.size(); s[2] = L.nnew; s[3] = (int64_t)L.sd.size();
+  s[4] = (int64_t)L.rd.size(); s[5] = (int64_t)L.cols.size(); s[6] = (int64_t)L.slab; s[7] = L.slab_bytes;
+  s[8] = (int64_t)L.stash; s[9] = L.stash_bytes; s[10] = (int64_t)L.desc; s[11] = L.desc_bytes;
+  for (int i = 0; i < 6; ++i) s[12 + i] = L.o_desc[i];
+  s[18] = D->h2d; s[19] = D->d2h;
+  int64_t* p = ptrs;
+  p[0] = (int64_t)L.idx.data(); p[1] = (int64_t)L.code.data(); p[2] = (int64_t)L.act_off.data();
+  p[3] = (int64_t)L.act.data(); p[4] = (int64_t)L.perm.data(); p[5] = (int64_t)L.k.data();
+  p[6] = (int64_t)L.steps.data(); p[7] = (int64_t)L.gap.data(); p[8] = (int64_t)L.info.data();
+  p[9] = (int64_t)L.ratio.data(); p[10] = (int64_t)L.clean_pos.data();
+  for (int f = 0; f < 6; ++f) p[11 + f] = (int64_t)L.ptr[f].data();
+  p[17] = (int64_t)L.ipiv.data(); p[18] = (int64_t)L.sd_off.data(); p[19] = (int64_t)L.sd.data();
+  p[20] = (int64_t)L.rd_off.data(); p[21] = (int64_t)L.rd.data(); p[22] = (int64_t)L.cols_off.data();
+  p[23] = (int64_t)L.cols.data(); p[24] = (int64_t)L.st_us.data(); p[25] = (int64_t)L.st_ps.data();
+  p[26] = (int64_t)L.st_sp.data(); p[27] = (int64_t)L.new_pos.data();
+  return 0;
+}
+
+int skb_drv_free(int64_t handle) {
+  Driver* D = (Driver*)handle;
+  if (!D) return 0;
+  bool orphan = false;
+  for (auto& L : D->lv) orphan |= L.used && !L.adopted && (L.slab || L.stash || L.desc);
+  if (orphan) {
+    // an aborted run: nobody took over these allocations
+    cudaStreamSynchronize(D->c.S);
+    cudaStreamSynchronize(D->c.AS);
+    for (auto& L : D->lv)
+      if (L.used && !L.adopted) {
+        if (L.slab) cudaFree((void*)L.slab);
+        if (L.stash) cudaFree((void*)L.stash);
+        if (L.desc) cudaFree((void*)L.desc);
+      }
+  }
+  bool pending = false;
+  for (auto& L : D->lv) pending |= !L.resolved;
+  if (pending) cudaStreamSynchronize(D->c.S);     // a pivot-info copy may still be in flight
+  for (auto& L : D->lv) {
+    if (L.ready) cudaEventDestroy(L.ready);
+    if (L.pev) cudaEventDestroy(L.pev);
+  }
+  if (D->shared_pinned) {
+    std::lock_guard<std::recursive_mutex> lk(host_mutex());
+    g_drv_pinned().busy = false;
+  } else if (D->pinned) {
+    cudaFreeHost(D->pinned);
+  }
+  delete D;
   return 0;
 }
 

@@ -84,7 +84,7 @@ extern "C" int skb_level_schur(int64_t nbox, const int64_t* nB, const int64_t* k
   // permuted self blocks with the children's Xss (skel.py:282-291, 316)
   Packed pk;
   pk.add(child_off, 5 * B);
-  pk.add((const int64_t*)child_xss, 5 * B);
+  pk.add((const int64_t*)child_xss, 4 * B);   // four children per box
   pk.add(E_off.data(), B);
   pk.add(ldE.data(), B);
   int64_t* dpk = nullptr;

@@ -338,6 +338,7 @@ def _tree_native(t: Tree) -> dict:
                   iy=np.ascontiguousarray(t.iy, np.int64),
                   leaf=np.ascontiguousarray(t.is_leaf, np.uint8),
                   ls=np.ascontiguousarray(t.level_start, np.int64),
+                  parent=np.ascontiguousarray(t.parent, np.int64),
                   root=np.array([t.root_center[0], t.root_center[1], t.root_half_width]))
         t._native = nv
     return nv
@@ -376,6 +377,13 @@ class _DevSlab:
         call("skb_dev_alloc", int(max(nbytes, 8)), stream.cuda_stream, out)
         self.ptr = int(out[0])
         self.nbytes = int(nbytes)
+
+    @classmethod
+    def adopt(cls, addr: int, nbytes: int) -> "_DevSlab":
+        """Take over an allocation the native driver made from the same pool."""
+        o = cls.__new__(cls)
+        o.ptr, o.nbytes = int(addr), int(nbytes)
+        return o
 
     def data_ptr(self) -> int:
         return self.ptr
@@ -1603,8 +1611,10 @@ class _AugPipeUpdate(_AugPipe):
              L.st_ps, L.st_sp, _stream())
 
 
-def _finish_top(ctx: _Ctx, levels, store, pipe: "_AugPipe"):
-    """Root block, augmentation sweep and corner LU (reference skel.py:364-425)."""
+def _finish_top(ctx: _Ctx, levels, store, pipe: "_AugPipe", before_sync=None):
+    """Root block, augmentation sweep and corner LU (reference skel.py:364-425).
+    ``before_sync`` runs after the corner LU is enqueued, before its status is
+    read back (host work that overlaps the device tail)."""
     t, b = ctx.t, ctx.b
     dev = _dev()
     s = _stream()
@@ -1659,6 +1669,8 @@ def _finish_top(ctx: _Ctx, levels, store, pipe: "_AugPipe"):
     _Prof.start()
     call("skb_getrf_batched", 1, _mats([_addr(top)], [n], [n], [n]),
          np.array([_addr(ipiv)], np.uint64), ptr(info), ptr(ratio), s)
+    if before_sync is not None:
+        before_sync()
     inf = int(info.cpu().item())
     _Prof.tick("d_corner_lu")
     if inf >= 0:
@@ -1679,6 +1691,11 @@ def _aug_level(L: LevelFactors, UH, PsiV, UH_div, schur, q):
 # The native level engine (csrc/engine.cu) drives factor() unless SKB_ENGINE=0
 # (then the single-threaded level loop below, which update() always uses).
 _ENGINE_ON = os.environ.get("SKB_ENGINE", "1") != "0"
+
+
+# Experiment: acknowledge a level as soon as its QRCP results arrive (the engine
+# enqueues the next level's kernels while this thread enqueues the Schur stage).
+_ACK_EARLY = os.environ.get("SKB_ACK_EARLY", "0") != "0"
 
 
 class _EngineAbort(Exception):
@@ -1722,9 +1739,13 @@ class _Engine:
         self.h = self.h.value
         if update is not None:
             self._upd = update                      # kept alive while the engine runs
-            todo, coff, cskel = update
-            self.lib.skb_engine_set_update(self.h, todo.ctypes.data, coff.ctypes.data,
-                                           cskel.ctypes.data)
+            if len(update) == 2:                    # (todo, previous level table): native driver
+                todo, table = update
+                self.lib.skb_engine_set_update_table(self.h, todo.ctypes.data, table.ctypes.data)
+            else:
+                todo, coff, cskel = update
+                self.lib.skb_engine_set_update(self.h, todo.ctypes.data, coff.ctypes.data,
+                                               cskel.ctypes.data)
             self.lib.skb_engine_go(self.h)
         # Run-ahead of the engine over the enqueued Schur stages.  On trees
         # with heavy levels (> 512 boxes, cfg3) the engine starts level L only
@@ -1793,6 +1814,211 @@ class _Engine:
             self.close(stop=True)
         except Exception:
             pass
+
+
+
+# The native level driver (csrc/engine.cu skb_drv_run) consumes the engine's
+# levels in C++ (merge, layout, Schur stage, sweep, level lists); this module
+# only wraps the resulting arrays.  SKB_NATIVE=0 keeps the Python consumer loop.
+_NATIVE_ON = os.environ.get("SKB_NATIVE", "1") != "0"
+_O_NF = 21
+
+
+class _RawDev:
+    """Device address with the data_ptr() protocol of a tensor."""
+    __slots__ = ("p",)
+
+    def __init__(self, p):
+        self.p = int(p)
+
+    def data_ptr(self) -> int:
+        return self.p
+
+
+def _level_code(L: "LevelFactors"):
+    c = L.__dict__.get("code")
+    if c is None:
+        side = np.int64(1) << np.int64(L.lev)
+        c = L.code = np.ascontiguousarray(L.tree.ix[L.idx] * side + L.tree.iy[L.idx], np.int64)
+    return c
+
+
+def _level_row(L: "LevelFactors"):
+    """Row of the previous-factorization table (engine.cu OldLevel) for one level."""
+    row = L.__dict__.get("_row")
+    if row is not None:
+        return row
+    bt = L.batch
+    bt.resolve()
+    keep = [_level_code(L), np.ascontiguousarray(bt.act_off, np.int64), np.ascontiguousarray(bt.act, np.int64),
+            np.ascontiguousarray(bt.perm, np.int32), np.ascontiguousarray(bt.k, np.int64)]
+    keep += [np.ascontiguousarray(bt.ptr[f], np.uint64) for f in BoxBatch.FIELDS]
+    keep += [np.ascontiguousarray(bt.ipiv, np.uint64), np.ascontiguousarray(bt.info, np.int64),
+             np.ascontiguousarray(bt.ratio, np.float64)]
+    st = L.__dict__.get("stash")
+    row = np.zeros(_O_NF, np.int64)
+    row[0] = len(L.idx)
+    for i, a in enumerate(keep):
+        row[1 + i] = a.ctypes.data
+    if st is not None:
+        sts = [np.ascontiguousarray(L.st_us, np.int64), np.ascontiguousarray(L.st_ps, np.int64),
+               np.ascontiguousarray(L.st_sp, np.int64)]
+        row[15] = _addr(st)
+        row[16], row[17], row[18] = (a.ctypes.data for a in sts)
+        keep += sts
+    tail = [np.ascontiguousarray(bt.gap, np.float64), np.ascontiguousarray(bt.steps, np.int64)]
+    row[19], row[20] = tail[0].ctypes.data, tail[1].ctypes.data
+    L._row_keep = keep + tail
+    L._row = row
+    return row
+
+
+def _native_level(lib, drv, lev, t, old, sizes, ptrs):
+    """LevelFactors / BoxBatch of one level from the native driver's arrays."""
+    rc = lib.skb_drv_level(drv, lev, sizes.ctypes.data, ptrs.ctypes.data)
+    if rc:
+        raise _lib.SkbError(f"skb_drv_level returned {rc}")
+    B, na, nnew, nsd, nrd, ncl = (int(v) for v in sizes[:6])
+    slab, slab_b, stash, stash_b, desc, desc_b = (int(v) for v in sizes[6:12])
+    od = [int(v) for v in sizes[12:18]]
+    arr = _Engine._arr
+    p = ptrs
+    i64, u64, f64 = np.int64, np.uint64, np.float64
+    bt = BoxBatch.__new__(BoxBatch)
+    bt.idx = arr(p[0], B, i64)
+    bt.act_off = arr(p[2], B + 1, i64)
+    bt.act = arr(p[3], na, i64)
+    bt.nB = np.diff(bt.act_off)
+    bt.perm = arr(p[4], na, np.int32)
+    bt.k = arr(p[5], B, i64)
+    bt.steps = arr(p[6], B, i64)
+    bt.gap = arr(p[7], B, f64)
+    bt.info = arr(p[8], B, i64)
+    bt.ratio = arr(p[9], B, f64)
+    bt.ptr = {f: arr(p[11 + i], B, u64) for i, f in enumerate(BoxBatch.FIELDS)}
+    bt.ipiv = arr(p[17], B, u64)
+    bt.slabs = []
+    bt.slab_of = np.full(B, -1, i64)
+    if nnew and slab:
+        bt.slabs.append(_DevSlab.adopt(slab, slab_b))
+        bt.slab_of[arr(p[27], nnew, i64)] = 0
+    if nnew < B:
+        cpos = arr(p[10], B, i64)
+        clean = np.flatnonzero(cpos >= 0)
+        ob = old[lev].batch
+        so = ob.slab_of[cpos[clean]]
+        lut = np.full(max(len(ob.slabs), 1), -1, i64)
+        for u in np.unique(so[so >= 0]):
+            lut[u] = len(bt.slabs)
+            bt.slabs.append(ob.slabs[u])
+        bt.slab_of[clean] = np.where(so >= 0, lut[np.maximum(so, 0)], -1)
+    L = LevelFactors.__new__(LevelFactors)
+    L.lev, L.tree, L.batch, L.idx = lev, t, bt, bt.idx
+    L.code = arr(p[1], B, i64)
+    L.k = bt.k.copy()
+    L.r = bt.nB - bt.k
+    L.sd_off, L.sd = arr(p[18], B + 1, i64), arr(p[19], nsd, i64)
+    L.rd_off, L.rd = arr(p[20], B + 1, i64), arr(p[21], nrd, i64)
+    L.cols_off, L.cols = arr(p[22], B + 1, i64), arr(p[23], ncl, i64)
+    L.ncols = np.diff(L.cols_off)
+    keep = _DevSlab.adopt(desc, desc_b)
+    L.d = {n: _RawDev(desc + 8 * o) for n, o in zip(("sd_off", "sd", "rd_off", "rd", "c_off", "c"), od)}
+    L.d["_keep"] = keep
+    L.P = {f: bt.ptr[f] for f in BoxBatch.FIELDS}
+    L.ipiv = bt.ipiv
+    if stash:
+        L.stash = _DevSlab.adopt(stash, stash_b)
+        L.st_us, L.st_ps, L.st_sp = arr(p[24], B, i64), arr(p[25], B, i64), arr(p[26], B, i64)
+    return L
+
+
+def _run_levels_native(ctx: _Ctx, upd=None):
+    """Level loop of factor() / update() on the native engine + driver."""
+    t, b = ctx.t, ctx.b
+    lib = _lib.load()
+    with _ht("N.store"):
+        store = ActStore(t, engine=True, dpn=ctx.dpn)
+    ctx.store = store
+    old = None
+    eupd = None
+    table = None
+    if upd is not None:
+        old_fct, dmask = upd
+        old = {L.lev: L for L in old_fct.levels}
+        with _ht("N.table"):
+            table = np.zeros((max(t.depth, max(old, default=0)) + 1, _O_NF), np.int64)
+            for lev, L in old.items():
+                table[lev] = _level_row(L)
+        dm8 = np.ascontiguousarray(dmask, np.uint8)
+        eupd = (dm8, table)
+    with _ht("N.engine"):
+        eng = _Engine(ctx, store, update=eupd)
+    drv = ctypes.c_int64(0)
+    try:
+        with torch.cuda.stream(ctx.sstream):
+            with _ht("N.pipe"):
+                pipe = _make_pipe(ctx)
+            ctx.pipe = pipe
+            nv = _tree_native(t)
+            if b.n_holes:
+                pb, pc = t.hole_pairs(np.asarray(b.offsets, np.int64))
+                pb, pc = np.ascontiguousarray(pb, np.int64), np.ascontiguousarray(pc, np.int64)
+            else:
+                pb = pc = np.zeros(1, np.int64)
+            cfg = np.zeros(24, np.int64)
+            cfg[0] = _stream()
+            cfg[2] = ptr(ctx.g.kap)
+            cfg[3] = pipe.q
+            cfg[4] = len(pb) if b.n_holes else 0
+            cfg[5], cfg[6], cfg[7] = pb.ctypes.data, pc.ctypes.data, nv["parent"].ctypes.data
+            if pipe.q:
+                cfg[1] = pipe.stream.cuda_stream
+                cfg[8], cfg[9], cfg[10], cfg[11] = ptr(pipe.UH), ptr(pipe.PsiV), ptr(pipe.UH_div), ptr(pipe.schur)
+            inc = bool(getattr(pipe, "inc", False))
+            if upd is not None:
+                cfg[12] = 1
+                cfg[13] = dm8.ctypes.data
+                cfg[17] = table.ctypes.data
+            if inc:
+                qc = np.ascontiguousarray(pipe.qc, np.int64)
+                cfg[14] = len(qc)
+                cfg[15] = qc.ctypes.data if len(qc) else 0
+                cfg[16] = ptr(pipe.qmask_d)
+                cfg[18] = 1
+            cfg[19] = store.xss.ctypes.data
+            with _ht("N.run"):
+                rc = lib.skb_drv_run(eng.h, cfg.ctypes.data, PIVOT_RATIO_FLOOR, ctypes.byref(drv))
+            if rc in (100, 101):
+                raise _EngineAbort()
+            if rc == 102:
+                raise RuntimeError("clean box changed its active set")
+            if rc:
+                raise _lib.SkbError(f"native level driver failed (rc {rc})")
+        eng.close()
+        torch.cuda.current_stream().wait_stream(ctx.sstream)
+        return store, (lib, drv, old)
+    except BaseException:
+        eng.close(stop=True)
+        if drv.value:
+            lib.skb_drv_free(drv.value)
+        raise
+
+
+def _native_collect(ctx: _Ctx, handle):
+    """Wrap the driver's per-level arrays (after the remaining device work has
+    been enqueued: this host work overlaps it) and release the driver."""
+    lib, drv, old = handle
+    t = ctx.t
+    sizes, ptrs = np.zeros(24, np.int64), np.zeros(32, np.int64)
+    try:
+        with _ht("N.collect"):
+            levels = [_native_level(lib, drv.value, lev, t, old, sizes, ptrs)
+                      for lev in range(t.depth, 0, -1)]
+        IO["h2d"] += int(sizes[18])
+        IO["d2h"] += int(sizes[19])
+    finally:
+        lib.skb_drv_free(drv.value)
+    return levels
 
 
 def _run_levels_engine(ctx: _Ctx):
@@ -1881,6 +2107,8 @@ def _engine_loop(ctx, eng, store, reuse=None, dirty=None):
             h = eng.wait(lev)
             bt_new = None
             if h is not None:
+                if _ACK_EARLY:
+                    eng.lib.skb_engine_ack(eng.h, lev)
                 bt_new = BoxBatch(h["idx"], h["act_off"], h["act"])
                 bt_new.perm[:] = h["perm"]
                 bt_new.k[:] = h["k"]
@@ -2081,18 +2309,30 @@ def factor(spec, b, t: Tree, tol: float, workers: int = 1,
         ctx = _Ctx(spec, b, t, tol, proxy_count, proxy_factor)
     with torch.cuda.stream(_compress_stream()):
         with _ht("run_levels"):
-            levels = None
+            levels = nh = None
             if _ENGINE_ON and not _Prof.enabled:
                 try:
-                    levels, store, _ = _run_levels_engine(ctx)
+                    if _NATIVE_ON:
+                        store, nh = _run_levels_native(ctx)
+                    else:
+                        levels, store, _ = _run_levels_engine(ctx)
                 except _EngineAbort:
                     _drain(ctx)
                     ctx = _Ctx(spec, b, t, tol, proxy_count, proxy_factor)
-                    levels = None
-            if levels is None:
+                    levels = nh = None
+            if levels is None and nh is None:
                 levels, store, _ = _run_levels(ctx)
         with _ht("finish_top"):
-            rd, E_root, top, ipiv, UH, PsiV, UH_div, q, ratio = _finish_top(ctx, levels, store, ctx.pipe)
+            got = []
+            collect = (lambda: got.append(_native_collect(ctx, nh))) if nh is not None else None
+            try:
+                rd, E_root, top, ipiv, UH, PsiV, UH_div, q, ratio = _finish_top(
+                    ctx, levels, store, ctx.pipe, before_sync=collect)
+            finally:
+                if nh is not None and not got:
+                    nh[0].skb_drv_free(nh[1].value)
+            if nh is not None:
+                levels = got[0]
     with _ht("final_sync"):
         torch.cuda.synchronize()
     stats = {"k_per_level": {L.lev: int(L.k.max(initial=0)) for L in levels},
@@ -2123,18 +2363,30 @@ def update(fct: Factorization, b_new, report, workers: int = 1) -> Factorization
     ctx.upd_old = (fct, dmask)
     torch.cuda.current_stream().synchronize()
     with torch.cuda.stream(_compress_stream()):
-        levels = None
+        levels = nh = None
         if _ENGINE_ON and not _Prof.enabled:
             try:
-                levels, store, n_recomp = _run_levels_engine_update(ctx, old, dmask)
+                if _NATIVE_ON:
+                    store, nh = _run_levels_native(ctx, upd=(fct, dmask))
+                else:
+                    levels, store, n_recomp = _run_levels_engine_update(ctx, old, dmask)
             except _EngineAbort:
                 _drain(ctx)
                 ctx = _Ctx(fct.spec, b_new, t_new, fct.tol, fct.proxy_count, fct.proxy_factor)
                 ctx.upd_old = (fct, dmask)
-                levels = None
-        if levels is None:
+                levels = nh = None
+        if levels is None and nh is None:
             levels, store, n_recomp = _run_levels(ctx, reuse=old, dirty=dmask)
-        rd, E_root, top, ipiv, UH, PsiV, UH_div, q, ratio = _finish_top(ctx, levels, store, ctx.pipe)
+        got = []
+        collect = (lambda: got.append(_native_collect(ctx, nh))) if nh is not None else None
+        try:
+            rd, E_root, top, ipiv, UH, PsiV, UH_div, q, ratio = _finish_top(
+                ctx, levels, store, ctx.pipe, before_sync=collect)
+        finally:
+            if nh is not None and not got:
+                nh[0].skb_drv_free(nh[1].value)
+        if nh is not None:
+            levels = got[0]
     torch.cuda.synchronize()
     ctx.upd_old = None                                  # no chain of old factorizations
     ctx.pipe = None

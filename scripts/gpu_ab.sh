@@ -1,5 +1,7 @@
 cd $GRAFT_REPO_ROOT
-python scripts/ab_factor.py cfg3 10
-SKB_QRCP_SMEM_FIRST=1 python scripts/ab_factor.py cfg3 10
-python scripts/ab_factor.py cfg2 10
-SKB_QRCP_SMEM_FIRST=1 python scripts/ab_factor.py cfg2 10
+python scripts/upd_bench.py
+SKB_QRCP_CMIN=8 python scripts/upd_bench.py
+SKB_QRCP_CMIN=16 python scripts/upd_bench.py
+SKB_QRCP_CMIN=8 python scripts/ab_factor.py cfg2 12
+SKB_QRCP_CMIN=16 python scripts/ab_factor.py cfg2 12
+SKB_QRCP_CMIN=8 python scripts/ab_factor.py cfg3 12
