@@ -9,18 +9,48 @@
 
 namespace skb {
 
+// Batched 2-D copies / row gathers / row scatters.  Pure data movement (HBM /
+// L2 bound): consecutive threads walk consecutive columns of a row, rows are
+// dealt to warps (narrow rows) or to whole blocks (wide rows), all index
+// arithmetic in 32 bits without divisions; compact blocks copy as double2.
 __global__ void k_copy2d(const SkbMat* __restrict__ dst, const SkbMat* __restrict__ src,
                          int trans) {
   const SkbMat D = dst[blockIdx.y], S = src[blockIdx.y];
-  const int64_t tot = D.rows * D.cols;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    int64_t i, j;
-    if (trans) { j = t / D.rows; i = t - j * D.rows; }   // walk src rows contiguously
-    else { i = t / D.cols; j = t - i * D.cols; }
-    D.ptr[i * D.ld + j] = trans ? S.ptr[j * S.ld + i] : S.ptr[i * S.ld + j];
+  const int rows = (int)D.rows, cols = (int)D.cols;
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x, nthr = gridDim.x * blockDim.x;
+  if (trans) {                                     // D[i][j] = S[j][i] (one small call per factorization)
+    const unsigned tot = (unsigned)rows * (unsigned)cols;
+    for (unsigned t = gtid; t < tot; t += nthr) {
+      const unsigned j = t / (unsigned)rows, i = t - j * (unsigned)rows;   // walk src rows contiguously
+      D.ptr[(int64_t)i * D.ld + j] = S.ptr[(int64_t)j * S.ld + i];
+    }
+    return;
+  }
+  if (D.ld == cols && S.ld == cols) {              // compact block: flat copy
+    const int64_t tot = (int64_t)rows * cols;
+    if ((((uintptr_t)D.ptr | (uintptr_t)S.ptr) & 15) == 0) {
+      const int64_t n2 = tot >> 1;
+      double2* d2 = reinterpret_cast<double2*>(D.ptr);
+      const double2* s2 = reinterpret_cast<const double2*>(S.ptr);
+      for (int64_t t = gtid; t < n2; t += nthr) d2[t] = s2[t];
+      if ((tot & 1) && gtid == 0) D.ptr[tot - 1] = S.ptr[tot - 1];
+    } else {
+      for (int64_t t = gtid; t < tot; t += nthr) D.ptr[t] = S.ptr[t];
+    }
+    return;
+  }
+  const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
+  const int gw = blockIdx.x * wpb + (threadIdx.x >> 5), nw = gridDim.x * wpb;
+  for (int i = gw; i < rows; i += nw) {
+    const double* sp = S.ptr + (int64_t)i * S.ld;
+    double* dp = D.ptr + (int64_t)i * D.ld;
+    for (int j = lane; j < cols; j += 32) dp[j] = sp[j];
   }
 }
+
+// rows per step and threads per row for a row length nc: 256 threads cover
+// 256 / tpr rows at a time, tpr = 32 .. 256 consecutive threads on one row
+__device__ __forceinline__ int row_tpr(int nc) { return nc > 128 ? 256 : (nc > 64 ? 128 : (nc > 32 ? 64 : 32)); }
 
 __global__ void k_gather_rows(const int64_t* __restrict__ idx_off, const int64_t* __restrict__ idx,
                               const int64_t* __restrict__ col_off,
@@ -29,16 +59,31 @@ __global__ void k_gather_rows(const int64_t* __restrict__ idx_off, const int64_t
                               double* __restrict__ dst, const int64_t* __restrict__ dst_off,
                               const int64_t* __restrict__ dst_ld) {
   const int64_t b = blockIdx.y;
-  const int64_t i0 = idx_off[b], nr = idx_off[b + 1] - i0;
+  const int64_t i0 = idx_off[b];
+  const int nr = (int)(idx_off[b + 1] - i0);
   const int64_t c0 = col ? col_off[b] : 0;
-  const int64_t nc = col ? col_off[b + 1] - c0 : ncols;
+  const int nc = (int)(col ? col_off[b + 1] - c0 : ncols);
   double* d = dst + dst_off[b];
   const int64_t ld = dst_ld[b];
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nr * nc;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = t / nc, c = t - i * nc;
-    const int64_t sc = col ? col[c0 + c] : c;
-    d[i * ld + c] = src[idx[i0 + i] * src_ld + sc];
+  const int tpr = row_tpr(nc), rps = 256 / tpr;
+  const int tr = threadIdx.x / tpr, tc = threadIdx.x - tr * tpr;
+  if (!col && tpr == 256 && !(nc & 1) && !(src_ld & 1) && !(ld & 1) && !(dst_off[b] & 1) &&
+      ((((uintptr_t)src | (uintptr_t)dst) & 15) == 0)) {
+    const int n2 = nc >> 1;
+    for (int i = blockIdx.x; i < nr; i += gridDim.x) {
+      const double2* sp = reinterpret_cast<const double2*>(src + idx[i0 + i] * src_ld);
+      double2* dp = reinterpret_cast<double2*>(d + (int64_t)i * ld);
+      for (int c = tc; c < n2; c += 256) dp[c] = sp[c];
+    }
+    return;
+  }
+  for (int i = blockIdx.x * rps + tr; i < nr; i += gridDim.x * rps) {
+    const double* sp = src + idx[i0 + i] * src_ld;
+    double* dp = d + (int64_t)i * ld;
+    if (col)
+      for (int c = tc; c < nc; c += tpr) dp[c] = sp[col[c0 + c]];
+    else
+      for (int c = tc; c < nc; c += tpr) dp[c] = sp[c];
   }
 }
 
@@ -51,19 +96,33 @@ __global__ void k_scatter_rows(const int64_t* __restrict__ idx_off,
                                const int64_t* __restrict__ src_ld, double* __restrict__ dst,
                                int64_t dst_ld, int accumulate, double alpha) {
   const int64_t b = blockIdx.y;
-  const int64_t i0 = idx_off[b], nr = idx_off[b + 1] - i0;
+  const int64_t i0 = idx_off[b];
+  const int nr = (int)(idx_off[b + 1] - i0);
   const int64_t c0 = col ? col_off[b] : 0;
-  const int64_t nc = col ? col_off[b + 1] - c0 : ncols;
+  const int nc = (int)(col ? col_off[b + 1] - c0 : ncols);
   const double* s = src + src_off[b];
   const int64_t ld = src_ld[b];
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nr * nc;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = t / nc, c = t - i * nc;
-    const int64_t dc = col ? col[c0 + c] : c;
-    double* o = dst + idx[i0 + i] * dst_ld + dc;
-    const double v = s[i * ld + c];
-    if (accumulate) *o += alpha * v;
-    else *o = v;
+  const int tpr = row_tpr(nc), rps = 256 / tpr;
+  const int tr = threadIdx.x / tpr, tc = threadIdx.x - tr * tpr;
+  if (!col && !accumulate && tpr == 256 && !(nc & 1) && !(dst_ld & 1) && !(ld & 1) &&
+      !(src_off[b] & 1) && ((((uintptr_t)src | (uintptr_t)dst) & 15) == 0)) {
+    const int n2 = nc >> 1;
+    for (int i = blockIdx.x; i < nr; i += gridDim.x) {
+      const double2* sp = reinterpret_cast<const double2*>(s + (int64_t)i * ld);
+      double2* dp = reinterpret_cast<double2*>(dst + idx[i0 + i] * dst_ld);
+      for (int c = tc; c < n2; c += 256) dp[c] = sp[c];
+    }
+    return;
+  }
+  for (int i = blockIdx.x * rps + tr; i < nr; i += gridDim.x * rps) {
+    const double* sp = s + (int64_t)i * ld;
+    double* dp = dst + idx[i0 + i] * dst_ld;
+    for (int c = tc; c < nc; c += tpr) {
+      double* o = dp + (col ? col[c0 + c] : c);
+      const double v = sp[c];
+      if (accumulate) *o += alpha * v;
+      else *o = v;
+    }
   }
 }
 
@@ -191,7 +250,8 @@ extern "C" int skb_copy2d_batched(int64_t nbox, const SkbMat* dst, const SkbMat*
   ProfScope ps(F_MOVE, s);
   for (int64_t b0 = 0; b0 < nbox; b0 += 65535) {
     const int64_t nb = std::min<int64_t>(65535, nbox - b0);
-    dim3 grid(grid_cap((maxe + 255) / 256, 1024), (unsigned)nb);
+    // 2 doubles x 4 passes per thread on the flat path
+    dim3 grid(grid_cap((maxe + 2047) / 2048, nb > 64 ? 32 : 1024), (unsigned)nb);
     k_copy2d<<<grid, 256, 0, s>>>(dd + b0, ds + b0, trans);
   }
   cudaError_t e = cudaGetLastError();
@@ -207,7 +267,9 @@ extern "C" int skb_gather_rows(int64_t nbox, const int64_t* idx_off, const int64
                                int64_t max_cols, void* stream) {
   if (nbox <= 0 || max_rows <= 0 || max_cols <= 0) return 0;
   if (nbox > 65535) return 2;
-  dim3 grid(grid_cap((max_rows * max_cols + 255) / 256, 2048), (unsigned)nbox);
+  // one row per 32..256 threads (row_tpr): blocks walk the rows of a box
+  const int64_t rps_g = max_cols > 128 ? 1 : (max_cols > 64 ? 2 : (max_cols > 32 ? 4 : 8));
+  dim3 grid(grid_cap((max_rows + rps_g - 1) / rps_g, nbox > 64 ? 64 : 1024), (unsigned)nbox);
   ProfScope ps(F_MOVE, (cudaStream_t)stream);
   k_gather_rows<<<grid, 256, 0, (cudaStream_t)stream>>>(idx_off, idx, col_off, col, ncols, src,
                                                         src_ld, dst, dst_off, dst_ld);
@@ -223,7 +285,8 @@ extern "C" int skb_scatter_rows(int64_t nbox, const int64_t* idx_off, const int6
                                 int64_t max_cols, void* stream) {
   if (nbox <= 0 || max_rows <= 0 || max_cols <= 0) return 0;
   if (nbox > 65535) return 2;
-  dim3 grid(grid_cap((max_rows * max_cols + 255) / 256, 2048), (unsigned)nbox);
+  const int64_t rps_s = max_cols > 128 ? 1 : (max_cols > 64 ? 2 : (max_cols > 32 ? 4 : 8));
+  dim3 grid(grid_cap((max_rows + rps_s - 1) / rps_s, nbox > 64 ? 64 : 1024), (unsigned)nbox);
   ProfScope ps(F_MOVE, (cudaStream_t)stream);
   k_scatter_rows<<<grid, 256, 0, (cudaStream_t)stream>>>(idx_off, idx, col_off, col, ncols, src,
                                                          src_off, src_ld, dst, dst_ld, accumulate,

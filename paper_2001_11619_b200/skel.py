@@ -1960,11 +1960,12 @@ def _run_levels_native(ctx: _Ctx, upd=None):
                 pipe = _make_pipe(ctx)
             ctx.pipe = pipe
             nv = _tree_native(t)
-            if b.n_holes:
-                pb, pc = t.hole_pairs(np.asarray(b.offsets, np.int64))
-                pb, pc = np.ascontiguousarray(pb, np.int64), np.ascontiguousarray(pc, np.int64)
-            else:
-                pb = pc = np.zeros(1, np.int64)
+            with _ht("N.pairs"):
+                if b.n_holes:
+                    pb, pc = t.hole_pairs(np.asarray(b.offsets, np.int64))
+                    pb, pc = np.ascontiguousarray(pb, np.int64), np.ascontiguousarray(pc, np.int64)
+                else:
+                    pb = pc = np.zeros(1, np.int64)
             cfg = np.zeros(24, np.int64)
             cfg[0] = _stream()
             cfg[2] = ptr(ctx.g.kap)
@@ -2346,8 +2347,9 @@ def factor(spec, b, t: Tree, tol: float, workers: int = 1,
 
 def update(fct: Factorization, b_new, report, workers: int = 1) -> Factorization:
     """Refactor only what a local perturbation invalidated (reference skel.py:456-514)."""
-    torch.cuda.synchronize()
-    _DevSlab.flush()
+    with _ht("U.sync"):
+        torch.cuda.synchronize()
+        _DevSlab.flush()
     t0 = time.perf_counter()
     try:
         with _ht("U.refit"):
@@ -2359,9 +2361,11 @@ def update(fct: Factorization, b_new, report, workers: int = 1) -> Factorization
     if not np.array_equal(report.old_to_new, np.arange(len(report.old_to_new))):
         raise NotImplementedError("only DOF-preserving edits (hole moves) are supported")
     old = {L.lev: L for L in fct.levels}
-    ctx = _Ctx(fct.spec, b_new, t_new, fct.tol, fct.proxy_count, fct.proxy_factor)
-    ctx.upd_old = (fct, dmask)
-    torch.cuda.current_stream().synchronize()
+    with _ht("U.ctx"):
+        ctx = _Ctx(fct.spec, b_new, t_new, fct.tol, fct.proxy_count, fct.proxy_factor)
+        ctx.upd_old = (fct, dmask)
+        ctx.g                                           # geometry upload
+        torch.cuda.current_stream().synchronize()
     with torch.cuda.stream(_compress_stream()):
         levels = nh = None
         if _ENGINE_ON and not _Prof.enabled:
@@ -2380,14 +2384,16 @@ def update(fct: Factorization, b_new, report, workers: int = 1) -> Factorization
         got = []
         collect = (lambda: got.append(_native_collect(ctx, nh))) if nh is not None else None
         try:
-            rd, E_root, top, ipiv, UH, PsiV, UH_div, q, ratio = _finish_top(
-                ctx, levels, store, ctx.pipe, before_sync=collect)
+            with _ht("U.finish"):
+                rd, E_root, top, ipiv, UH, PsiV, UH_div, q, ratio = _finish_top(
+                    ctx, levels, store, ctx.pipe, before_sync=collect)
         finally:
             if nh is not None and not got:
                 nh[0].skb_drv_free(nh[1].value)
         if nh is not None:
             levels = got[0]
-    torch.cuda.synchronize()
+    with _ht("U.final"):
+        torch.cuda.synchronize()
     ctx.upd_old = None                                  # no chain of old factorizations
     ctx.pipe = None
     for L in levels:

@@ -401,3 +401,98 @@ def test_laplace_stack_and_self_block_bitwise(golden):
     for bi_, lst in enumerate(lists):
         refE = O.lap_self_block(wl.boundary, lst, lst)
         assert np.array_equal(En[eo[bi_]:eo[bi_ + 1]].reshape(nBs[bi_], nBs[bi_]), refE)
+
+
+def test_move_kernels_bit_exact():
+    """skb_copy2d_batched / skb_gather_rows / skb_scatter_rows move bytes only:
+    bit-exact against NumPy indexing over compact / strided / unaligned / odd /
+    empty shapes, with and without column lists, narrow and wide rows."""
+    from paper_2001_11619_b200._lib import MAT_DT, ptr
+    rng = np.random.default_rng(3)
+    s = skel._stream()
+    # -- copy2d: (rows, cols, ld_dst, ld_src, element offset of the source block)
+    pool = _dev(rng.standard_normal(400000))
+    cases = [(7, 5, 5, 5, 0), (7, 5, 5, 5, 1), (64, 64, 64, 64, 2), (33, 17, 40, 23, 3),
+             (1, 1, 1, 1, 0), (200, 129, 129, 129, 7), (0, 4, 4, 4, 0), (117, 117, 117, 117, 100)]
+    for trans in (0, 1):
+        dst_t, ms_d, ms_s, refs = [], [], [], []
+        off = 0
+        for (r, c, ldd, lds, so) in cases:
+            src_rows, src_cols = (c, r) if trans else (r, c)
+            lds_eff = max(lds, src_cols)
+            sview = pool[off + so: off + so + src_rows * lds_eff].view(src_rows, lds_eff) if src_rows else None
+            off += so + src_rows * lds_eff + 8
+            d = torch.full((max(r, 1), max(ldd, c, 1)), -7.0, dtype=torch.float64, device="cuda")
+            dst_t.append(d)
+            ms_d.append((d.data_ptr(), r, c, d.shape[1]))
+            ms_s.append((sview.data_ptr() if sview is not None else pool.data_ptr(), src_rows, src_cols, lds_eff))
+            if r and c:
+                sv = sview[:, :src_cols].cpu().numpy()
+                refs.append(sv.T.copy() if trans else sv.copy())
+            else:
+                refs.append(None)
+        md = np.array(ms_d, dtype=[("ptr", "u8"), ("rows", "i8"), ("cols", "i8"), ("ld", "i8")]).astype(MAT_DT)
+        msr = np.array(ms_s, dtype=[("ptr", "u8"), ("rows", "i8"), ("cols", "i8"), ("ld", "i8")]).astype(MAT_DT)
+        call("skb_copy2d_batched", len(cases), md, msr, trans, s)
+        torch.cuda.synchronize()
+        for d, (r, c, *_), ref in zip(dst_t, cases, refs):
+            if ref is None:
+                continue
+            got = d.cpu().numpy()
+            assert np.array_equal(got[:r, :c], ref)
+            assert np.all(got[:r, c:] == -7.0)
+    # -- gather / scatter rows
+    for nrows_src, ncols in ((500, 3), (500, 48), (300, 129), (200, 256), (100, 770)):
+        X = rng.standard_normal((nrows_src, ncols))
+        dX = _dev(X)
+        B = 5
+        perm_all = rng.permutation(nrows_src)               # disjoint row sets (as in the sweeps)
+        cuts = np.cumsum([0, 0, 1, 33, 64, 97])
+        lists = [perm_all[cuts[j]:cuts[j + 1]] for j in range(5)]
+        idx_off = np.zeros(B + 1, np.int64)
+        np.cumsum([len(l) for l in lists], out=idx_off[1:])
+        idx = np.concatenate(lists).astype(np.int64)
+        for use_cols in (False, True):
+            if use_cols:
+                cl = [np.sort(rng.permutation(ncols)[:max(1, (b * ncols) // 6)]) for b in range(B)]
+                col_off = np.zeros(B + 1, np.int64)
+                np.cumsum([len(c) for c in cl], out=col_off[1:])
+                colv = np.concatenate(cl).astype(np.int64)
+                widths = np.array([len(c) for c in cl], np.int64)
+            else:
+                cl = [np.arange(ncols)] * B
+                widths = np.full(B, ncols, np.int64)
+            ld = widths + np.array([0, 1, 0, 2, 0])          # odd leading dimensions too
+            sizes = np.array([len(l) for l in lists], np.int64) * ld
+            dst_off = np.zeros(B, np.int64)
+            np.cumsum(sizes[:-1] + np.array([1, 0, 3, 0]), out=dst_off[1:])   # odd offsets
+            buf = torch.full((int(dst_off[-1] + sizes[-1]) + 8,), -3.0, dtype=torch.float64, device="cuda")
+            d_io, d_idx, d_do, d_ld = _dev(idx_off), _dev(idx if len(idx) else np.zeros(1, np.int64)), _dev(dst_off), _dev(ld)
+            d_cols = (_dev(col_off), _dev(colv)) if use_cols else None      # kept alive for the calls
+            args_c = (ptr(d_cols[0]), ptr(d_cols[1])) if use_cols else (None, None)
+            call("skb_gather_rows", B, ptr(d_io), ptr(d_idx), args_c[0], args_c[1], ncols, ptr(dX), ncols,
+                 ptr(buf), ptr(d_do), ptr(d_ld), 97, int(widths.max()), s)
+            torch.cuda.synchronize()
+            got = buf.cpu().numpy()
+            for b in range(B):
+                n = len(lists[b])
+                blk = got[dst_off[b]: dst_off[b] + n * ld[b]].reshape(n, ld[b])
+                assert np.array_equal(blk[:, :widths[b]], X[lists[b]][:, cl[b]])
+                assert np.all(blk[:, widths[b]:] == -3.0)
+            # scatter back into a fresh array (plain store, then accumulate with alpha)
+            Y0 = rng.standard_normal((nrows_src, ncols))
+            for acc, alpha in ((0, 1.0), (1, -0.5)):
+                dY = _dev(Y0)
+                call("skb_scatter_rows", B, ptr(d_io), ptr(d_idx), args_c[0], args_c[1], ncols, ptr(buf),
+                     ptr(d_do), ptr(d_ld), ptr(dY), ncols, acc, alpha, 97, int(widths.max()), s)
+                torch.cuda.synchronize()
+                ref = Y0.copy()
+                for b in range(B):
+                    if len(lists[b]) == 0:
+                        continue
+                    sub = X[lists[b]][:, cl[b]]
+                    if acc:
+                        ref[np.ix_(lists[b], cl[b])] = ref[np.ix_(lists[b], cl[b])] + alpha * sub
+                    else:
+                        ref[np.ix_(lists[b], cl[b])] = sub
+                assert np.array_equal(dY.cpu().numpy(), ref)
