@@ -31,7 +31,7 @@ HOST_SOURCES = {"host.cpp": []}
 CXX = os.environ.get("CXX", "g++")
 HOST_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-fno-fast-math", "-g"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
-          "--expt-relaxed-constexpr"]
+          "--expt-relaxed-constexpr", *os.environ.get("SKB_NVCC_EXTRA", "").split()]
 
 
 def _stale(objs) -> bool:
