@@ -376,6 +376,9 @@ int skb_engine_go(int64_t handle);
  * T, X_rr, LU, X_sr, X_rs_div, Xss (uint64 per box), ipiv, info, ratio, stash
  * (device address), st_us, st_ps, st_sp, gap, steps}; host arrays of the caller. */
 int skb_engine_set_update_table(int64_t handle, const uint8_t* todo, const int64_t* old_table);
+/* Grow the engine's stream-ordered pool and the default pool to the given
+ * reserved sizes now (no pool growth inside a later level pipeline).         */
+int skb_pool_prewarm(int64_t engine_bytes, int64_t default_bytes);
 /* Native level driver: the consumer side of the level loop (run_level
  * skel.py:340-361, compress_box (c) skel.py:316-338, the _finish_top sweep
  * skel.py:384-396) on the calling thread.  Per level: wait for the engine,

@@ -83,6 +83,7 @@ SIGNATURES = {
     "skb_engine_ack": [_i64, _i64],
     "skb_engine_set_update": [_i64, _vp, _vp, _vp],
     "skb_engine_set_update_table": [_i64, _vp, _vp],
+    "skb_pool_prewarm": [_i64, _i64],
     "skb_drv_run": [_i64, _vp, _f64, _vp],
     "skb_drv_level": [_i64, _i64, _vp, _vp],
     "skb_drv_free": [_i64],

@@ -523,30 +523,34 @@ int run_level(Engine& E, int64_t L, LevelOut& R) {
   return 0;
 }
 
+// The engine thread allocates from a stream-ordered pool of its own (never
+// shrinks), so its allocations never share a pool with the caller's.
+cudaMemPool_t engine_pool(int dev) {
+  static cudaMemPool_t pool = nullptr;
+  static std::mutex pm;
+  std::lock_guard<std::mutex> lk(pm);
+  if (!pool) {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    if (cudaMemPoolCreate(&pool, &props) == cudaSuccess) {
+      uint64_t thr = ~0ull;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      if (getenv("SKB_POOL_STRICT")) pool_strict(pool);   // debug, see ring_stage
+    } else {
+      pool = nullptr;
+    }
+  }
+  return pool;
+}
+
 void engine_main(Engine* E) {
   cudaSetDevice(E->dev);
   use_engine_side(true);
   use_engine_ring(true);          // descriptor uploads through the engine's own pinned ring
-  if (!getenv("SKB_ENGINE_SHARED_POOL")) {
-    static cudaMemPool_t pool = nullptr;
-    static std::mutex pm;
-    std::lock_guard<std::mutex> lk(pm);
-    if (!pool) {
-      cudaMemPoolProps props = {};
-      props.allocType = cudaMemAllocationTypePinned;
-      props.handleTypes = cudaMemHandleTypeNone;
-      props.location.type = cudaMemLocationTypeDevice;
-      props.location.id = E->dev;
-      if (cudaMemPoolCreate(&pool, &props) == cudaSuccess) {
-        uint64_t thr = ~0ull;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-        if (getenv("SKB_POOL_STRICT")) pool_strict(pool);   // debug, see ring_stage
-      } else {
-        pool = nullptr;
-      }
-    }
-    skb::tl_pool() = pool;
-  }
+  if (!getenv("SKB_ENGINE_SHARED_POOL")) skb::tl_pool() = engine_pool(E->dev);
   for (int64_t L = E->depth; L >= E->lev_lo; --L) {
     LevelOut& R = E->out[L];
     int rc = 0;
@@ -1200,6 +1204,33 @@ int drv_level(Driver& D, int64_t lev) {
 }  // namespace
 
 extern "C" {
+
+// Grow the engine's pool / the default stream-ordered pool to at least the
+// given reserved sizes now (one allocation + free each), so that no level of
+// a later factorization pays for pool growth -- a host-side stall of tens to
+// hundreds of milliseconds in the middle of the level pipeline.
+int skb_pool_prewarm(int64_t engine_bytes, int64_t default_bytes) {
+  int dev = 0;
+  SKB_RET(cudaGetDevice(&dev));
+  cudaMemPool_t pools[2] = {getenv("SKB_ENGINE_SHARED_POOL") ? nullptr : engine_pool(dev), nullptr};
+  SKB_RET(cudaDeviceGetDefaultMemPool(&pools[1], dev));
+  const int64_t want[2] = {engine_bytes, default_bytes};
+  for (int i = 0; i < 2; ++i) {
+    if (!pools[i] || want[i] <= 0) continue;
+    uint64_t thr = ~0ull, have = 0;
+    SKB_RET(cudaMemPoolSetAttribute(pools[i], cudaMemPoolAttrReleaseThreshold, &thr));
+    SKB_RET(cudaMemPoolGetAttribute(pools[i], cudaMemPoolAttrReservedMemCurrent, &have));
+    if ((int64_t)have >= want[i]) continue;
+    void* p = nullptr;
+    if (cudaMallocFromPoolAsync(&p, (size_t)want[i], pools[i], 0) != cudaSuccess) {
+      cudaGetLastError();                    // not enough memory: keep what is there
+      continue;
+    }
+    SKB_RET(cudaFreeAsync(p, 0));
+  }
+  SKB_RET(cudaStreamSynchronize(0));
+  return 0;
+}
 
 // Update mode with the previous factorization's level table (see OldLevel):
 // clean boxes' skeletons are read from it by the engine itself.

@@ -1707,6 +1707,24 @@ def _i64p(vals):
     return (ctypes.c_uint64 * len(vals))(*[int(v) for v in vals])
 
 
+_PREWARMED = [0]
+_PREWARM_KB = float(os.environ.get("SKB_PREWARM_KB_PER_DOF", "12"))
+
+
+def _prewarm_pools(lib, n_dofs: int):
+    """Reserve the engine's and the default stream-ordered pool for a problem
+    of n_dofs unknowns before the first level runs (ID stacks of ~3 levels in
+    flight: ~12 KB per unknown; Schur scratch half of that).  Pool growth in
+    the middle of a factorization stalls the host for 30-200 ms."""
+    if n_dofs <= _PREWARMED[0] or _PREWARM_KB <= 0:
+        return
+    _PREWARMED[0] = n_dofs
+    eb = int(_PREWARM_KB * 1024 * n_dofs)
+    rc = lib.skb_pool_prewarm(eb, eb // 2)
+    if rc:
+        raise _lib.SkbError(f"skb_pool_prewarm returned {rc}")
+
+
 class _Engine:
     """Host handle of the native level engine (csrc/engine.cu)."""
 
@@ -1714,6 +1732,7 @@ class _Engine:
         t, g = ctx.t, ctx.g
         nv = _tree_native(t)
         self.lib = _lib.load()
+        _prewarm_pools(self.lib, ctx.dpn * t.n_nodes)
         self._keep = [nv, store]
         self.children = np.ascontiguousarray(t.children, np.int64)
         self.px, self.py = ctx.px, ctx.py
@@ -1748,16 +1767,19 @@ class _Engine:
                                                cskel.ctypes.data)
             self.lib.skb_engine_go(self.h)
         # Run-ahead of the engine over the enqueued Schur stages.  On trees
-        # with heavy levels (> 512 boxes, cfg3) the engine starts level L only
-        # once level L+1's Schur stage is enqueued (lead 0): deeper run-ahead
-        # is ~5 % faster in the median but lets the compression chain's
-        # cluster kernels starve behind two levels of Schur / sweep work
-        # (0.3-1 s steps in ~1 of 40 factorizations, scripts/outliers.py).
-        # Lighter trees (cfg2: 26 vs 31 ms) and updates (a few boxes per level)
-        # run ahead unbounded.  SKB_ENGINE_LEAD=n overrides.  Levels without
-        # boxes to compress count as acknowledged (engine.cu).
+        # with heavy levels (> 512 boxes, cfg3) the engine enqueues level L's
+        # kernels once level L+2's Schur stage is enqueued (lead 1): bounded
+        # device memory (ID stacks of three levels in flight) at the speed of
+        # unbounded run-ahead (cfg3 160 vs 171 ms at lead 0).  With the pools
+        # reserved up front (_prewarm_pools) and the consumer loop native, 600
+        # consecutive cfg3 factorizations stayed within 166 ms
+        # (scripts/stall_hunt.py); the 0.3-1 s outliers seen with the Python
+        # consumer at lead >= 1 were pool growth and interpreter pauses.
+        # Lighter trees and updates (a few boxes per level) run ahead
+        # unbounded.  SKB_ENGINE_LEAD=n overrides.  Levels without boxes to
+        # compress count as acknowledged (engine.cu).
         heavy = update is None and int(np.diff(t.level_start).max(initial=0)) > 512
-        lead = int(os.environ.get("SKB_ENGINE_LEAD", "0" if heavy else "-1"))
+        lead = int(os.environ.get("SKB_ENGINE_LEAD", "1" if heavy else "-1"))
         if lead >= 0:
             self.lib.skb_engine_set_lead(self.h, lead)
         self.sizes = np.zeros(8, np.int64)
