@@ -451,6 +451,13 @@ int skb_host_far_lists(int64_t nb, const int64_t* idx, const double* center, con
 /* Proxy rings (kernels.py:263-273): pts = centre + r_p (cos, sin)(2 pi j / P),
  * radial normals about the ring centroid (kernels.py:340-342), weights
  * 2 pi r_p / P.  cs: P x 2 (cos, sin); pts, pn: nb x P x 2; pw: nb.          */
+/* Leaf active sets (skel.py:243-249) appended to `big` level by level; returns
+ * the fill (or -1: capacity).                                                */
+int64_t skb_host_leaf_actives(int64_t nbox, int64_t depth, const int64_t* lev, const uint8_t* is_leaf,
+                              const int64_t* node_start, const int64_t* node_cnt,
+                              const int64_t* level_nodes, const int64_t* level_nodes_off,
+                              const int64_t* level_start, int64_t dpn, int64_t* big, int64_t cap,
+                              int64_t* a_start, int64_t* a_len);
 int skb_host_proxies(int64_t nb, const int64_t* idx, const double* center, const double* hw,
                      double factor, int64_t P, const double* cs, double* pts, double* pn,
                      double* pw);

@@ -98,6 +98,7 @@ SIGNATURES = {
     "skb_host_far_lists": [_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _f64,
                            _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _i32],
     "skb_host_proxies": [_i64, _vp, _vp, _vp, _f64, _i64, _vp, _vp, _vp, _vp],
+    "skb_host_leaf_actives": [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _vp, _i64, _vp, _vp],
     "skb_host_init": [],
     "skb_tree_build": [_vp, _i64, _i64, _i64, _vp, _vp],
     "skb_tree_sizes": [_i64, _vp],
@@ -124,7 +125,7 @@ def load(path: str = LIB_PATH):
     for name, args in SIGNATURES.items():
         fn = getattr(lib, name)
         fn.argtypes = args
-        fn.restype = ctypes.c_int64 if name == "skb_debug_snap" else ctypes.c_int
+        fn.restype = ctypes.c_int64 if name in ("skb_debug_snap", "skb_host_leaf_actives") else ctypes.c_int
     lib.skb_host_init()
     _LIB = lib
     return lib

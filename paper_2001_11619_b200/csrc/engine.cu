@@ -869,6 +869,10 @@ struct DrvCfg {
   int64_t inc;
   uint64_t* xss;
   double floor;
+  // npairs < 0: (box, curve) membership computed here from the tree's node lists
+  const int64_t *level_nodes = nullptr, *level_nodes_off = nullptr, *node_start = nullptr,
+                *node_cnt = nullptr, *curve_off = nullptr;
+  int64_t ncurves = 0;
 };
 
 struct Driver {
@@ -881,6 +885,7 @@ struct Driver {
   bool shared_pinned = false;
   int64_t h2d = 0, d2h = 0;
   int64_t fail_level = -1;
+  std::vector<std::vector<int32_t>> curves;   // per box: curves with nodes in the box (ascending)
 };
 
 // process-wide pinned landing buffer of the pivot info (one driver at a time)
@@ -1172,7 +1177,37 @@ int drv_level(Driver& D, int64_t lev) {
     for (int64_t j = kk; j < n; ++j) rd[j - kk] = act[pm[j]];
   }
   L.cols.clear();
-  if (c.npairs > 0) {
+  if (c.npairs < 0) {
+    // curve membership leaves -> root (tree.py hole_pairs): a leaf holds the
+    // curves of its nodes, an internal box the union of its children's
+    std::vector<int32_t> tmp;
+    for (int64_t b = 0; b < B; ++b) {
+      const int64_t i = L.idx[b];
+      std::vector<int32_t>& cv = D.curves[i];
+      tmp.clear();
+      if (E.leaf[i]) {
+        const int64_t* nd = c.level_nodes + c.level_nodes_off[lev] + c.node_start[i];
+        int32_t last = -1;
+        for (int64_t t = 0; t < c.node_cnt[i]; ++t) {
+          const int32_t cur = (int32_t)(std::upper_bound(c.curve_off, c.curve_off + c.ncurves + 1, nd[t]) -
+                                        c.curve_off) - 1;
+          if (cur != last) { tmp.push_back(cur); last = cur; }
+        }
+      } else {
+        for (int qd = 0; qd < 4; ++qd) {
+          const int64_t ch = E.children[4 * i + qd];
+          if (ch >= 0) tmp.insert(tmp.end(), D.curves[ch].begin(), D.curves[ch].end());
+        }
+      }
+      std::sort(tmp.begin(), tmp.end());
+      tmp.erase(std::unique(tmp.begin(), tmp.end()), tmp.end());
+      cv = tmp;
+      for (int32_t cur : cv)
+        if (cur >= 1)
+          for (int e = 0; e < 3; ++e) L.cols.push_back(3 * (int64_t)(cur - 1) + e);
+      L.cols_off[b + 1] = (int64_t)L.cols.size();
+    }
+  } else if (c.npairs > 0) {
     for (int64_t b = 0; b < B; ++b) {
       const int64_t i = L.idx[b];
       const int64_t* lo = std::lower_bound(c.pair_box, c.pair_box + c.npairs, i);
@@ -1255,7 +1290,8 @@ int skb_engine_set_update_table(int64_t handle, const uint8_t* todo, const int64
 }
 
 // Run the consumer side of every level on the calling thread (see above).
-// cfg (int64 x 24): level stream, sweep stream, curvature (device), q, npairs,
+// cfg (int64 x 24; [20..23] = level_nodes, level_nodes_off, node_start, node_cnt and
+// [5], [6] = curve offsets, curve count when npairs < 0): level stream, sweep stream, curvature (device), q, npairs,
 // pair_box, pair_curve, parent, UH, PsiV, UH_div, schur, update, dmask, nqc, qc,
 // qmask (device), old level table, incremental sweep, xss (uint64 per box).
 // Returns 0, 100 (a box must migrate), 101/102 (clean box missing / changed)
@@ -1275,6 +1311,12 @@ int skb_drv_run(int64_t engine, const int64_t* cfg, double pivot_floor, int64_t*
   c.qmask_dev = (const uint8_t*)cfg[16]; c.old_table = (const int64_t*)cfg[17]; c.inc = cfg[18];
   c.xss = (uint64_t*)cfg[19];
   c.floor = pivot_floor;
+  if (c.npairs < 0) {
+    c.level_nodes = (const int64_t*)cfg[20]; c.level_nodes_off = (const int64_t*)cfg[21];
+    c.node_start = (const int64_t*)cfg[22]; c.node_cnt = (const int64_t*)cfg[23];
+    c.curve_off = (const int64_t*)cfg[5]; c.ncurves = cfg[6];
+    D->curves.resize(E->level_start[E->depth + 1]);
+  }
   D->lv.resize(E->depth + 1);
   const int64_t nbox = E->level_start[E->depth + 1];
   {

@@ -11,6 +11,8 @@
 #include <malloc.h>
 #include <math.h>
 #include <stdint.h>
+#include <chrono>
+#include <stdio.h>
 #include <string.h>
 
 #include <algorithm>
@@ -133,6 +135,32 @@ int skb_host_far_lists(int64_t nb, const int64_t* idx, const double* center, con
   return o <= cap ? 0 : 1;
 }
 
+// Leaf active sets (skel.py:243-249): DOFs dpn * node + {0 .. dpn-1} of each
+// leaf's owned nodes (ascending), appended to `big` level by level, leaves in
+// index order; a_start / a_len per box (0 for internal boxes).  Returns the
+// fill, or -1 when `big` (capacity cap) is too small.
+int64_t skb_host_leaf_actives(int64_t nbox, int64_t depth, const int64_t* lev, const uint8_t* is_leaf,
+                              const int64_t* node_start, const int64_t* node_cnt,
+                              const int64_t* level_nodes, const int64_t* level_nodes_off,
+                              const int64_t* level_start, int64_t dpn, int64_t* big, int64_t cap,
+                              int64_t* a_start, int64_t* a_len) {
+  int64_t fill = 0;
+  for (int64_t i = 0; i < nbox; ++i) { a_start[i] = 0; a_len[i] = 0; }
+  for (int64_t l = 0; l <= depth; ++l)
+    for (int64_t i = level_start[l]; i < level_start[l + 1]; ++i) {
+      if (!is_leaf[i]) continue;
+      (void)lev;
+      const int64_t* nd = level_nodes + level_nodes_off[l] + node_start[i];
+      const int64_t n = node_cnt[i];
+      if (fill + dpn * n > cap) return -1;
+      a_start[i] = fill;
+      a_len[i] = dpn * n;
+      for (int64_t t = 0; t < n; ++t)
+        for (int64_t e = 0; e < dpn; ++e) big[fill++] = dpn * nd[t] + e;
+    }
+  return fill;
+}
+
 // Proxy rings with radial normals about the ring centroid and weights
 // (kernels.py:263-273, 340-342); pts/pn: nb x P x 2, pw: nb.
 int skb_host_proxies(int64_t nb, const int64_t* idx, const double* center, const double* hw,
@@ -182,6 +210,14 @@ int skb_tree_build(const double* pos, int64_t N, int64_t leaf_cap, int64_t max_d
                    const double* root, int64_t* handle) {
   NativeTree* T = new NativeTree();
   T->n_nodes = N;
+  const bool tt_on = getenv("SKB_TREE_TIMING") != nullptr;
+  auto tt0 = std::chrono::steady_clock::now();
+  auto tt = [&](const char* nm) {
+    if (!tt_on) return;
+    auto t1 = std::chrono::steady_clock::now();
+    fprintf(stderr, " %s %.0f", nm, std::chrono::duration<double, std::micro>(t1 - tt0).count());
+    tt0 = t1;
+  };
   // level 0
   std::vector<int64_t> nxt_ix{0}, nxt_iy{0}, nxt_par{-1}, nxt_cnt{N}, nxt_nodes(N);
   std::vector<double> nxt_cx{root[0]}, nxt_cy{root[1]}, nxt_half{root[2]};
@@ -256,6 +292,7 @@ int skb_tree_build(const double* pos, int64_t N, int64_t leaf_cap, int64_t max_d
     nxt_nodes.swap(nnodes); nxt_cx.swap(ncx); nxt_cy.swap(ncy); nxt_half.swap(nhalf);
     ++l;
   }
+  tt("levels");
   T->depth = l;
   const int64_t nlev = l + 1;
   T->level_start.assign(nlev + 1, 0);
@@ -286,6 +323,7 @@ int skb_tree_build(const double* pos, int64_t N, int64_t leaf_cap, int64_t max_d
     T->level_nodes_off[q + 1] = T->level_nodes_off[q] + (int64_t)L.nodes.size();
     T->level_nodes.insert(T->level_nodes.end(), L.nodes.begin(), L.nodes.end());
   }
+  tt("flatten");
   // same-level neighbours in sorted key order (tree.py:70-81)
   T->nbr.assign(8 * nbox, -1);
   TreeView tv{T->center.data(), T->hw.data(), nullptr, T->lev.data(), T->ix.data(), T->iy.data(),
@@ -301,12 +339,15 @@ int skb_tree_build(const double* pos, int64_t N, int64_t leaf_cap, int64_t max_d
         ++s;
       }
   }
+  tt("nbr");
   T->node_leaf.assign(N, -1);
   for (int64_t g = 0; g < nbox; ++g)
     if (T->nchild[g] == 0) {
       const int64_t* nd = T->level_nodes.data() + T->level_nodes_off[T->lev[g]] + T->node_start[g];
       for (int64_t t = 0; t < T->node_cnt[g]; ++t) T->node_leaf[nd[t]] = g;
     }
+  tt("node_leaf");
+  if (tt_on) fprintf(stderr, " us\n");
   *handle = (int64_t)T;
   return 0;
 }

@@ -253,6 +253,21 @@ class ActStore:
             return
         self.a_start = np.zeros(nbox, np.int64)
         self.a_len = np.zeros(nbox, np.int64)
+        flat = getattr(t, "_level_nodes_flat", None)
+        if flat is not None:
+            # trees of the native build: leaf actives in the native host runtime
+            nv = _tree_native(t)
+            fill = _lib.load().skb_host_leaf_actives(
+                nbox, t.depth, nv["lev"].ctypes.data, nv["leaf"].ctypes.data,
+                t.node_start.ctypes.data, t.node_cnt.ctypes.data, flat.ctypes.data,
+                t._level_nodes_off.ctypes.data, nv["ls"].ctypes.data, dpn, self.big.ctypes.data,
+                len(self.big), self.a_start.ctypes.data, self.a_len.ctypes.data)
+            if fill < 0:
+                raise RuntimeError("active-set store too small")
+            self.fill = int(fill)
+            setattr(t, f"_store_init{dpn}",
+                    (self.fill, self.a_start.copy(), self.a_len.copy(), self.big[:self.fill].copy()))
+            return
         leaves = np.flatnonzero(t.is_leaf)
         # leaf actives: dofs 2*node + {0,1} of the sorted owned nodes (skel.py:243-249)
         for l in range(t.depth + 1):
@@ -1982,18 +1997,23 @@ def _run_levels_native(ctx: _Ctx, upd=None):
                 pipe = _make_pipe(ctx)
             ctx.pipe = pipe
             nv = _tree_native(t)
+            cfg = np.zeros(24, np.int64)
+            flat = getattr(t, "_level_nodes_flat", None)
             with _ht("N.pairs"):
-                if b.n_holes:
+                if b.n_holes and flat is not None:
+                    # (box, curve) membership from the tree's node lists, in the driver
+                    coff = np.ascontiguousarray(b.offsets, np.int64)
+                    cfg[4], cfg[5], cfg[6] = -1, coff.ctypes.data, len(coff) - 1
+                    cfg[20], cfg[21] = flat.ctypes.data, t._level_nodes_off.ctypes.data
+                    cfg[22], cfg[23] = t.node_start.ctypes.data, t.node_cnt.ctypes.data
+                elif b.n_holes:
                     pb, pc = t.hole_pairs(np.asarray(b.offsets, np.int64))
                     pb, pc = np.ascontiguousarray(pb, np.int64), np.ascontiguousarray(pc, np.int64)
-                else:
-                    pb = pc = np.zeros(1, np.int64)
-            cfg = np.zeros(24, np.int64)
+                    cfg[4], cfg[5], cfg[6] = len(pb), pb.ctypes.data, pc.ctypes.data
             cfg[0] = _stream()
             cfg[2] = ptr(ctx.g.kap)
             cfg[3] = pipe.q
-            cfg[4] = len(pb) if b.n_holes else 0
-            cfg[5], cfg[6], cfg[7] = pb.ctypes.data, pc.ctypes.data, nv["parent"].ctypes.data
+            cfg[7] = nv["parent"].ctypes.data
             if pipe.q:
                 cfg[1] = pipe.stream.cuda_stream
                 cfg[8], cfg[9], cfg[10], cfg[11] = ptr(pipe.UH), ptr(pipe.PsiV), ptr(pipe.UH_div), ptr(pipe.schur)

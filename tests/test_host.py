@@ -131,3 +131,18 @@ def test_native_dirty_sets_match_numpy():
         tn = refit_tree(t, nb.positions)
         assert dirty_set(t, tn, nb, rep, wl.proxy_factor) == dirty_set_np(t, tn, nb, rep, wl.proxy_factor)
         t = tn
+
+
+def test_native_leaf_actives_match_numpy():
+    """ActStore leaf actives (skel.py:243-249): the native host runtime on a
+    natively built tree equals the NumPy path on the NumPy-built tree."""
+    from paper_2001_11619_b200.skel import ActStore
+    from paper_2001_11619_b200.tree import build_tree_np
+    for wl in (configs.cfg1(), configs.mini_holes()):
+        b = wl.boundary
+        tn, tp = build_tree(b.positions, wl.leaf_cap), build_tree_np(b.positions, wl.leaf_cap)
+        for dpn in (1, 2):
+            a, r = ActStore(tn, dpn=dpn), ActStore(tp, dpn=dpn)
+            assert a.fill == r.fill
+            assert np.array_equal(a.big[:a.fill], r.big[:r.fill])
+            assert np.array_equal(a.a_start, r.a_start) and np.array_equal(a.a_len, r.a_len)
