@@ -186,6 +186,37 @@ def test_engine_matches_python_level_loop(monkeypatch):
     assert all(np.array_equal(out[False][2][k], out[True][2][k]) for k in out[False][2])
 
 
+def test_native_driver_matches_python_consumer(monkeypatch):
+    """The native level driver (csrc/engine.cu skb_drv_run: merge, layout, Schur
+    stage, sweeps, level lists in C++) and the Python consumer loop over the
+    same engine give bitwise identical factorizations and update chains on
+    cfg2, and the same per-level arrays (skeleton / redundant lists, hole
+    columns, ranks)."""
+    wl = configs.cfg2()
+    b = wl.boundary
+    rhs = wl.extra["rhs"]
+    seq = configs.hole_move_sequence(b, 3)
+    out = {}
+    for native in (False, True):
+        monkeypatch.setattr(skel, "_NATIVE_ON", native)
+        f = _factor(wl)
+        xs = [f.solve(rhs)]
+        lv = [(L.lev, L.k.copy(), L.sd.copy(), L.rd.copy(), L.cols.copy(), L.cols_off.copy()) for L in f.levels]
+        cur = f
+        for (h, d, nb, rep) in seq:
+            cur = update(cur, nb, rep)
+            xs.append(cur.solve(rhs))
+        lv += [(L.lev, L.k.copy(), L.sd.copy(), L.rd.copy(), L.cols.copy(), L.cols_off.copy()) for L in cur.levels]
+        out[native] = (xs, lv, cur.stats["dirty"])
+    for a, c in zip(out[False][0], out[True][0]):
+        assert np.array_equal(a, c)
+    assert out[False][2] == out[True][2]
+    for la, lc in zip(out[False][1], out[True][1]):
+        assert la[0] == lc[0]
+        for x, y in zip(la[1:], lc[1:]):
+            assert np.array_equal(x, y)
+
+
 def test_engine_repeatable_cfg2():
     """Repeated engine factorizations of cfg2 are bitwise identical."""
     wl = configs.cfg2()
