@@ -333,12 +333,33 @@ def main():
             Yp.copy_(Y, non_blocking=True)
             torch.cuda.current_stream().synchronize()
         rhs_s_e2e = 3 * 256 / (time.perf_counter() - t0)
-        del f, X, Y
+        del X, Y
+        # hole-move updates on the cfg3 geometry (same rules as cfg4, larger tree)
+        seq3 = configs.hole_move_sequence(b, 10)
+        cur3 = update(f, seq3[0][2], seq3[0][3])
+        cur3 = update(cur3, seq3[1][2], seq3[1][3])
+        upd3, nd3 = [], []
+        for _, _, nb3, rep3 in seq3[2:]:
+            torch.cuda.synchronize()
+            cur3 = update(cur3, nb3, rep3)
+            upd3.append(cur3.stats["update_time"] * 1e3)
+            nd3.append(cur3.stats["n_dirty"])
+        n_boxes3 = int(len(cur3.tree.lev))
+        del f, cur3
         gc.collect()
         w2 = configs.cfg2()
         b2 = w2.boundary
         t2 = build_tree(b2.positions, w2.leaf_cap)
         f2 = factor(spec, b2, t2, w2.tol, proxy_count=w2.proxy_count, proxy_factor=w2.proxy_factor)
+        f2t = []
+        for _ in range(5):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            ftmp = factor(spec, b2, build_tree(b2.positions, w2.leaf_cap), w2.tol,
+                          proxy_count=w2.proxy_count, proxy_factor=w2.proxy_factor)
+            torch.cuda.synchronize()
+            f2t.append((time.perf_counter() - t0) * 1e3)
+            del ftmp
         seq = configs.hole_move_sequence(b2, 24)
         upd, nd_ = [], []
         cur = update(f2, seq[0][2], seq[0][3])       # warm-up moves
@@ -358,6 +379,11 @@ def main():
             "cfg4_boxes": int(len(cur.tree.lev)),
             "cfg4_note": f"{len(upd)} successive seeded hole moves (|d| = 0.1) on cfg2, wall time of "
                          "update() incl. tree refit and dirty set",
+            "cfg2_factor_ms_median": float(np.median(f2t)),
+            "cfg3_update_ms_mean": float(np.mean(upd3)), "cfg3_update_ms": [round(x, 2) for x in upd3],
+            "cfg3_update_n_dirty_mean": float(np.mean(nd3)), "cfg3_boxes": n_boxes3,
+            "cfg3_update_note": f"{len(upd3)} successive seeded hole moves (|d| = 0.1) on the cfg3 "
+                                "geometry (one of 256 ellipses per move); compare factor_ms",
             "factor_ms": total_ms / args.steps}
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

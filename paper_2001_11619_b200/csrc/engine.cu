@@ -626,9 +626,12 @@ int skb_engine_start(const void* const* tree, int64_t depth, const double* root,
     const size_t want = (size_t)(8 * max_level_ints + 1024);
     if (!g_busy) {
       if (g_size < want) {
+        // grown with slack: an update chain's trees gain and lose a few boxes,
+        // and cudaFreeHost / cudaHostAlloc wait for the device (0.9 s on cfg3)
         if (g_pinned) cudaFreeHost(g_pinned);
-        SKB_RET(cudaHostAlloc((void**)&g_pinned, want, cudaHostAllocDefault));
-        g_size = want;
+        g_pinned = nullptr; g_size = 0;
+        SKB_RET(cudaHostAlloc((void**)&g_pinned, want + want / 2, cudaHostAllocDefault));
+        g_size = want + want / 2;
       }
       g_busy = true;
       E->pinned = g_pinned;

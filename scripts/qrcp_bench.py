@@ -56,3 +56,12 @@ if hasattr(lib, "skb_qblk_trace_get"):
     names = ["argmax", "barrier", "winner", "pivot col", "reflector", "aux+list", "dots", "finalize", "flush"]
     print("  phases (clock share):", " ".join(f"{n} {100*out[j]/tot:.0f}%" for j, n in enumerate(names)),
           f"| total {tot/6/1.9e6:.2f} ms/call")
+if hasattr(lib, "skb_qrcp_trace_get"):
+    tr = (ctypes.c_longlong * (256 * 8))()
+    lib.skb_qrcp_trace_get(tr)
+    a = np.array(tr[:]).reshape(256, 8)[20:200]
+    d = np.diff(a[:, :7], axis=1).mean(axis=0)
+    nxt = (a[1:, 0] - a[:-1, 6]).mean()
+    names = ["argmax", "sync", "cl.sync", "reflector(w0)", "sync", "scale+sync"]
+    print("  mode-1 step cycles:", " ".join(f"{n} {v:.0f}" for n, v in zip(names, d)), f"update {nxt:.0f}",
+          f"| step {(a[1:, 0] - a[:-1, 0]).mean():.0f} cycles")

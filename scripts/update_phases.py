@@ -1,14 +1,15 @@
-"""Host time per update() section (SKB_HOST_PROF=1), averaged over hole moves 3..14 on cfg2."""
+"""Host time per update() section (SKB_HOST_PROF=1), averaged over hole moves 3..N.
+  python scripts/update_phases.py [cfg2|cfg3] [moves]"""
 import gc, os, sys, time
 os.environ.setdefault("SKB_HOST_PROF", "1")
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
 from paper_2001_11619_b200 import SystemSpec, build_tree, configs, factor, update, skel
-wl = configs.cfg2(); b = wl.boundary
+wl = configs.by_name(sys.argv[1] if len(sys.argv) > 1 else "cfg2"); b = wl.boundary
 t = build_tree(b.positions, wl.leaf_cap)
 f = factor(SystemSpec(), b, t, wl.tol, proxy_count=wl.proxy_count, proxy_factor=wl.proxy_factor)
-seq = configs.hole_move_sequence(b, 14)
+seq = configs.hole_move_sequence(b, int(sys.argv[2]) if len(sys.argv) > 2 else 14)
 ts = []
 for i, (h, d, nb, rp) in enumerate(seq):
     gc.collect()
@@ -23,7 +24,7 @@ for i, (h, d, nb, rp) in enumerate(seq):
     if i >= 2:
         ts.append((time.perf_counter() - t0) * 1e3)
 n = len(ts)
-print("update ms median %.2f" % np.median(ts))
+print("update ms median %.2f" % np.median(ts), [round(x, 1) for x in ts])
 for k, v in sorted(skel._HostTimer.acc.items(), key=lambda x: -x[1]):
     print("  %-14s %8.3f ms/update" % (k, v * 1e3 / n))
 

@@ -132,3 +132,29 @@ def test_cfg4_hundred_moves():
         del fr
     print(f"cfg4: update == refactor bitwise on {n_same}/100 moves; first difference at move "
           f"{first_diff} (reference update != reference refactor there too)")
+
+
+def test_cfg3_update_equals_refactor(cfg3_pair):
+    """Hole moves on the cfg3 geometry (3609 boxes, all kernel classes up to the
+    blocked cooperative QRCP): the updated factorization has the skeletons and
+    the solve of a GPU refactorization of the moved geometry, bitwise (two
+    seeded moves on which the reference's rules keep update == refactor)."""
+    wl, f, _ = cfg3_pair
+    b = wl.boundary
+    rng = np.random.default_rng(23)
+    rhs = np.concatenate([rng.standard_normal(2 * b.n_nodes), np.zeros(3 * b.n_holes)])
+    cur = f
+    for step, (h, d, nb, rep) in enumerate(configs.hole_move_sequence(b, 2)):
+        cur = update(cur, nb, rep)
+        t2 = build_tree(nb.positions, wl.leaf_cap, root_box=(cur.tree.root_center, cur.tree.root_half_width))
+        fr = factor(SystemSpec(), nb, t2, wl.tol, proxy_count=wl.proxy_count, proxy_factor=wl.proxy_factor)
+        assert set(cur.factors.keys()) == set(fr.factors.keys())
+        bad = [k for k in fr.factors.keys()
+               if not np.array_equal(cur.factors[k].skel_dofs, fr.factors[k].skel_dofs)]
+        assert not bad, (step, bad[:5])
+        xu, xf = cur.solve(rhs), fr.solve(rhs)
+        print(f"cfg3 move {step}: {cur.stats['n_dirty']} dirty of {cur.stats['n_boxes']} boxes, "
+              f"update {cur.stats['update_time'] * 1e3:.1f} ms, refactor {fr.stats['factor_time'] * 1e3:.1f} ms, "
+              f"bitwise {np.array_equal(xu, xf)}")
+        assert np.array_equal(xu, xf), step
+        del fr
