@@ -12,6 +12,8 @@
 #include <math.h>
 #include <stdint.h>
 #include <chrono>
+#include <functional>
+#include <thread>
 #include <stdio.h>
 #include <string.h>
 
@@ -218,80 +220,125 @@ int skb_tree_build(const double* pos, int64_t N, int64_t leaf_cap, int64_t max_d
     fprintf(stderr, " %s %.0f", nm, std::chrono::duration<double, std::micro>(t1 - tt0).count());
     tt0 = t1;
   };
-  // level 0
-  std::vector<int64_t> nxt_ix{0}, nxt_iy{0}, nxt_par{-1}, nxt_cnt{N}, nxt_nodes(N);
-  std::vector<double> nxt_cx{root[0]}, nxt_cy{root[1]}, nxt_half{root[2]};
-  for (int64_t i = 0; i < N; ++i) nxt_nodes[i] = i;
-  int64_t l = 0;
-  std::vector<std::vector<int64_t>> L_children;   // per level, nb x 4 (local child idx, by quadrant)
-  struct Lv { std::vector<int64_t> ix, iy, par, cnt, nodes; std::vector<double> cx, cy, half; };
+  // Level-by-level split.  The node lists of all levels are written straight
+  // into the flat level_nodes array (level l at level_nodes_off[l]); a level's
+  // nodes are the nodes of the split boxes of the level above, so only those
+  // are visited.  Working indices are 32-bit (N < 2^31).
+  struct Lv { std::vector<int64_t> ix, iy, par, cnt; std::vector<double> cx, cy, half; int64_t noff; };
   std::vector<Lv> levels;
   levels.reserve(64);
+  std::vector<std::vector<int64_t>> L_children;   // per level, nb x 4 (local child idx, by quadrant)
+  T->level_nodes.reserve((size_t)N * 14);     // ~ nodes x levels (grows if a tree is deeper)
+  T->level_nodes.resize((size_t)N);
+  for (int64_t i = 0; i < N; ++i) T->level_nodes[i] = i;
+  T->level_nodes_off.assign(1, 0);
+  {
+    Lv L0;
+    L0.ix = {0}; L0.iy = {0}; L0.par = {-1}; L0.cnt = {N};
+    L0.cx = {root[0]}; L0.cy = {root[1]}; L0.half = {root[2]};
+    L0.noff = 0;
+    levels.push_back(std::move(L0));
+  }
+  std::vector<uint8_t> quad((size_t)N);
+  double ph[4] = {0, 0, 0, 0};
+  auto pnow = [] { return std::chrono::steady_clock::now(); };
+  auto pus = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+  std::vector<int64_t> start, qcnt, slot, fillp;
+  struct Kid { int64_t code, b, q; };
+  std::vector<Kid> kids;
+  int64_t l = 0;
   while (true) {
-    const int64_t nb = (int64_t)nxt_ix.size();
-    levels.push_back(Lv{std::move(nxt_ix), std::move(nxt_iy), std::move(nxt_par),
-                        std::move(nxt_cnt), std::move(nxt_nodes), std::move(nxt_cx),
-                        std::move(nxt_cy), std::move(nxt_half)});
     const Lv& cur = levels.back();
+    const int64_t nb = (int64_t)cur.ix.size();
     const auto& ix = cur.ix; const auto& iy = cur.iy; const auto& cnt = cur.cnt;
-    const auto& nodes = cur.nodes; const auto& cx = cur.cx; const auto& cy = cur.cy;
-    const auto& half = cur.half;
+    const auto& cx = cur.cx; const auto& cy = cur.cy; const auto& half = cur.half;
+    const int64_t* nodes = T->level_nodes.data() + cur.noff;
+    int64_t nn = 0;
+    for (int64_t b = 0; b < nb; ++b) nn += cnt[b];
+    T->level_nodes_off.push_back(cur.noff + nn);
     std::vector<int64_t> ch(4 * nb, -1);
-    std::vector<int64_t> start(nb + 1, 0);
-    for (int64_t b = 0; b < nb; ++b) start[b + 1] = start[b] + cnt[b];
     bool any = false;
     for (int64_t b = 0; b < nb; ++b) any |= (cnt[b] > leaf_cap) && (l < max_depth);
-    if (!any) { L_children.push_back(ch); break; }
+    if (!any) { L_children.push_back(std::move(ch)); break; }
     // children of all split boxes, keyed by code = cix * side + ciy; nodes of
     // a child keep their order in the parent (counting sort per quadrant)
     const int64_t side = (int64_t)1 << (l + 1);
-    std::vector<int64_t> quad(nodes.size());
-    std::vector<int64_t> qcnt(4 * nb, 0);
+    start.assign(nb + 1, 0);
+    for (int64_t b = 0; b < nb; ++b) start[b + 1] = start[b] + cnt[b];
+    qcnt.assign(4 * nb, 0);
+    int64_t nnext = 0;
+    auto p0 = pnow();
     for (int64_t b = 0; b < nb; ++b) {
       if (!((cnt[b] > leaf_cap) && (l < max_depth))) continue;
+      const double bx = cx[b], by = cy[b];
+      // counters in registers (a per-quadrant array increment would serialise
+      // the loop on store-to-load forwarding)
+      int64_t ne = 0, nn_ = 0, nne = 0;
       for (int64_t t = start[b]; t < start[b + 1]; ++t) {
-        const int64_t nd = nodes[t];
-        const int64_t dx = pos[2 * nd] >= cx[b] ? 1 : 0;
-        const int64_t dy = pos[2 * nd + 1] >= cy[b] ? 1 : 0;
-        quad[t] = dx + 2 * dy;
-        qcnt[4 * b + quad[t]]++;
+        const double* pp = pos + 2 * nodes[t];
+        const int dx = pp[0] >= bx ? 1 : 0, dy = pp[1] >= by ? 1 : 0;
+        quad[t] = (uint8_t)(dx + 2 * dy);
+        ne += dx; nn_ += dy; nne += dx & dy;
       }
+      qcnt[4 * b + 3] = nne;
+      qcnt[4 * b + 1] = ne - nne;
+      qcnt[4 * b + 2] = nn_ - nne;
+      qcnt[4 * b + 0] = cnt[b] - ne - nn_ + nne;
     }
-    struct Kid { int64_t code, b, q; };
-    std::vector<Kid> kids;
+    for (int64_t b = 0; b < nb; ++b)
+      if ((cnt[b] > leaf_cap) && (l < max_depth)) nnext += cnt[b];
+    auto p1 = pnow();
+    kids.clear();
     for (int64_t b = 0; b < nb; ++b)
       for (int64_t q = 0; q < 4; ++q)
         if (qcnt[4 * b + q] > 0)
           kids.push_back(Kid{(2 * ix[b] + (q & 1)) * side + (2 * iy[b] + (q >> 1)), b, q});
     std::sort(kids.begin(), kids.end(), [](const Kid& a, const Kid& b) { return a.code < b.code; });
     const size_t nk = kids.size();
-    std::vector<int64_t> nix(nk), niy(nk), npar(nk), ncnt(nk), kstart(nk + 1, 0);
-    std::vector<double> ncx(nk), ncy(nk), nhalf(nk);
-    std::vector<int64_t> slot(4 * nb, -1);
+    Lv nx;
+    nx.ix.resize(nk); nx.iy.resize(nk); nx.par.resize(nk); nx.cnt.resize(nk);
+    nx.cx.resize(nk); nx.cy.resize(nk); nx.half.resize(nk);
+    nx.noff = cur.noff + nn;
+    slot.assign(4 * nb, -1);
+    fillp.assign(nk + 1, 0);
     for (size_t c = 0; c < nk; ++c) {
       const int64_t b = kids[c].b, q = kids[c].q, dx = q & 1, dy = q >> 1;
       ch[4 * b + q] = (int64_t)c;
       slot[4 * b + q] = (int64_t)c;
-      nix[c] = 2 * ix[b] + dx;
-      niy[c] = 2 * iy[b] + dy;
-      npar[c] = b;
-      ncnt[c] = qcnt[4 * b + q];
-      kstart[c + 1] = kstart[c] + ncnt[c];
-      ncx[c] = cx[b] + ((double)dx - 0.5) * half[b];
-      ncy[c] = cy[b] + ((double)dy - 0.5) * half[b];
-      nhalf[c] = half[b] / 2;
+      nx.ix[c] = 2 * ix[b] + dx;
+      nx.iy[c] = 2 * iy[b] + dy;
+      nx.par[c] = b;
+      nx.cnt[c] = qcnt[4 * b + q];
+      fillp[c + 1] = fillp[c] + nx.cnt[c];
+      nx.cx[c] = cx[b] + ((double)dx - 0.5) * half[b];
+      nx.cy[c] = cy[b] + ((double)dy - 0.5) * half[b];
+      nx.half[c] = half[b] / 2;
     }
-    std::vector<int64_t> nnodes(kstart[nk]);
-    std::vector<int64_t> fillp(kstart.begin(), kstart.end() - 1);
+    auto p2 = pnow();
+    const size_t base = (size_t)nx.noff;
+    T->level_nodes.resize(base + (size_t)nnext);
+    auto p3 = pnow();
+    nodes = T->level_nodes.data() + cur.noff;          // (resize may have moved the array)
+    int64_t* out = T->level_nodes.data() + base;
     for (int64_t b = 0; b < nb; ++b) {
       if (!((cnt[b] > leaf_cap) && (l < max_depth))) continue;
-      for (int64_t t = start[b]; t < start[b + 1]; ++t) nnodes[fillp[slot[4 * b + quad[t]]]++] = nodes[t];
+      int64_t f[4];
+      for (int q = 0; q < 4; ++q) f[q] = slot[4 * b + q] >= 0 ? fillp[slot[4 * b + q]] : 0;
+      int64_t f0 = f[0], f1 = f[1], f2 = f[2], f3 = f[3];     // write cursors in registers
+      for (int64_t t = start[b]; t < start[b + 1]; ++t) {
+        const int q = quad[t];
+        const int64_t at = q == 0 ? f0 : (q == 1 ? f1 : (q == 2 ? f2 : f3));
+        out[at] = nodes[t];
+        f0 += q == 0; f1 += q == 1; f2 += q == 2; f3 += q == 3;
+      }
     }
-    L_children.push_back(ch);
-    nxt_ix.swap(nix); nxt_iy.swap(niy); nxt_par.swap(npar); nxt_cnt.swap(ncnt);
-    nxt_nodes.swap(nnodes); nxt_cx.swap(ncx); nxt_cy.swap(ncy); nxt_half.swap(nhalf);
+    auto p4 = pnow();
+    ph[0] += pus(p0, p1); ph[1] += pus(p1, p2); ph[2] += pus(p2, p3); ph[3] += pus(p3, p4);
+    L_children.push_back(std::move(ch));
+    levels.push_back(std::move(nx));
     ++l;
   }
+  if (tt_on) fprintf(stderr, " [quad %.0f kids %.0f resize %.0f scatter %.0f]", ph[0], ph[1], ph[2], ph[3]);
   tt("levels");
   T->depth = l;
   const int64_t nlev = l + 1;
@@ -302,7 +349,6 @@ int skb_tree_build(const double* pos, int64_t N, int64_t leaf_cap, int64_t max_d
   T->lev.resize(nbox); T->ix.resize(nbox); T->iy.resize(nbox); T->parent.resize(nbox);
   T->center.resize(2 * nbox); T->hw.resize(nbox); T->children.assign(4 * nbox, -1);
   T->nchild.assign(nbox, 0); T->node_start.resize(nbox); T->node_cnt.resize(nbox);
-  T->level_nodes_off.assign(nlev + 1, 0);
   for (int64_t q = 0; q < nlev; ++q) {
     const Lv& L = levels[q];
     const int64_t base = T->level_start[q];
@@ -320,24 +366,40 @@ int skb_tree_build(const double* pos, int64_t N, int64_t leaf_cap, int64_t max_d
       }
       T->nchild[g] = nc;
     }
-    T->level_nodes_off[q + 1] = T->level_nodes_off[q] + (int64_t)L.nodes.size();
-    T->level_nodes.insert(T->level_nodes.end(), L.nodes.begin(), L.nodes.end());
   }
   tt("flatten");
-  // same-level neighbours in sorted key order (tree.py:70-81)
+  // same-level neighbours in sorted key order (tree.py:70-81): a box's three
+  // neighbours in cell column ix + dx are consecutive keys, found by one
+  // binary search per column restricted to the level
   T->nbr.assign(8 * nbox, -1);
-  TreeView tv{T->center.data(), T->hw.data(), nullptr, T->lev.data(), T->ix.data(), T->iy.data(),
-              nullptr, T->level_start.data(), T->depth, root[0], root[1], root[2]};
-  for (int64_t g = 0; g < nbox; ++g) {
-    const int64_t q = T->lev[g], side = (int64_t)1 << q;
-    int s = 0;
-    for (int dx = -1; dx <= 1; ++dx)
-      for (int dy = -1; dy <= 1; ++dy) {
-        if (!dx && !dy) continue;
-        const int64_t nx = T->ix[g] + dx, ny = T->iy[g] + dy;
-        if (nx >= 0 && ny >= 0 && nx < side && ny < side) T->nbr[8 * g + s] = find_code(tv, q, nx * side + ny);
-        ++s;
+  for (int64_t q = 0; q < nlev; ++q) {
+    const int64_t lo0 = T->level_start[q], hi0 = T->level_start[q + 1], side = (int64_t)1 << q;
+    const int64_t* ixp = T->ix.data();
+    const int64_t* iyp = T->iy.data();
+    for (int64_t g = lo0; g < hi0; ++g) {
+      for (int dx = -1; dx <= 1; ++dx) {
+        const int64_t nxc = ixp[g] + dx;
+        if (nxc < 0 || nxc >= side) continue;
+        const int64_t ylo = iyp[g] - 1;
+        // first box of the level with key >= nxc * side + max(ylo, 0)
+        const int64_t want = nxc * side + (ylo < 0 ? 0 : ylo);
+        int64_t lo = lo0, hi = hi0;
+        if (dx == 0) { lo = g > lo0 ? g - 1 : g; hi = g + 2 < hi0 ? g + 2 : hi0; }   // own column: adjacent keys
+        while (lo < hi) {
+          const int64_t mid = (lo + hi) >> 1;
+          if (ixp[mid] * side + iyp[mid] < want) lo = mid + 1;
+          else hi = mid;
+        }
+        for (int64_t j = lo; j < hi0 && ixp[j] == nxc && iyp[j] <= iyp[g] + 1; ++j) {
+          const int dy = (int)(iyp[j] - iyp[g]);
+          if (dx == 0 && dy == 0) continue;
+          // slot order of the reference loop: dx outer, dy inner, (0, 0) skipped
+          int sl = (dx + 1) * 3 + (dy + 1);
+          if (sl > 4) --sl;
+          T->nbr[8 * g + sl] = j;
+        }
       }
+    }
   }
   tt("nbr");
   T->node_leaf.assign(N, -1);
