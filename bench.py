@@ -380,7 +380,8 @@ def main():
             "cfg4_note": f"{len(upd)} successive seeded hole moves (|d| = 0.1) on cfg2, wall time of "
                          "update() incl. tree refit and dirty set",
             "cfg2_factor_ms_median": float(np.median(f2t)),
-            "cfg3_update_ms_mean": float(np.mean(upd3)), "cfg3_update_ms": [round(x, 2) for x in upd3],
+            "cfg3_update_ms_mean": float(np.mean(upd3)), "cfg3_update_ms_median": float(np.median(upd3)),
+            "cfg3_update_ms": [round(x, 2) for x in upd3],
             "cfg3_update_n_dirty_mean": float(np.mean(nd3)), "cfg3_boxes": n_boxes3,
             "cfg3_update_note": f"{len(upd3)} successive seeded hole moves (|d| = 0.1) on the cfg3 "
                                 "geometry (one of 256 ellipses per move); compare factor_ms",
