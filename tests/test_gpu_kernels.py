@@ -496,3 +496,52 @@ def test_move_kernels_bit_exact():
                     else:
                         ref[np.ix_(lists[b], cl[b])] = sub
                 assert np.array_equal(dY.cpu().numpy(), ref)
+
+
+def _qrcp_call(mats, tol):
+    """skb_qrcp_id_batched on a list of equal-shape host matrices; returns (perm, k, steps, diag)."""
+    nbox = len(mats)
+    m, n = mats[0].shape
+    flat = np.concatenate([A.T.ravel() for A in mats])
+    d = _dev(flat)
+    A = (d.data_ptr() + 8 * np.arange(nbox, dtype=np.int64) * (m * n)).astype(np.int64)
+    act_off = np.arange(nbox + 1, dtype=np.int64) * n
+    perm = torch.empty(nbox * n, dtype=torch.int32, device="cuda")
+    diag = torch.empty(nbox * n, dtype=torch.float64, device="cuda")
+    ko = torch.empty(2 * nbox, dtype=torch.int32, device="cuda")
+    gap = torch.empty(nbox, dtype=torch.float64, device="cuda")
+    call("skb_qrcp_id_batched", nbox, np.full(nbox, m, np.int64), np.full(nbox, n, np.int64),
+         np.full(nbox, m, np.int64), A, np.zeros(nbox, np.int64), tol, act_off, perm, diag, ko,
+         ko.data_ptr() + 4 * nbox, gap, skel._stream())
+    torch.cuda.synchronize()
+    kk = ko.cpu().numpy()
+    return perm.cpu().numpy().reshape(nbox, n), kk[:nbox], kk[nbox:], diag.cpu().numpy().reshape(nbox, n)
+
+
+def test_qrcp_blocked_cooperative_vs_lapack():
+    """k_qrcp_blk (dlaqps-style delayed updates, R in L2, cooperative launch):
+    on matrices with a decaying spectrum whose R does not fit a 16-CTA cluster,
+    rank and skeleton (order included) equal SciPy's dgeqp3 at the tolerance,
+    |diag R| matches to 1e-12 |R_00|, and repeated runs are bitwise identical."""
+    rng = np.random.default_rng(5)
+    tol, m, n, k = 1e-8, 1400, 900, 90
+    mats = []
+    for _ in range(2):
+        U, _ = np.linalg.qr(rng.standard_normal((m, n)))
+        V, _ = np.linalg.qr(rng.standard_normal((n, n)))
+        mats.append((U * 10.0 ** (-8.0 * np.arange(n) / k)) @ V.T)
+    runs = [_qrcp_call(mats, tol) for _ in range(3)]
+    pm, kk, steps, dg = runs[0]
+    for other in runs[1:]:
+        assert np.array_equal(other[1], kk) and np.array_equal(other[2], steps)
+        for b in range(2):
+            assert np.array_equal(other[0][b, :kk[b]], pm[b, :kk[b]])
+            assert np.array_equal(other[3][b, :steps[b]], dg[b, :steps[b]])
+    for b, A in enumerate(mats):
+        _, R, p = sla.qr(A, mode="economic", pivoting=True)
+        d = np.abs(np.diag(R))
+        kr = int(np.count_nonzero(d > tol * d[0]))
+        assert kk[b] == kr
+        assert np.array_equal(pm[b, :kr], p[:kr])
+        assert np.allclose(dg[b, :kr], d[:kr], rtol=1e-9, atol=1e-12 * d[0])   # absolute: eps-level in |A|
+        assert sorted(pm[b]) == list(range(n))          # a permutation: every column listed once
