@@ -400,6 +400,9 @@ int skb_drv_run(int64_t engine, const int64_t* cfg, double pivot_ratio_floor, in
  * (int32), k, steps, gap, info, ratio, clean_pos, T, X_rr, LU, X_sr, X_rs_div,
  * Xss, ipiv, sd_off, sd, rd_off, rd, cols_off, cols, st_us, st_ps, st_sp,
  * new_pos}.  The device allocations (skb_dev_alloc pool) become the caller's. */
+/* Wait for every level's X_RR pivot info (skb_drv_run only polls it): 0, or 100
+ * = a box must migrate.  Call before skb_drv_level.                           */
+int skb_drv_resolve(int64_t handle);
 int skb_drv_level(int64_t handle, int64_t lev, int64_t* sizes, int64_t* ptrs);
 int skb_drv_free(int64_t handle);
 /* stream waits for level L's compression */

@@ -85,6 +85,7 @@ SIGNATURES = {
     "skb_engine_set_update_table": [_i64, _vp, _vp],
     "skb_pool_prewarm": [_i64, _i64],
     "skb_drv_run": [_i64, _vp, _f64, _vp],
+    "skb_drv_resolve": [_i64],
     "skb_drv_level": [_i64, _i64, _vp, _vp],
     "skb_drv_free": [_i64],
     "skb_engine_go": [_i64],

@@ -1352,7 +1352,21 @@ int skb_drv_run(int64_t engine, const int64_t* cfg, double pivot_floor, int64_t*
     int rc;
     if ((rc = drv_sweep(*D, *D->prev))) { D->fail_level = D->prev->lev; return rc; }
   }
+  // pivot info already landed is checked now; the rest by skb_drv_resolve (the
+  // caller first enqueues its root block / corner LU behind the last level)
   for (int64_t L = E->depth; L >= 1; --L) {
+    if (!D->lv[L].used) continue;
+    const int rc = drv_resolve(*D, D->lv[L], false);
+    if (rc) { D->fail_level = L; return rc; }
+  }
+  return 0;
+}
+
+// Wait for the X_RR pivot info of every level (the Schur stages on the
+// device) and apply the migration trigger: 0, or 100 = a box must migrate.
+int skb_drv_resolve(int64_t handle) {
+  Driver* D = (Driver*)handle;
+  for (int64_t L = (int64_t)D->lv.size() - 1; L >= 1; --L) {
     if (!D->lv[L].used) continue;
     const int rc = drv_resolve(*D, D->lv[L]);
     if (rc) { D->fail_level = L; return rc; }

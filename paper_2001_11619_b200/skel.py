@@ -2054,6 +2054,12 @@ def _native_collect(ctx: _Ctx, handle):
     t = ctx.t
     sizes, ptrs = np.zeros(24, np.int64), np.zeros(32, np.int64)
     try:
+        with _ht("N.resolve"):
+            rc = lib.skb_drv_resolve(drv.value)        # waits for the last Schur stages
+        if rc == 100:
+            raise _EngineAbort()
+        if rc:
+            raise _lib.SkbError(f"skb_drv_resolve returned {rc}")
         with _ht("N.collect"):
             levels = [_native_level(lib, drv.value, lev, t, old, sizes, ptrs)
                       for lev in range(t.depth, 0, -1)]
@@ -2061,6 +2067,7 @@ def _native_collect(ctx: _Ctx, handle):
         IO["d2h"] += int(sizes[19])
     finally:
         lib.skb_drv_free(drv.value)
+        drv.value = 0                                  # (the caller's cleanup sees it released)
     return levels
 
 
@@ -2335,6 +2342,47 @@ def _drain(ctx: "_Ctx"):
     torch.cuda.current_stream().wait_stream(ctx.sstream)
 
 
+def _levels_and_top(make_ctx, upd=None, reuse=None, dirty=None):
+    """Level loop and _finish_top: the native engine + driver first; a migration
+    (R -> S, skel.py:317-330) or a clean box without a twin aborts that run and
+    the Python level loop redoes everything on a fresh context."""
+    attempts = (True, False) if (_ENGINE_ON and not _Prof.enabled) else (False,)
+    prev = None
+    for fast in attempts:
+        if prev is not None:
+            _drain(prev)
+        with _ht("ctx"):
+            ctx = make_ctx()
+        prev = ctx
+        levels = nh = None
+        try:
+            with _ht("run_levels"):
+                if fast and _NATIVE_ON:
+                    store, nh = _run_levels_native(ctx, upd=upd)
+                elif fast and upd is not None:
+                    levels, store, _ = _run_levels_engine_update(ctx, reuse, dirty)
+                elif fast:
+                    levels, store, _ = _run_levels_engine(ctx)
+                else:
+                    levels, store, _ = _run_levels(ctx, reuse=reuse, dirty=dirty)
+            got = []
+            collect = (lambda: got.append(_native_collect(ctx, nh))) if nh is not None else None
+            try:
+                with _ht("finish_top"):
+                    top = _finish_top(ctx, levels, store, ctx.pipe, before_sync=collect)
+            finally:
+                if nh is not None and not got and nh[1].value:
+                    nh[0].skb_drv_free(nh[1].value)     # (collect frees it otherwise)
+                    nh[1].value = 0
+            if nh is not None:
+                levels = got[0]
+            return ctx, levels, top
+        except _EngineAbort:
+            if not fast:
+                raise
+    raise RuntimeError("unreachable")
+
+
 def factor(spec, b, t: Tree, tol: float, workers: int = 1,
            proxy_count: int = DEFAULT_PROXY_COUNT, proxy_factor: float = DEFAULT_PROXY_FACTOR,
            propagate_zeros: bool = False) -> Factorization:
@@ -2348,34 +2396,9 @@ def factor(spec, b, t: Tree, tol: float, workers: int = 1,
     torch.cuda.synchronize()
     _DevSlab.flush()
     t0 = time.perf_counter()
-    with _ht("ctx"):
-        ctx = _Ctx(spec, b, t, tol, proxy_count, proxy_factor)
     with torch.cuda.stream(_compress_stream()):
-        with _ht("run_levels"):
-            levels = nh = None
-            if _ENGINE_ON and not _Prof.enabled:
-                try:
-                    if _NATIVE_ON:
-                        store, nh = _run_levels_native(ctx)
-                    else:
-                        levels, store, _ = _run_levels_engine(ctx)
-                except _EngineAbort:
-                    _drain(ctx)
-                    ctx = _Ctx(spec, b, t, tol, proxy_count, proxy_factor)
-                    levels = nh = None
-            if levels is None and nh is None:
-                levels, store, _ = _run_levels(ctx)
-        with _ht("finish_top"):
-            got = []
-            collect = (lambda: got.append(_native_collect(ctx, nh))) if nh is not None else None
-            try:
-                rd, E_root, top, ipiv, UH, PsiV, UH_div, q, ratio = _finish_top(
-                    ctx, levels, store, ctx.pipe, before_sync=collect)
-            finally:
-                if nh is not None and not got:
-                    nh[0].skb_drv_free(nh[1].value)
-            if nh is not None:
-                levels = got[0]
+        ctx, levels, (rd, E_root, top, ipiv, UH, PsiV, UH_div, q, ratio) = _levels_and_top(
+            lambda: _Ctx(spec, b, t, tol, proxy_count, proxy_factor))
     with _ht("final_sync"):
         torch.cuda.synchronize()
     stats = {"k_per_level": {L.lev: int(L.k.max(initial=0)) for L in levels},
@@ -2403,37 +2426,17 @@ def update(fct: Factorization, b_new, report, workers: int = 1) -> Factorization
     if not np.array_equal(report.old_to_new, np.arange(len(report.old_to_new))):
         raise NotImplementedError("only DOF-preserving edits (hole moves) are supported")
     old = {L.lev: L for L in fct.levels}
-    with _ht("U.ctx"):
+
+    def make_ctx():
         ctx = _Ctx(fct.spec, b_new, t_new, fct.tol, fct.proxy_count, fct.proxy_factor)
         ctx.upd_old = (fct, dmask)
         ctx.g                                           # geometry upload
         torch.cuda.current_stream().synchronize()
+        return ctx
+
     with torch.cuda.stream(_compress_stream()):
-        levels = nh = None
-        if _ENGINE_ON and not _Prof.enabled:
-            try:
-                if _NATIVE_ON:
-                    store, nh = _run_levels_native(ctx, upd=(fct, dmask))
-                else:
-                    levels, store, n_recomp = _run_levels_engine_update(ctx, old, dmask)
-            except _EngineAbort:
-                _drain(ctx)
-                ctx = _Ctx(fct.spec, b_new, t_new, fct.tol, fct.proxy_count, fct.proxy_factor)
-                ctx.upd_old = (fct, dmask)
-                levels = nh = None
-        if levels is None and nh is None:
-            levels, store, n_recomp = _run_levels(ctx, reuse=old, dirty=dmask)
-        got = []
-        collect = (lambda: got.append(_native_collect(ctx, nh))) if nh is not None else None
-        try:
-            with _ht("U.finish"):
-                rd, E_root, top, ipiv, UH, PsiV, UH_div, q, ratio = _finish_top(
-                    ctx, levels, store, ctx.pipe, before_sync=collect)
-        finally:
-            if nh is not None and not got:
-                nh[0].skb_drv_free(nh[1].value)
-        if nh is not None:
-            levels = got[0]
+        ctx, levels, (rd, E_root, top, ipiv, UH, PsiV, UH_div, q, ratio) = _levels_and_top(
+            make_ctx, upd=(fct, dmask), reuse=old, dirty=dmask)
     with _ht("U.final"):
         torch.cuda.synchronize()
     ctx.upd_old = None                                  # no chain of old factorizations
