@@ -6,8 +6,8 @@ Drop-in for the hot path of the reference package ``skelsolve``
 kernels of ``libskelb200.so``.
 """
 
-from .geometry import (Boundary, Curve, GeometryError, MoveHole, PerturbationReport,
-                       apply_perturbation)
+from .geometry import (AddHole, Boundary, Curve, DeleteHole, GeometryError, MoveHole,
+                       PerturbationReport, apply_perturbation)
 from .tree import Tree, TreeError, build_tree, default_root_box, proxy_radius, refit_tree
 from .skel import (BoxFactors, Factorization, LAPLACE, RootBoxExceededError, SingularPivotError, STOKES,
                    SystemSpec, evaluate_interior, factor, point_in_domain,

@@ -147,7 +147,7 @@ def circle_curve(n: int, center=(0.0, 0.0), radius: float = 1.0,
 
 
 # ---------------------------------------------------------------------------
-# perturbations (reference geometry.py:281-395, MoveHole subset + reports)
+# perturbations (reference geometry.py:281-395: MoveHole, AddHole, DeleteHole + reports)
 # ---------------------------------------------------------------------------
 @dataclass(frozen=True)
 class MoveHole:
@@ -156,9 +156,28 @@ class MoveHole:
     new_center: tuple | None = None
 
 
+@dataclass(frozen=True, eq=False)
+class AddHole:
+    """A new hole, appended after the kept curves (reference ``geometry.py:289-291``).
+    The reference discretises a ``CurveSpec`` by its spline fit; here the hole is
+    handed over discretised (a ``Curve`` from the analytic builders or from node
+    arrays), optionally re-centred."""
+    curve: Curve
+    center: tuple | None = None
+
+
+@dataclass(frozen=True)
+class DeleteHole:
+    """Remove hole ``curve_id`` (reference ``geometry.py:294-296``)."""
+    curve_id: int
+
+
 @dataclass
 class PerturbationReport:
-    """Changed nodes in old/new numbering (reference ``geometry.py:302-321``)."""
+    """Changed nodes in old/new numbering (reference ``geometry.py:302-321``):
+    ``old_to_new`` maps an old node to its new index (-1: deleted);
+    ``modified_nodes_old`` lists moved and deleted curves' nodes,
+    ``modified_nodes_new`` moved and added ones."""
 
     modified_nodes_old: np.ndarray
     modified_nodes_new: np.ndarray
@@ -189,25 +208,55 @@ def check_arrangement(b: Boundary, gap: float = 0.0):
 
 
 def apply_perturbation(b: Boundary, edits, gap: float = 0.0):
-    """Apply MoveHole edits; returns (new boundary, report)."""
+    """Apply MoveHole / DeleteHole / AddHole edits; returns (new boundary,
+    report) with the reference's node bookkeeping (``geometry.py:328-390``):
+    kept curves in their old order, added holes appended."""
+    if not edits:
+        return b, PerturbationReport(np.empty(0, np.int64), np.empty(0, np.int64),
+                                     np.arange(b.n_nodes), b.positions)
     curves = list(b.curves)
-    touched = []
+    touched, added = [], []
     for e in edits:
-        if not isinstance(e, MoveHole):
-            raise GeometryError(f"unsupported edit {e!r}")
-        if not (1 <= e.curve_id < len(curves)):
-            raise GeometryError(f"curve {e.curve_id} is not a hole")
-        cur = curves[e.curve_id]
-        if e.new_center is not None:
-            shift = np.asarray(e.new_center, float) - cur.nodes.mean(axis=0)
+        if isinstance(e, (MoveHole, DeleteHole)):
+            if not (1 <= e.curve_id < len(curves)):
+                raise GeometryError(f"curve {e.curve_id} is not a hole")
+            cur = curves[e.curve_id]
+            if cur is None:
+                raise GeometryError(f"curve {e.curve_id} already deleted")
+            if isinstance(e, DeleteHole):
+                curves[e.curve_id] = None
+            else:
+                if e.new_center is not None:
+                    shift = np.asarray(e.new_center, float) - cur.nodes.mean(axis=0)
+                else:
+                    shift = np.asarray(e.translation, float)
+                curves[e.curve_id] = cur.translated(shift)
+            touched.append(e.curve_id)
+        elif isinstance(e, AddHole):
+            c = e.curve
+            if c.orientation != HOLE:
+                raise GeometryError("an added curve must be a hole")
+            if e.center is not None:
+                c = c.translated(np.asarray(e.center, float) - c.nodes.mean(axis=0))
+            added.append(c)
         else:
-            shift = np.asarray(e.translation, float)
-        curves[e.curve_id] = cur.translated(shift)
-        touched.append(e.curve_id)
-    b_new = Boundary(curves)
+            raise GeometryError(f"unsupported edit {e!r}")
+    kept = [c for c in curves if c is not None] + added
+    b_new = Boundary(kept)
     check_arrangement(b_new, gap)
+    old_to_new = np.full(b.n_nodes, -1, dtype=np.int64)
+    pos, new_ids = 0, {}
+    for old_id, c in enumerate(curves):
+        if c is None:
+            continue
+        n = c.n_nodes
+        old_to_new[b.offsets[old_id]:b.offsets[old_id] + n] = np.arange(pos, pos + n)
+        new_ids[old_id] = len(new_ids)
+        pos += n
     mod = sorted(set(touched))
-    nodes = (np.concatenate([b.curve_nodes(c) for c in mod]) if mod
-             else np.empty(0, np.int64))
-    rep = PerturbationReport(nodes, np.sort(nodes), np.arange(b.n_nodes), b.positions)
-    return b_new, rep
+    nodes_old = (np.concatenate([b.curve_nodes(c) for c in mod]) if mod else np.empty(0, np.int64))
+    moved_new = [new_ids[c] for c in mod if curves[c] is not None]
+    added_new = list(range(len(kept) - len(added), len(kept)))
+    nodes_new = (np.concatenate([b_new.curve_nodes(c) for c in moved_new + added_new])
+                 if (moved_new or added_new) else np.empty(0, np.int64))
+    return b_new, PerturbationReport(nodes_old, np.sort(nodes_new), old_to_new, b.positions)

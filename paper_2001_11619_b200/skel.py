@@ -1505,7 +1505,7 @@ _INC_SWEEP = os.environ.get("SKB_INC_SWEEP", "1") != "0"
 
 
 def _make_pipe(ctx: "_Ctx"):
-    upd = getattr(ctx, "upd_old", None) if _INC_SWEEP else None
+    upd = getattr(ctx, "upd_old", None) if (_INC_SWEEP and getattr(ctx, "upd_inc", True)) else None
     return _AugPipeUpdate(ctx, *upd) if upd is not None else _AugPipe(ctx)
 
 
@@ -1980,8 +1980,8 @@ def _run_levels_native(ctx: _Ctx, upd=None):
     eupd = None
     table = None
     if upd is not None:
-        old_fct, dmask = upd
-        old = {L.lev: L for L in old_fct.levels}
+        old_fct, dmask = upd[0], upd[1]
+        old = upd[2] if len(upd) > 2 else {L.lev: L for L in old_fct.levels}
         with _ht("N.table"):
             table = np.zeros((max(t.depth, max(old, default=0)) + 1, _O_NF), np.int64)
             for lev, L in old.items():
@@ -2342,6 +2342,31 @@ def _drain(ctx: "_Ctx"):
     torch.cuda.current_stream().wait_stream(ctx.sstream)
 
 
+def _remap_old_levels(fct: "Factorization", old_to_new, dpn: int) -> dict:
+    """Level views of the previous factorization in the NEW DOF numbering
+    (reference BoxFactors.remapped, skel.py:82-85, with the dof_map of
+    skel.py:493-498): index arrays are remapped copies, matrices are shared.
+    Boxes that held deleted nodes carry -1 entries; the ownership rule makes
+    them dirty, so they are never reused."""
+    import copy
+    o2n = np.asarray(old_to_new, np.int64)
+    dof_map = np.full(dpn * len(o2n), -1, np.int64)
+    valid = np.flatnonzero(o2n >= 0)
+    for c in range(dpn):
+        dof_map[dpn * valid + c] = dpn * o2n[valid] + c
+    out = {}
+    for L in fct.levels:
+        L.batch.resolve()
+        L2, bt2 = copy.copy(L), copy.copy(L.batch)
+        bt2.act = dof_map[np.asarray(L.batch.act, np.int64)]
+        L2.batch = bt2
+        L2.__dict__.pop("_row", None)
+        L2.__dict__.pop("_row_keep", None)
+        _level_code(L2)
+        out[L.lev] = L2
+    return out
+
+
 def _levels_and_top(make_ctx, upd=None, reuse=None, dirty=None):
     """Level loop and _finish_top: the native engine + driver first; a migration
     (R -> S, skel.py:317-330) or a clean box without a twin aborts that run and
@@ -2423,20 +2448,28 @@ def update(fct: Factorization, b_new, report, workers: int = 1) -> Factorization
         raise RootBoxExceededError("perturbed node escaped the root box; refactor with a fresh tree") from e
     with _ht("U.dirty"):
         dmask = dirty_mask(fct.tree, t_new, b_new, report, fct.proxy_factor)
-    if not np.array_equal(report.old_to_new, np.arange(len(report.old_to_new))):
-        raise NotImplementedError("only DOF-preserving edits (hole moves) are supported")
-    old = {L.lev: L for L in fct.levels}
+    o2n = np.asarray(report.old_to_new, np.int64)
+    same_dofs = len(o2n) == b_new.n_nodes and np.array_equal(o2n, np.arange(len(o2n)))
+    if same_dofs:
+        old = {L.lev: L for L in fct.levels}
+    else:
+        # AddHole / DeleteHole (reference skel.py:493-498): clean boxes are reused
+        # with remapped DOF lists; the augmentation block changes its size, so the
+        # sweep is the full one
+        with _ht("U.remap"):
+            old = _remap_old_levels(fct, o2n, fct.spec.dof_per_node)
 
     def make_ctx():
         ctx = _Ctx(fct.spec, b_new, t_new, fct.tol, fct.proxy_count, fct.proxy_factor)
         ctx.upd_old = (fct, dmask)
+        ctx.upd_inc = same_dofs
         ctx.g                                           # geometry upload
         torch.cuda.current_stream().synchronize()
         return ctx
 
     with torch.cuda.stream(_compress_stream()):
         ctx, levels, (rd, E_root, top, ipiv, UH, PsiV, UH_div, q, ratio) = _levels_and_top(
-            make_ctx, upd=(fct, dmask), reuse=old, dirty=dmask)
+            make_ctx, upd=(fct, dmask, old), reuse=old, dirty=dmask)
     with _ht("U.final"):
         torch.cuda.synchronize()
     ctx.upd_old = None                                  # no chain of old factorizations

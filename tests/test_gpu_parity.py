@@ -430,3 +430,45 @@ def test_box_factors_lu_view():
     assert lu.n == X.shape[0] and lu.piv.shape == (X.shape[0],)
     assert np.abs(lu.solve(X) - np.eye(lu.n)).max() < 1e-10
     assert 0 < lu.pivot_ratio <= 1
+
+
+def test_add_and_delete_hole_updates(monkeypatch):
+    """Non-DOF-preserving edits (reference skel.py:493-498, BoxFactors.remapped):
+    update() after DeleteHole / AddHole marks the reference's dirty set, solves
+    within 10 eps of the reference's updated factorization (fixtures recorded from
+    the unmodified reference, tests/golden/make_golden_edits.py) and equals a GPU
+    refactorization of the new geometry bitwise -- on the native driver and on the
+    Python level loop; a hole move chained after the edit stays incremental."""
+    import os
+    from paper_2001_11619_b200.geometry import AddHole, Curve, DeleteHole, HOLE
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "reference_golden_edits.npz"))
+    wl = configs.mini_holes()
+    b = wl.boundary
+    nodes = g["add_nodes"]
+    rad = float(np.sqrt(((nodes - nodes.mean(axis=0)) ** 2).sum(axis=1)).max())
+    hole = Curve(nodes, g["add_weights"], g["add_normals"], g["add_curvatures"], HOLE, rad)
+    cases = (("del", [DeleteHole(2)]), ("add", [AddHole(hole)]))
+    for engine in (True, False):
+        monkeypatch.setattr(skel, "_ENGINE_ON", engine)
+        f = _factor(wl)
+        for name, edits in cases:
+            nb, rep = apply_perturbation(b, edits)
+            fu = update(f, nb, rep)
+            want = {tuple(int(v) for v in k) for k in g[f"{name}_dirty"]}
+            assert fu.stats["dirty"] == want, (engine, name)
+            rhs = g[f"{name}_rhs"]
+            assert fu.dim == len(rhs)
+            x = fu.solve(rhs)
+            assert _rel(x, g[f"{name}_x"]) <= 10 * wl.tol, (engine, name, _rel(x, g[f"{name}_x"]))
+            t2 = build_tree(nb.positions, wl.leaf_cap, root_box=(f.tree.root_center, f.tree.root_half_width))
+            fr = factor(SystemSpec(), nb, t2, wl.tol, proxy_count=wl.proxy_count, proxy_factor=wl.proxy_factor)
+            assert set(fu.factors.keys()) == set(fr.factors.keys())
+            for k in fr.factors.keys():
+                assert np.array_equal(fu.factors[k].skel_dofs, fr.factors[k].skel_dofs), (engine, name, k)
+            assert np.array_equal(x, fr.solve(rhs)), (engine, name)
+            # a hole move on top of the edited factorization (incremental sweep again)
+            nb2, rep2 = apply_perturbation(nb, [MoveHole(1, translation=(0.04, -0.03))])
+            fu2 = update(fu, nb2, rep2)
+            t3 = build_tree(nb2.positions, wl.leaf_cap, root_box=(f.tree.root_center, f.tree.root_half_width))
+            fr2 = factor(SystemSpec(), nb2, t3, wl.tol, proxy_count=wl.proxy_count, proxy_factor=wl.proxy_factor)
+            assert np.array_equal(fu2.solve(rhs), fr2.solve(rhs)), (engine, name, "move after edit")

@@ -146,3 +146,35 @@ def test_native_leaf_actives_match_numpy():
             assert a.fill == r.fill
             assert np.array_equal(a.big[:a.fill], r.big[:r.fill])
             assert np.array_equal(a.a_start, r.a_start) and np.array_equal(a.a_len, r.a_len)
+
+
+def _edit_cases():
+    """(name, new boundary, report) for the DeleteHole / AddHole fixtures recorded
+    from the reference (tests/golden/make_golden_edits.py)."""
+    import os
+    from paper_2001_11619_b200.geometry import AddHole, Curve, DeleteHole, HOLE
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "reference_golden_edits.npz"))
+    b = configs.mini_holes().boundary
+    nb_d, rep_d = apply_perturbation(b, [DeleteHole(2)])
+    nodes = g["add_nodes"]
+    rad = float(np.sqrt(((nodes - nodes.mean(axis=0)) ** 2).sum(axis=1)).max())
+    hole = Curve(nodes, g["add_weights"], g["add_normals"], g["add_curvatures"], HOLE, rad)
+    nb_a, rep_a = apply_perturbation(b, [AddHole(hole)])
+    return g, b, (("del", nb_d, rep_d), ("add", nb_a, rep_a))
+
+
+def test_add_delete_hole_reports_and_dirty_sets_match_reference():
+    """Non-DOF-preserving edits: node map, modified-node lists and the dirty set
+    (reference geometry.py:328-390, skel.py:476-491) equal the reference's."""
+    g, b, cases = _edit_cases()
+    wl = configs.mini_holes()
+    t_old = build_tree(b.positions, wl.leaf_cap)
+    assert np.array_equal(cases[1][1].positions, g["add_positions"])
+    assert np.array_equal(cases[1][1].hole_centers, g["add_hole_centers"])
+    for name, nb, rep in cases:
+        assert np.array_equal(rep.old_to_new, g[f"{name}_old_to_new"])
+        assert np.array_equal(rep.modified_nodes_old, g[f"{name}_mod_old"])
+        assert np.array_equal(rep.modified_nodes_new, g[f"{name}_mod_new"])
+        t_new = refit_tree(t_old, nb.positions)
+        want = {tuple(int(v) for v in k) for k in g[f"{name}_dirty"]}
+        assert dirty_set(t_old, t_new, nb, rep, wl.proxy_factor) == want
