@@ -686,9 +686,11 @@ class OracleFactorization:
 class _Pass:
     """State of one factor pass (skel.py:227-361)."""
 
-    def __init__(self, g, tree, tol, count, factor, pde=STOKES):
+    def __init__(self, g, tree, tol, count, factor, pde=STOKES, propagate_zeros=False):
         self.g, self.tree, self.tol, self.count, self.factor = g, tree, tol, count, factor
         self.pde = pde
+        self.propagate_zeros = propagate_zeros          # skel.py:267-270, 354-361
+        self.done = set()
         self.dpn = dpn(pde)
         self.dof_xy = np.repeat(g.positions, self.dpn, axis=0)        # skel.py:233
         self.active = {}
@@ -702,7 +704,8 @@ class _Pass:
     def far(self, bx):
         """skel.py:258-280 (first tuple element)."""
         rp = proxy_radius(bx.hw, self.factor)
-        parts = [self.active[k] for k in self.tree.neighbours(bx.key)]
+        parts = [self.out[k].skel if (self.propagate_zeros and k in self.done) else self.active[k]
+                 for k in self.tree.neighbours(bx.key)]
         parts += [self.active[k] for k in self.tree.coarse_leaves(bx.center, rp, bx.key[0])]
         if not parts:
             return np.empty(0, dtype=np.int64)
@@ -767,13 +770,14 @@ class _Pass:
             for k in keys:
                 if reuse is not None and k not in dirty:
                     self.out[k] = reuse[k]
-            if workers > 1 and len(todo) > 1:
+            if workers > 1 and len(todo) > 1 and not self.propagate_zeros:
                 with ThreadPoolExecutor(max_workers=workers) as ex:
                     for k, r in zip(todo, ex.map(self.compress, todo)):
                         self.out[k] = r
             else:
                 for k in todo:
                     self.out[k] = self.compress(k)
+                    self.done.add(k)
             sweep.append((lev, keys))
         return sweep
 
@@ -839,11 +843,12 @@ class _Pass:
                                    {"k_per_level": kpl, "root_size": len(rd), "pde": self.pde})
 
 
-def factor(g, tree, tol, proxy_count=64, proxy_factor=1.5, workers=1, record=None, pde=STOKES):
+def factor(g, tree, tol, proxy_count=64, proxy_factor=1.5, workers=1, record=None, pde=STOKES,
+           propagate_zeros=False):
     """skel.py:428-453."""
     t0 = time.perf_counter()
     with threadpool_limits(limits=1):          # skel.py:441
-        p = _Pass(g, tree, tol, proxy_count, proxy_factor, pde)
+        p = _Pass(g, tree, tol, proxy_count, proxy_factor, pde, propagate_zeros)
         p.record = record
         sweep = p.run(workers)
         f = p.top(sweep, workers)
@@ -951,8 +956,9 @@ def update(fct, b_new, report, workers=1):
     return f
 
 
-def factor_full(g, leaf_cap, tol, proxy_count, proxy_factor, workers=1, record=None, pde=STOKES):
+def factor_full(g, leaf_cap, tol, proxy_count, proxy_factor, workers=1, record=None, pde=STOKES,
+                propagate_zeros=False):
     t = QTree(g.positions, leaf_cap)
-    f = factor(g, t, tol, proxy_count, proxy_factor, workers, record, pde)
+    f = factor(g, t, tol, proxy_count, proxy_factor, workers, record, pde, propagate_zeros)
     f.proxy_count, f.proxy_factor = proxy_count, proxy_factor
     return f

@@ -2297,6 +2297,45 @@ def _run_levels(ctx: _Ctx, reuse=None, dirty=None):
     return levels, store, n_recomp
 
 
+def _run_levels_pz(ctx: _Ctx):
+    """Level loop of the validation mode ``propagate_zeros=True`` (reference
+    skel.py:267-270, 354-361): the boxes of a level are compressed one after
+    the other in key order, and a box's far field sees the SKELETONS of the
+    colleagues compressed before it (the zeros they created) instead of their
+    active sets.  Sequential by construction: one box per launch."""
+    t = ctx.t
+    store = ActStore(t, dpn=ctx.dpn)
+    ctx.store = store
+    pairs = t.hole_pairs(np.asarray(ctx.b.offsets, np.int64)) if ctx.b.n_holes else None
+    pipe = _make_pipe(ctx)
+    ctx.pipe = pipe
+    levels = []
+    n = 0
+    for lev in range(t.depth, 0, -1):
+        idx = t.level_indices(lev)
+        store.set_internal(t, idx)                    # assign_internal_actives, skel.py:251-256
+        act_off, act = store.acts(idx)                # the boxes' own active sets (before any substitution)
+        bt = BoxBatch(idx, act_off, act)
+        one = np.zeros(1, np.int64)
+        for j, i in enumerate(idx):
+            sub = ctx.compress(np.array([i], np.int64), store)
+            ctx.migrate(sub, store)                   # R -> S migration, skel.py:317-330
+            bt.take(np.array([j], np.int64), sub, one)
+            store.set_skel(sub.idx, sub.act_off, sub.act, sub.perm, sub.k)
+            # colleagues compressed after this box see its skeleton only
+            store.a_start[i], store.a_len[i] = store.s_start[i], store.s_len[i]
+            n += 1
+        bt.resolve()
+        store.xss[bt.idx] = bt.ptr["Xss"]
+        if levels:
+            pipe.submit(levels[-1])
+        levels.append(LevelFactors(lev, t, bt, *_hole_columns(t, ctx.b, bt.idx, pairs)))
+    if levels:
+        pipe.submit(levels[-1])
+    torch.cuda.current_stream().wait_stream(ctx.sstream)
+    return levels, store, n
+
+
 def _merge_level(ctx, idx, store, todo, bt_new, old_levels):
     """Level batch for an update: dirty boxes from bt_new, clean boxes share the
     old factor memory (reference run_level reuse path, skel.py:342-353)."""
@@ -2414,16 +2453,21 @@ def factor(spec, b, t: Tree, tol: float, workers: int = 1,
     """Build the skeletonization factorization on the GPU (reference skel.py:428-453).
 
     ``workers`` is accepted for signature parity (the GPU batches every box of a
-    level); ``propagate_zeros`` (a sequential validation mode) is not supported.
+    level).  ``propagate_zeros=True`` is the reference's sequential validation
+    mode (one box per launch, far fields thinned by the zeros of the boxes
+    compressed before; skel.py:267-270): slow by design.
     """
-    if propagate_zeros:
-        raise NotImplementedError("propagate_zeros is a sequential CPU validation mode")
     torch.cuda.synchronize()
     _DevSlab.flush()
     t0 = time.perf_counter()
     with torch.cuda.stream(_compress_stream()):
-        ctx, levels, (rd, E_root, top, ipiv, UH, PsiV, UH_div, q, ratio) = _levels_and_top(
-            lambda: _Ctx(spec, b, t, tol, proxy_count, proxy_factor))
+        if propagate_zeros:
+            ctx = _Ctx(spec, b, t, tol, proxy_count, proxy_factor)
+            levels, store, _ = _run_levels_pz(ctx)
+            rd, E_root, top, ipiv, UH, PsiV, UH_div, q, ratio = _finish_top(ctx, levels, store, ctx.pipe)
+        else:
+            ctx, levels, (rd, E_root, top, ipiv, UH, PsiV, UH_div, q, ratio) = _levels_and_top(
+                lambda: _Ctx(spec, b, t, tol, proxy_count, proxy_factor))
     with _ht("final_sync"):
         torch.cuda.synchronize()
     stats = {"k_per_level": {L.lev: int(L.k.max(initial=0)) for L in levels},

@@ -83,6 +83,21 @@ def main():
     out["add_rhs"], out["add_x"] = rhs, fu.solve(rhs)
     out["add_positions"] = b_add.positions
     out["add_hole_centers"] = b_add.hole_centers
+    # (c) the sequential validation mode propagate_zeros=True (skel.py:267-270, 354-361)
+    for nm, w in (("pzm", configs.mini_holes()), ("pz1", configs.cfg1())):
+        rb = to_ref_boundary(s, w.boundary)
+        tr = s.build_tree(rb.positions, leaf_cap=w.leaf_cap)
+        fz = s.factor(spec, rb, tr, w.tol, proxy_count=w.proxy_count, proxy_factor=w.proxy_factor,
+                      propagate_zeros=True)
+        keys = sorted(fz.factors)
+        out[nm + "_keys"] = np.array(keys, dtype=np.int64)
+        sk_all = [np.asarray(fz.factors[k].skel_dofs) for k in keys]
+        out[nm + "_skel_off"] = np.concatenate([[0], np.cumsum([len(x) for x in sk_all])]).astype(np.int64)
+        out[nm + "_skel"] = np.concatenate(sk_all).astype(np.int64)
+        out[nm + "_x"] = fz.solve(w.extra["rhs"])
+        f0 = s.factor(spec, rb, tr, w.tol, proxy_count=w.proxy_count, proxy_factor=w.proxy_factor)
+        ndiff = sum(len(fz.factors[k].S_loc) != len(f0.factors[k].S_loc) for k in keys)
+        print(nm, "propagate_zeros: boxes with a different rank than the default mode:", ndiff, "of", len(keys))
     print("delete: dirty", len(out["del_dirty"]), "add: dirty", len(out["add_dirty"]),
           "update vs refactor (reference, delete)",
           np.linalg.norm(out["del_x"] - out["del_x_refactor"]) / np.linalg.norm(out["del_x"]))

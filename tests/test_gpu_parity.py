@@ -472,3 +472,26 @@ def test_add_and_delete_hole_updates(monkeypatch):
             t3 = build_tree(nb2.positions, wl.leaf_cap, root_box=(f.tree.root_center, f.tree.root_half_width))
             fr2 = factor(SystemSpec(), nb2, t3, wl.tol, proxy_count=wl.proxy_count, proxy_factor=wl.proxy_factor)
             assert np.array_equal(fu2.solve(rhs), fr2.solve(rhs)), (engine, name, "move after edit")
+
+
+@pytest.mark.parametrize("nm,builder", [("pzm", configs.mini_holes), ("pz1", configs.cfg1)])
+def test_propagate_zeros_mode_vs_reference(nm, builder):
+    """factor(propagate_zeros=True), the reference's sequential validation mode
+    (skel.py:267-270, 354-361): skeletons identical to the reference's box for box
+    (fixtures recorded from the unmodified reference) and the solve within 10 eps;
+    it differs from the default mode on some boxes, so the mode is exercised."""
+    import os
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "reference_golden_edits.npz"))
+    wl = builder()
+    b = wl.boundary
+    t = build_tree(b.positions, wl.leaf_cap)
+    f = factor(SystemSpec(), b, t, wl.tol, proxy_count=wl.proxy_count, proxy_factor=wl.proxy_factor,
+               propagate_zeros=True)
+    keys = [tuple(int(v) for v in k) for k in g[nm + "_keys"]]
+    off = g[nm + "_skel_off"]
+    assert set(keys) == set(f.factors.keys())
+    for i, k in enumerate(keys):
+        assert np.array_equal(f.factors[k].skel_dofs, g[nm + "_skel"][off[i]:off[i + 1]]), k
+    assert _rel(f.solve(wl.extra["rhs"]), g[nm + "_x"]) <= 10 * wl.tol
+    f0 = _factor(wl)
+    assert any(len(f.factors[k].skel_dofs) != len(f0.factors[k].skel_dofs) for k in keys)

@@ -129,3 +129,20 @@ def test_oracle_unphased_cfg2_vs_reference(golden):
     for i, k in enumerate(keys):
         assert np.array_equal(f.boxes[k].S, S[so[i]:so[i + 1]]), k
     assert np.array_equal(f.solve(wl.extra["rhs"]), golden["cfg2u_x"])
+
+
+@pytest.mark.parametrize("nm,builder", [("pzm", configs.mini_holes), ("pz1", configs.cfg1)])
+def test_oracle_propagate_zeros_matches_reference(nm, builder):
+    """propagate_zeros=True (skel.py:267-270, 354-361): the oracle's sequential
+    mode picks the reference's skeletons box for box and solves to its bits."""
+    import os
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "reference_golden_edits.npz"))
+    wl = builder()
+    f = O.factor_full(wl.boundary, wl.leaf_cap, wl.tol, wl.proxy_count, wl.proxy_factor,
+                      propagate_zeros=True)
+    keys = [tuple(int(v) for v in k) for k in g[nm + "_keys"]]
+    off = g[nm + "_skel_off"]
+    assert set(keys) == set(f.boxes)
+    for i, k in enumerate(keys):
+        assert np.array_equal(f.boxes[k].skel, g[nm + "_skel"][off[i]:off[i + 1]]), k
+    assert np.array_equal(f.solve(wl.extra["rhs"]), g[nm + "_x"])
