@@ -69,6 +69,7 @@ struct PinnedRing {
   uint64_t lap = 1;
   Slot slot[kSlots];
   std::vector<cudaEvent_t> pool;
+  std::mutex mu;                 // per ring: a wait on a lap wrap never blocks the other thread's ring
 };
 PinnedRing& ring();
 // host-side state shared by the Python thread and the native level engine
@@ -83,8 +84,8 @@ inline int pool_strict(cudaMemPool_t pool) {
 }
 
 inline int ring_stage(const void* host, size_t bytes, cudaStream_t s, void* dev) {
-  std::lock_guard<std::recursive_mutex> lk(host_mutex());
   PinnedRing& R = ring();
+  std::lock_guard<std::mutex> lk(R.mu);
   if (!R.base) {
     // keep stream-ordered allocations cached in the pool across synchronisations
     int dev = 0;
