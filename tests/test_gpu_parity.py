@@ -495,3 +495,41 @@ def test_propagate_zeros_mode_vs_reference(nm, builder):
     assert _rel(f.solve(wl.extra["rhs"]), g[nm + "_x"]) <= 10 * wl.tol
     f0 = _factor(wl)
     assert any(len(f.factors[k].skel_dofs) != len(f0.factors[k].skel_dofs) for k in keys)
+
+
+def test_mixed_edit_chain_equals_refactor():
+    """A chain of mixed edits on the 3-hole case (moves, a deletion, additions, a
+    deletion of an added hole): every updated factorization has the skeletons and
+    the solve of a GPU refactorization of the same geometry, bitwise, and the
+    augmentation block follows the hole count."""
+    from paper_2001_11619_b200.geometry import AddHole, DeleteHole, GeometryError, circle_curve, ellipse_curve
+    wl = configs.mini_holes()
+    b = wl.boundary
+    f = _factor(wl)
+    root = (f.tree.root_center, f.tree.root_half_width)
+    rng = np.random.default_rng(17)
+    script = [
+        [MoveHole(1, translation=(0.05, 0.02))],
+        [DeleteHole(2)],
+        [AddHole(circle_curve(160, center=(-1.3, -1.0), radius=0.3, clockwise=True))],
+        [MoveHole(3, translation=(0.03, 0.04)), MoveHole(1, translation=(-0.02, 0.01))],
+        [AddHole(circle_curve(128, center=(1.2, 1.3), radius=0.25, clockwise=True)), DeleteHole(1)],
+        [MoveHole(2, translation=(0.0, -0.05))],
+        [DeleteHole(3)],
+    ]
+    cur, cb = f, b
+    for step, edits in enumerate(script):
+        nb, rep = apply_perturbation(cb, edits)
+        cur = update(cur, nb, rep)
+        assert cur.n_aug == 3 * nb.n_holes and cur.dim == 2 * nb.n_nodes + 3 * nb.n_holes
+        t2 = build_tree(nb.positions, wl.leaf_cap, root_box=root)
+        fr = factor(SystemSpec(), nb, t2, wl.tol, proxy_count=wl.proxy_count, proxy_factor=wl.proxy_factor)
+        rhs = np.concatenate([rng.standard_normal(2 * nb.n_nodes), np.zeros(3 * nb.n_holes)])
+        assert set(cur.factors.keys()) == set(fr.factors.keys()), step
+        for k in fr.factors.keys():
+            assert np.array_equal(cur.factors[k].skel_dofs, fr.factors[k].skel_dofs), (step, k)
+        assert np.array_equal(cur.solve(rhs), fr.solve(rhs)), step
+        y = np.random.default_rng(step).standard_normal(cur.dim)
+        assert np.array_equal(cur.apply(y), fr.apply(y)), step
+        cb = nb
+        del fr
