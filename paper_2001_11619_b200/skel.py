@@ -1708,11 +1708,6 @@ def _aug_level(L: LevelFactors, UH, PsiV, UH_div, schur, q):
 _ENGINE_ON = os.environ.get("SKB_ENGINE", "1") != "0"
 
 
-# Experiment: acknowledge a level as soon as its QRCP results arrive (the engine
-# enqueues the next level's kernels while this thread enqueues the Schur stage).
-_ACK_EARLY = os.environ.get("SKB_ACK_EARLY", "0") != "0"
-
-
 class _EngineAbort(Exception):
     """A migration (R -> S, skel.py:317-330) was detected while the native
     engine runs ahead: the factorization restarts on the Python level path."""
@@ -2157,8 +2152,6 @@ def _engine_loop(ctx, eng, store, reuse=None, dirty=None):
             h = eng.wait(lev)
             bt_new = None
             if h is not None:
-                if _ACK_EARLY:
-                    eng.lib.skb_engine_ack(eng.h, lev)
                 bt_new = BoxBatch(h["idx"], h["act_off"], h["act"])
                 bt_new.perm[:] = h["perm"]
                 bt_new.k[:] = h["k"]
