@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libskelb200.so")
+LIB_PATH = os.environ.get("SKB_LIB") or os.path.join(_HERE, "libskelb200.so")   # SKB_LIB: A/B builds
 
 GEMM_DT = np.dtype([("A", "u8"), ("B", "u8"), ("C", "u8"), ("D", "u8"),
                     ("m", "i8"), ("n", "i8"), ("k", "i8"),
