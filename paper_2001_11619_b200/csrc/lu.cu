@@ -799,17 +799,50 @@ __global__ void k_ipiv_perm(const SwapDesc* __restrict__ descs, int32_t* __restr
   }
 }
 
+// The same composition with ipiv and the permutation in shared memory (one
+// warp per matrix; lane 0 walks the interchanges): ~50 ns per interchange
+// instead of a global-memory round trip (the 2532-row corner: 0.8 -> 0.15 ms).
+__global__ void k_ipiv_perm_smem(const SwapDesc* __restrict__ descs, int32_t* __restrict__ perm,
+                                 const int64_t* __restrict__ poff) {
+  extern __shared__ int32_t sp[];
+  const SwapDesc D = descs[blockIdx.x];
+  const int n = (int)D.n;
+  int32_t* piv = sp;
+  int32_t* p = sp + n;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) { piv[i] = D.ipiv[i]; p[i] = i; }
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int i = 0; i < n; ++i) {
+      const int q = piv[i];
+      if (q != i) { const int32_t t = p[i]; p[i] = p[q]; p[q] = t; }
+    }
+  __syncthreads();
+  int32_t* out = perm + poff[blockIdx.x];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = p[i];
+}
+
+// rows of a matrix over the blocks (x), consecutive threads on consecutive columns
 __global__ void k_perm_rows(const SwapDesc* __restrict__ descs, const int32_t* __restrict__ perm,
                             const int64_t* __restrict__ poff, double* __restrict__ tmp,
                             const int64_t* __restrict__ toff, int phase) {
   const SwapDesc D = descs[blockIdx.y];
   const int32_t* p = perm + poff[blockIdx.y];
   double* t = tmp + toff[blockIdx.y];
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < D.n * D.ncols;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = e / D.ncols, c = e - i * D.ncols;
-    if (phase == 0) t[e] = D.B[(int64_t)p[i] * D.ld + c];
-    else D.B[i * D.ld + c] = t[e];
+  const int n = (int)D.n, nc = (int)D.ncols;
+  const int tpr = nc > 128 ? 256 : (nc > 64 ? 128 : (nc > 32 ? 64 : 32)), rps = 256 / tpr;
+  const int tr = threadIdx.x / tpr, tc = threadIdx.x - tr * tpr;
+  for (int i = blockIdx.x * rps + tr; i < n; i += gridDim.x * rps) {
+    const int src = p[i];
+    if (src == i) continue;                       // unmoved row: nothing to do in either phase
+    if (phase == 0) {
+      const double* sp_ = D.B + (int64_t)src * D.ld;
+      double* dp = t + (int64_t)i * nc;
+      for (int c = tc; c < nc; c += tpr) dp[c] = sp_[c];
+    } else {
+      const double* sp_ = t + (int64_t)i * nc;
+      double* dp = D.B + (int64_t)i * D.ld;
+      for (int c = tc; c < nc; c += tpr) dp[c] = sp_[c];
+    }
   }
 }
 
@@ -909,8 +942,14 @@ int getrs_batched(int64_t nbox, const SkbMat* lu, const int64_t* ipiv, const Skb
   }
   if (sd.empty()) return 0;
   int rc = 0;
-  if (max_c <= 8) {
-    // narrow: permutation gather
+  int64_t max_rows = 0;
+  for (const SwapDesc& q : sd) max_rows = std::max(max_rows, q.n);
+  // SKB_IPIV_PERM_MIN: tall matrices (the corner, top-level boxes) also go
+  // through the composed permutation (pure data movement: same bits)
+  static const int64_t perm_min = getenv("SKB_IPIV_PERM_MIN") ? atoll(getenv("SKB_IPIV_PERM_MIN")) : 512;
+  const bool smem_perm = max_rows <= 5500;
+  if (max_c <= 8 || (max_rows >= perm_min && smem_perm)) {
+    // narrow or tall: permutation gather
     std::vector<int64_t> poff(sd.size()), toff(sd.size());
     int64_t pt = 0, tt = 0, maxe = 0;
     for (size_t i = 0; i < sd.size(); ++i) {
@@ -931,10 +970,13 @@ int getrs_batched(int64_t nbox, const SkbMat* lu, const int64_t* ipiv, const Skb
       ProfScope ps(F_TRSM, s);
       const int64_t nbx = (int64_t)sd.size();
       // one thread per matrix (exact multiple of the block via guard-free launch of 1-thread blocks)
-      k_ipiv_perm<<<(unsigned)nbx, 1, 0, s>>>(d, perm, dpo);
+      if (smem_perm && nbx <= 65535)
+        k_ipiv_perm_smem<<<(unsigned)nbx, 128, sizeof(int32_t) * 2 * (size_t)max_rows, s>>>(d, perm, dpo);
+      else
+        k_ipiv_perm<<<(unsigned)nbx, 1, 0, s>>>(d, perm, dpo);
       for (int64_t b0 = 0; b0 < nbx; b0 += 65535) {
         const int64_t nb = std::min<int64_t>(65535, nbx - b0);
-        dim3 grid(grid_cap((maxe + 255) / 256, 64), (unsigned)nb);
+        dim3 grid(grid_cap(max_rows, nb > 64 ? 64 : 1024), (unsigned)nb);
         k_perm_rows<<<grid, 256, 0, s>>>(d + b0, perm, dpo + b0, tmp, dto + b0, 0);
         k_perm_rows<<<grid, 256, 0, s>>>(d + b0, perm, dpo + b0, tmp, dto + b0, 1);
       }
